@@ -1,0 +1,147 @@
+/*
+ * oz2.h -- C ABI of liboz2.so: FP64 matrix multiplication C = AB emulated by
+ * Ozaki scheme II on the INT8 tensor cores of NVIDIA B200 (sm_100a).
+ *
+ * Method: Algorithm 1 of Ozaki, Uchino, Imamura, "Ozaki Scheme II: A
+ * GEMM-oriented emulation of floating-point matrix multiplication using an
+ * integer modular technique" (arXiv 2504.08009), with the
+ * OS II-fast scaling rule.  Citations "PAPER.md:L" are lines
+ * of the paper's LaTeX source; readings R1..R17 are listed in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Matrices are ROW-MAJOR with a leading dimension in elements: A is m x k
+ *    (lda >= k), B is k x n (ldb >= n), C is m x n (ldc >= n).
+ *    writes A in F^{p x q}, B in F^{q x r}; here m = p, k = q, n = r.  For
+ *    column-major (BLAS) semantics call with (n, m, k, B, ldb, A, lda, C, ldc).
+ *  - Every matrix / vector pointer is a DEVICE pointer owned by the caller,
+ *    except in oz2_dgemm_host (host pointers).  The library never frees
+ *    caller memory.
+ *  - Calls are ASYNCHRONOUS on the handle's stream (oz2_set_stream; default
+ *    the legacy default stream) except oz2_dgemm_host, which synchronises.
+ *    No call synchronises the device.  A handle may not be used by two host
+ *    threads at once; distinct handles are independent.
+ *  - num_moduli N must be in [2, 20]; the moduli are the first N entries of
+ *    (256, 255, 253, 251, 247, 239, 233, 229, 227, 223, 217, 211, 199, 197,
+ *    193, 191, 241, 181, 179, 173): Eq. (18) for N <= 16,
+ *    then reading R1.
+ *  - k must be < 2^17 so that every int32 product is exact.
+ *  - Rows of A / columns of B holding Inf or NaN give exponent
+ *    OZ2_EXP_NONFINITE and NaN in the corresponding row / column of C
+ *    (reading R13; the paper assumes finite data).
+ *  - Return value: OZ2_OK or an OZ2_ERR_* code; oz2_strerror() describes it.
+ *    On error nothing has been launched (argument errors) or the CUDA error
+ *    is reported (OZ2_ERR_CUDA) and the outputs are undefined.
+ */
+#ifndef OZ2_H
+#define OZ2_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OZ2_OK 0
+#define OZ2_ERR_INVALID_ARG 1   /* negative size, ld too small, NULL, bad mode */
+#define OZ2_ERR_NUM_MODULI 2    /* N outside [2, 20] */
+#define OZ2_ERR_K_TOO_LARGE 3   /* k >= 2^17 */
+#define OZ2_ERR_BUDGET 4        /* EQ17 mode: Eq. (17) gives k_A < 1 */
+#define OZ2_ERR_CUDA 5          /* a CUDA runtime / driver call failed */
+#define OZ2_ERR_NO_DEVICE 6     /* no sm_100 device */
+#define OZ2_ERR_WORKSPACE 7     /* caller workspace too small */
+
+#define OZ2_MODE_FAST 0   /* OS II-fast: Cauchy-Schwarz bound, reading R4 */
+#define OZ2_MODE_EQ17 1   /* Eqs. (15)-(17): k_A = k_B = floor(log2((M/2-1)/q)/2) */
+
+#define OZ2_EXP_NONFINITE INT32_MIN
+
+typedef struct oz2_context* oz2_handle_t;
+
+/* ---- handle -------------------------------------------------------------- */
+/* Create a handle bound to CUDA device `device` (mode FAST, legacy stream,
+ * library-managed workspace).  *h receives the handle. */
+int oz2_create(oz2_handle_t* h, int device);
+/* Destroy a handle; frees its library-managed workspace.  Does not synchronise
+ * the stream: the caller must not destroy a handle with work in flight. */
+int oz2_destroy(oz2_handle_t h);
+/* Subsequent calls launch on `stream` (a cudaStream_t; NULL = legacy). */
+int oz2_set_stream(oz2_handle_t h, void* stream);
+/* OZ2_MODE_FAST (default) or OZ2_MODE_EQ17: the rule for Alg. 1 line 1. */
+int oz2_set_mode(oz2_handle_t h, int mode);
+/* Use caller-owned device memory [ptr, ptr+bytes) as workspace (NULL, 0 =
+ * library-managed, grown on demand with cudaMalloc).  Must stay valid and
+ * unused by others while calls on this handle are in flight. */
+int oz2_set_workspace(oz2_handle_t h, void* ptr, size_t bytes);
+/* Workspace bytes oz2_dgemm_ex needs for (m, n, k, N). */
+size_t oz2_workspace_bytes(int64_t m, int64_t n, int64_t k, int num_moduli);
+
+/* ---- main entry points ---------------------------------------------------- */
+/* C := fl(A B) by Algorithm 1: all stages on the GPU.
+ * Uses a per-device default handle (mode FAST, legacy stream).
+ * m, n, k >= 0; k == 0 gives C = 0. */
+int oz2_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+              const double* B, int64_t ldb, double* C, int64_t ldc, int num_moduli);
+/* Same, on handle h (its stream, mode and workspace). */
+int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A,
+                 int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                 int num_moduli);
+/* End-to-end variant with HOST buffers: copies A and B to the device, runs
+ * oz2_dgemm_ex, copies C back and synchronises the handle's stream.  For full
+ * copy bandwidth the host buffers should be page-locked. */
+int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A,
+                   int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                   int num_moduli);
+
+/* ---- split API: each stage of Algorithm 1 on its own (stage parity) ------- */
+/* Alg. 1 line 1 for the rows of A (m x k): e[i] such that D = diag(2^e[i])
+ * (reading R4 / R5 by the handle's mode).  e: int32[m]. */
+int oz2_scale_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda,
+                   int num_moduli, int32_t* e);
+/* Alg. 1 line 1 for the columns of B (k x n): f[j], E = diag(2^f[j]).  f: int32[n]. */
+int oz2_scale_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb,
+                   int num_moduli, int32_t* f);
+/* Alg. 1 line 2: Ap = trunc(D A), m x k row-major FP64 integers (ld = k). */
+int oz2_trunc_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda,
+                   const int32_t* e, double* Ap);
+/* Alg. 1 line 3, transposed: BpT = trunc(B E)^T, n x k row-major (ld = k). */
+int oz2_trunc_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb,
+                   const int32_t* f, double* BpT);
+/* Alg. 1 lines 2+4 (Eq. 11): int8 planes
+ * Ares[t][i][l] = trunc(2^e[i] a_il) mod m_t (Eq. 1), t < N, i < m, l < k,
+ * plane row stride ld_res (a multiple of 16, >= k), plane stride m*ld_res.
+ * Bytes [k, ld_res) of each row are unspecified. */
+int oz2_residues_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda,
+                      const int32_t* e, int num_moduli, int8_t* Ares, int64_t ld_res);
+/* Alg. 1 lines 3+5 for B, stored K-major (transposed):
+ * Bres[t][j][l] = trunc(2^f[j] b_lj) mod m_t, plane stride n*ld_res. */
+int oz2_residues_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb,
+                      const int32_t* f, int num_moduli, int8_t* Bres, int64_t ld_res);
+/* Alg. 1 line 6 on the INT8 tensor cores: Cprod[t][i][j] = sum_l
+ * Ares[t][i][l] Bres[t][j][l] exactly (int32).
+ * Cprod: int32[N][m][n]. */
+int oz2_modmul(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const int8_t* Ares,
+               const int8_t* Bres, int64_t ld_res, int num_moduli, int32_t* Cprod);
+/* Alg. 1 lines 7-10: c''_t = Cprod_t mod m_t in [0, m_t), X = (sum_t c''_t
+ * M y_t / m_t) mod M (Eq. 1), C[i][j] = 2^-(e[i]+f[j]) RN(X)  (reading R10). */
+int oz2_crt(oz2_handle_t h, int64_t m, int64_t n, const int32_t* Cprod, const int32_t* e,
+            const int32_t* f, int num_moduli, double* C, int64_t ldc);
+
+/* ---- constants (host memory, no device needed) ----------------------------
+ * moduli[N], y[N] (M_t y_t == 1 mod m_t, least positive), W[P*N] with
+ * w_t = M y_t / m_t = sum_p W[p*N + t] 2^(40 p), 0 <= W < 2^40, Mp[P] the
+ * same split of M, *P pieces, *L = floor(log2(M/2 - 1)), *T = floor(L/2).
+ * Any output pointer may be NULL.  W must hold 4*N doubles, Mp 4. */
+int oz2_tables(int num_moduli, int32_t* moduli, int32_t* y, double* W, double* Mp,
+               int32_t* P, int32_t* L, int32_t* T);
+/* Eq. (17) in exact integer form: max{kappa : q 4^kappa <= M/2 - 1}, -1 if none. */
+int oz2_eq17_k(int num_moduli, int64_t q);
+
+const char* oz2_strerror(int code);
+/* 100 * major + minor */
+int oz2_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OZ2_H */

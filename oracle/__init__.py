@@ -57,6 +57,8 @@ def lib():
         L.oz2o_constants.argtypes = [i32, P, P, P, P, P, P]
         L.oz2o_smod_i64.argtypes = [i64, i64]
         L.oz2o_smod_i64.restype = i64
+        L.oz2o_smod_i64_long.argtypes = [i64, i64]
+        L.oz2o_smod_i64_long.restype = i64
         L.oz2o_crt_scalar.argtypes = [i32, P, P]
         L.oz2o_eq17_k.argtypes = [i32, i64]
         L.oz2o_scale_fast.argtypes = [i64, i64, P, i64, i64, i32, P]
@@ -126,6 +128,11 @@ def constants(N: int) -> dict:
 
 def smod(a: int, m: int) -> int:
     return int(lib().oz2o_smod_i64(int(a), int(m)))
+
+
+def smod_long(a: int, m: int) -> int:
+    """Eq. (1) through the wide long-division path (the one the CRT uses)."""
+    return int(lib().oz2o_smod_i64_long(int(a), int(m)))
 
 
 def crt_scalar(N: int, c) -> int:

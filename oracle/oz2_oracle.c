@@ -125,6 +125,31 @@ static wide_t w_floordiv(wide_t num, wide_t den) {
     if (!w_is_zero(r)) q = w_sub(q, w_from_i64(1));
     return q;
 }
+/* schoolbook short division of num >= 0 by a one-limb den > 0 */
+static void w_udivmod_small(wide_t num, uint64_t den, wide_t* q, uint64_t* r) {
+    u128 rem = 0;
+    for (int i = WL - 1; i >= 0; i--) {
+        u128 cur = (rem << 64) | num.l[i];
+        q->l[i] = (uint64_t)(cur / den);
+        rem = cur % den;
+    }
+    *r = (uint64_t)rem;
+}
+/* floor(num / den) for any num and a one-limb den > 0 */
+static wide_t w_floordiv_small(wide_t num, uint64_t den) {
+    wide_t q; uint64_t r;
+    if (!w_is_neg(num)) { w_udivmod_small(num, den, &q, &r); return q; }
+    w_udivmod_small(w_neg(num), den, &q, &r);
+    q = w_neg(q);
+    if (r) q = w_sub(q, w_from_i64(1));
+    return q;
+}
+/* Eq. (1) for a modulus that fits one limb (all m_t): same formula, short division */
+static wide_t w_smod_small(wide_t a, int64_t m) {
+    wide_t mm = w_from_i64(m);
+    wide_t q = w_floordiv_small(w_add(w_add(a, a), mm), (uint64_t)(2 * m));
+    return w_sub(a, w_mul(mm, q));
+}
 /* Eq. (1): r = a - m * floor(a/m + 1/2) = a - m * floor((2a + m) / (2m)) */
 static wide_t w_smod(wide_t a, wide_t m) {
     wide_t two_a_plus_m = w_add(w_add(a, a), m);
@@ -228,6 +253,11 @@ int oz2o_constants(int N, int32_t* moduli, int32_t* y, uint64_t* M_limbs4,
 
 /* Eq. (1) on int64 inputs (for brute-force tests) */
 int64_t oz2o_smod_i64(int64_t a, int64_t m) {
+    wide_t r = w_smod_small(w_from_i64(a), m);
+    return (int64_t)r.l[0];
+}
+/* the same through the general (long-division) path, used for the CRT */
+int64_t oz2o_smod_i64_long(int64_t a, int64_t m) {
     wide_t r = w_smod(w_from_i64(a), w_from_i64(m));
     return (int64_t)r.l[0];
 }
@@ -367,7 +397,7 @@ int oz2o_residues(int64_t rows, int64_t len, const double* Xp, int N, int8_t* ou
         for (int64_t l = 0; l < len; l++) {
             wide_t x = w_from_double(Xp[r * len + l]);
             for (int t = 0; t < N; t++) {
-                wide_t res = w_smod(x, w_from_i64(c.m[t]));
+                wide_t res = w_smod_small(x, c.m[t]);
                 out[((int64_t)t * rows + r) * len + l] = (int8_t)(int64_t)res.l[0];
             }
         }

@@ -1,0 +1,458 @@
+// api.cu -- the C ABI of liboz2.so (declared in include/oz2.h): argument
+// checking, handles, workspace, TMA tensor maps and the launch sequence of
+// Algorithm 1.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "../../include/oz2.h"
+#include "oz2_device.cuh"
+#include "oz2_kernels.h"
+
+namespace {
+
+Oz2Table g_tabs[OZ2_MAX_MODULI + 1];
+bool g_tabs_ok = false;
+std::once_flag g_tabs_once;
+std::mutex g_mu;
+bool g_dev_uploaded[64] = {false};
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+
+void build_tables_once() {
+    g_tabs_ok = (oz2_build_tables(g_tabs) == 0);
+    for (int N = 2; N <= OZ2_MAX_MODULI && g_tabs_ok; N++) {
+        int P = N <= 5 ? 1 : (N <= 10 ? 2 : (N <= 15 ? 3 : 4));     // kernels assume this
+        if (g_tabs[N].P != P) g_tabs_ok = false;
+    }
+}
+
+int ensure_device(int dev) {
+    std::call_once(g_tabs_once, build_tables_once);
+    if (!g_tabs_ok) return OZ2_ERR_INVALID_ARG;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (dev < 0 || dev >= 64) return OZ2_ERR_NO_DEVICE;
+    if (!g_encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return OZ2_ERR_CUDA;
+        g_encode = (EncodeTiledFn)fn;
+    }
+    if (!g_dev_uploaded[dev]) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cudaSetDevice(dev) != cudaSuccess) return OZ2_ERR_NO_DEVICE;
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) { cudaSetDevice(cur); return OZ2_ERR_NO_DEVICE; }
+        if (prop.major != 10) { cudaSetDevice(cur); return OZ2_ERR_NO_DEVICE; }
+        cudaError_t e = cudaMemcpyToSymbol(c_tab, g_tabs, sizeof(g_tabs));
+        cudaSetDevice(cur);
+        if (e != cudaSuccess) return OZ2_ERR_CUDA;
+        g_dev_uploaded[dev] = true;
+    }
+    return OZ2_OK;
+}
+
+}  // namespace
+
+namespace oz2 {
+int host_T(int N) {
+    std::call_once(g_tabs_once, build_tables_once);
+    return g_tabs[N].T;
+}
+}  // namespace oz2
+
+struct oz2_context {
+    int device;
+    int num_sms;
+    cudaStream_t stream;
+    int mode;
+    void* ws_user;
+    size_t ws_user_bytes;
+    void* ws_own;
+    size_t ws_own_bytes;
+};
+
+namespace {
+
+inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+struct Layout {
+    int64_t ldr;
+    size_t off_Ares, off_Bres, off_e, off_f, off_stats, off_cprod, total;
+};
+
+Layout layout_for(int64_t m, int64_t n, int64_t k, int N) {
+    Layout L;
+    L.ldr = round_up(k > 0 ? k : 1, 16);
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = (size_t)round_up((int64_t)(off + bytes), 256); return o; };
+    L.off_Ares = take((size_t)N * (size_t)m * (size_t)L.ldr);
+    L.off_Bres = take((size_t)N * (size_t)n * (size_t)L.ldr);
+    L.off_e = take(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));
+    L.off_f = take(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    L.off_stats = take(oz2::cols_stats_bytes(k, n));
+    L.off_cprod = take(sizeof(int32_t) * (size_t)N * (size_t)m * (size_t)n);
+    L.total = off;
+    return L;
+}
+
+int check_common(int64_t m, int64_t n, int64_t k, int N) {
+    if (m < 0 || n < 0 || k < 0) return OZ2_ERR_INVALID_ARG;
+    if (N < 2 || N > OZ2_MAX_MODULI) return OZ2_ERR_NUM_MODULI;
+    if (k >= (int64_t)1 << 17) return OZ2_ERR_K_TOO_LARGE;
+    if (m > INT32_MAX || n > INT32_MAX) return OZ2_ERR_INVALID_ARG;
+    return OZ2_OK;
+}
+
+int kstar_for(oz2_handle_t h, int N, int64_t k, int* kstar) {
+    *kstar = 0;
+    if (h->mode == OZ2_MODE_EQ17) {
+        int ks = oz2_host_eq17_k(N, k);
+        if (ks < 1) return OZ2_ERR_BUDGET;
+        *kstar = ks;
+    }
+    return OZ2_OK;
+}
+
+int get_workspace(oz2_handle_t h, size_t bytes, uint8_t** ws) {
+    if (h->ws_user) {
+        if (h->ws_user_bytes < bytes) return OZ2_ERR_WORKSPACE;
+        *ws = (uint8_t*)h->ws_user;
+        return OZ2_OK;
+    }
+    if (h->ws_own_bytes < bytes) {
+        if (h->ws_own) {
+            cudaStreamSynchronize(h->stream);
+            cudaFree(h->ws_own);
+            h->ws_own = nullptr;
+            h->ws_own_bytes = 0;
+        }
+        if (cudaMalloc(&h->ws_own, bytes) != cudaSuccess) return OZ2_ERR_CUDA;
+        h->ws_own_bytes = bytes;
+    }
+    *ws = (uint8_t*)h->ws_own;
+    return OZ2_OK;
+}
+
+// 3-D tensor map over residue planes [N][rows][ldr] (int8), box 128 x box_rows x 1, 128B swizzle
+int make_plane_map(CUtensorMap* tm, const int8_t* base, int64_t rows, int64_t k, int64_t ldr, int N,
+                   int box_rows) {
+    cuuint64_t dims[3] = {(cuuint64_t)k, (cuuint64_t)rows, (cuuint64_t)N};
+    cuuint64_t strides[2] = {(cuuint64_t)ldr, (cuuint64_t)(ldr * rows)};
+    cuuint32_t box[3] = {128, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? OZ2_OK : OZ2_ERR_CUDA;
+}
+
+inline int cuda_status() {
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? OZ2_OK : OZ2_ERR_CUDA;
+}
+
+struct DevGuard {
+    int prev;
+    bool changed;
+    explicit DevGuard(int dev) : prev(0), changed(false) {
+        cudaGetDevice(&prev);
+        if (prev != dev) { cudaSetDevice(dev); changed = true; }
+    }
+    ~DevGuard() { if (changed) cudaSetDevice(prev); }
+};
+
+oz2_handle_t g_default[64] = {nullptr};
+
+}  // namespace
+
+extern "C" {
+
+int oz2_version(void) { return 100; }
+
+const char* oz2_strerror(int code) {
+    switch (code) {
+        case OZ2_OK: return "ok";
+        case OZ2_ERR_INVALID_ARG: return "invalid argument";
+        case OZ2_ERR_NUM_MODULI: return "num_moduli must be in [2, 20]";
+        case OZ2_ERR_K_TOO_LARGE: return "k must be < 2^17 (int32 exactness, PAPER.md:457-459)";
+        case OZ2_ERR_BUDGET: return "EQ17 mode: Eq. (17) budget k_A < 1 for this (N, k)";
+        case OZ2_ERR_CUDA: return "CUDA error";
+        case OZ2_ERR_NO_DEVICE: return "no sm_100 CUDA device";
+        case OZ2_ERR_WORKSPACE: return "workspace too small";
+        default: return "unknown error";
+    }
+}
+
+int oz2_tables(int N, int32_t* moduli, int32_t* y, double* W, double* Mp, int32_t* P, int32_t* L, int32_t* T) {
+    std::call_once(g_tabs_once, build_tables_once);
+    if (!g_tabs_ok) return OZ2_ERR_INVALID_ARG;
+    if (N < 2 || N > OZ2_MAX_MODULI) return OZ2_ERR_NUM_MODULI;
+    const Oz2Table& t = g_tabs[N];
+    for (int i = 0; i < N; i++) {
+        if (moduli) moduli[i] = t.m[i];
+        if (y) y[i] = t.y[i];
+        if (W) for (int p = 0; p < 4; p++) W[p * N + i] = t.W[p][i];
+    }
+    if (Mp) for (int p = 0; p < 4; p++) Mp[p] = t.Mp[p];
+    if (P) *P = t.P;
+    if (L) *L = t.L;
+    if (T) *T = t.T;
+    return OZ2_OK;
+}
+
+int oz2_eq17_k(int N, int64_t q) {
+    if (N < 2 || N > OZ2_MAX_MODULI) return -2;
+    return oz2_host_eq17_k(N, q);
+}
+
+int oz2_create(oz2_handle_t* h, int device) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = ensure_device(device);
+    if (rc) return rc;
+    oz2_context* c = (oz2_context*)calloc(1, sizeof(oz2_context));
+    if (!c) return OZ2_ERR_INVALID_ARG;
+    c->device = device;
+    if (cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+        free(c);
+        return OZ2_ERR_CUDA;
+    }
+    c->mode = OZ2_MODE_FAST;
+    *h = c;
+    return OZ2_OK;
+}
+
+int oz2_destroy(oz2_handle_t h) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    if (h->ws_own) { DevGuard g(h->device); cudaFree(h->ws_own); }
+    free(h);
+    return OZ2_OK;
+}
+
+int oz2_set_stream(oz2_handle_t h, void* stream) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    h->stream = (cudaStream_t)stream;
+    return OZ2_OK;
+}
+
+int oz2_set_mode(oz2_handle_t h, int mode) {
+    if (!h || (mode != OZ2_MODE_FAST && mode != OZ2_MODE_EQ17)) return OZ2_ERR_INVALID_ARG;
+    h->mode = mode;
+    return OZ2_OK;
+}
+
+int oz2_set_workspace(oz2_handle_t h, void* ptr, size_t bytes) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    h->ws_user = ptr;
+    h->ws_user_bytes = ptr ? bytes : 0;
+    return OZ2_OK;
+}
+
+size_t oz2_workspace_bytes(int64_t m, int64_t n, int64_t k, int N) {
+    if (m < 0 || n < 0 || k < 0 || N < 2 || N > OZ2_MAX_MODULI) return 0;
+    return layout_for(m, n, k, N).total;
+}
+
+// ---------------------------------------------------------------------------
+// split API
+// ---------------------------------------------------------------------------
+int oz2_scale_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda, int N, int32_t* e) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(m, 1, k, N);
+    if (rc) return rc;
+    if (lda < (k > 0 ? k : 1) || (m > 0 && (!A || !e))) return OZ2_ERR_INVALID_ARG;
+    int kstar;
+    if ((rc = kstar_for(h, N, k, &kstar))) return rc;
+    DevGuard g(h->device);
+    oz2::launch_rows(A, m, k, lda, N, 1, h->mode, kstar, e, nullptr, 0, h->stream);
+    return cuda_status();
+}
+
+int oz2_scale_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb, int N, int32_t* f) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(1, n, k, N);
+    if (rc) return rc;
+    if (ldb < (n > 0 ? n : 1) || (n > 0 && (!B || !f))) return OZ2_ERR_INVALID_ARG;
+    int kstar;
+    if ((rc = kstar_for(h, N, k, &kstar))) return rc;
+    DevGuard g(h->device);
+    uint8_t* ws;
+    if ((rc = get_workspace(h, oz2::cols_stats_bytes(k, n), &ws))) return rc;
+    oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws, h->stream);
+    return cuda_status();
+}
+
+int oz2_trunc_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda, const int32_t* e,
+                   double* Ap) {
+    if (!h || m < 0 || k < 0 || lda < (k > 0 ? k : 1)) return OZ2_ERR_INVALID_ARG;
+    DevGuard g(h->device);
+    oz2::launch_trunc_rows(A, m, k, lda, e, Ap, h->stream);
+    return cuda_status();
+}
+
+int oz2_trunc_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb, const int32_t* f,
+                   double* BpT) {
+    if (!h || n < 0 || k < 0 || ldb < (n > 0 ? n : 1)) return OZ2_ERR_INVALID_ARG;
+    DevGuard g(h->device);
+    oz2::launch_trunc_cols(B, k, n, ldb, f, BpT, h->stream);
+    return cuda_status();
+}
+
+int oz2_residues_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda, const int32_t* e,
+                      int N, int8_t* Ares, int64_t ld_res) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(m, 1, k, N);
+    if (rc) return rc;
+    if (lda < (k > 0 ? k : 1) || ld_res < k || ld_res % 16) return OZ2_ERR_INVALID_ARG;
+    DevGuard g(h->device);
+    if (k > 0) oz2::launch_rows(A, m, k, lda, N, 2, h->mode, 0, const_cast<int32_t*>(e), Ares, ld_res, h->stream);
+    return cuda_status();
+}
+
+int oz2_residues_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb, const int32_t* f,
+                      int N, int8_t* Bres, int64_t ld_res) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(1, n, k, N);
+    if (rc) return rc;
+    if (ldb < (n > 0 ? n : 1) || ld_res < k || ld_res % 16) return OZ2_ERR_INVALID_ARG;
+    DevGuard g(h->device);
+    oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, ld_res, h->stream);
+    return cuda_status();
+}
+
+int oz2_modmul(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const int8_t* Ares, const int8_t* Bres,
+               int64_t ld_res, int N, int32_t* Cprod) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(m, n, k, N);
+    if (rc) return rc;
+    if (ld_res < k || ld_res % 16) return OZ2_ERR_INVALID_ARG;
+    if (m == 0 || n == 0) return OZ2_OK;
+    DevGuard g(h->device);
+    if (k == 0) {
+        return cudaMemsetAsync(Cprod, 0, sizeof(int32_t) * (size_t)N * m * n, h->stream) == cudaSuccess ? OZ2_OK
+                                                                                                        : OZ2_ERR_CUDA;
+    }
+    CUtensorMap tA, tB;
+    if ((rc = make_plane_map(&tA, Ares, m, k, ld_res, N, 128))) return rc;
+    if ((rc = make_plane_map(&tB, Bres, n, k, ld_res, N, 256))) return rc;
+    if (oz2::launch_modmul(&tA, &tB, m, n, k, N, Cprod, h->num_sms, h->stream)) return OZ2_ERR_CUDA;
+    return cuda_status();
+}
+
+int oz2_crt(oz2_handle_t h, int64_t m, int64_t n, const int32_t* Cprod, const int32_t* e, const int32_t* f,
+            int N, double* C, int64_t ldc) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(m, n, 0, N);
+    if (rc) return rc;
+    if (ldc < (n > 0 ? n : 1)) return OZ2_ERR_INVALID_ARG;
+    DevGuard g(h->device);
+    oz2::launch_crt(Cprod, m, n, e, f, N, C, ldc, h->stream);
+    return cuda_status();
+}
+
+// ---------------------------------------------------------------------------
+// main entry points
+// ---------------------------------------------------------------------------
+int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                 const double* B, int64_t ldb, double* C, int64_t ldc, int N) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(m, n, k, N);
+    if (rc) return rc;
+    if (lda < (k > 0 ? k : 1) || ldb < (n > 0 ? n : 1) || ldc < (n > 0 ? n : 1)) return OZ2_ERR_INVALID_ARG;
+    if (m == 0 || n == 0) return OZ2_OK;
+    if (!A || !B || !C) return OZ2_ERR_INVALID_ARG;
+    int kstar;
+    if ((rc = kstar_for(h, N, k, &kstar))) return rc;
+    DevGuard g(h->device);
+    if (k == 0) {
+        cudaError_t e = cudaMemset2DAsync(C, sizeof(double) * ldc, 0, sizeof(double) * n, m, h->stream);
+        return e == cudaSuccess ? OZ2_OK : OZ2_ERR_CUDA;
+    }
+    Layout L = layout_for(m, n, k, N);
+    uint8_t* ws;
+    if ((rc = get_workspace(h, L.total, &ws))) return rc;
+    int8_t* Ares = (int8_t*)(ws + L.off_Ares);
+    int8_t* Bres = (int8_t*)(ws + L.off_Bres);
+    int32_t* e = (int32_t*)(ws + L.off_e);
+    int32_t* f = (int32_t*)(ws + L.off_f);
+    int32_t* cprod = (int32_t*)(ws + L.off_cprod);
+    // Part 1 + 2-a (Alg. 1 lines 1-5)
+    oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
+    oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, h->stream);
+    oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, h->stream);
+    // Part 2-b (line 6)
+    CUtensorMap tA, tB;
+    if ((rc = make_plane_map(&tA, Ares, m, k, L.ldr, N, 128))) return rc;
+    if ((rc = make_plane_map(&tB, Bres, n, k, L.ldr, N, 256))) return rc;
+    if (oz2::launch_modmul(&tA, &tB, m, n, k, N, cprod, h->num_sms, h->stream)) return OZ2_ERR_CUDA;
+    // Parts 2-c, 3, 4 (lines 7-10)
+    oz2::launch_crt(cprod, m, n, e, f, N, C, ldc, h->stream);
+    return cuda_status();
+}
+
+int oz2_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B, int64_t ldb,
+              double* C, int64_t ldc, int N) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return OZ2_ERR_NO_DEVICE;
+    if (dev < 0 || dev >= 64) return OZ2_ERR_NO_DEVICE;
+    if (!g_default[dev]) {
+        oz2_handle_t hh;
+        int rc = oz2_create(&hh, dev);
+        if (rc) return rc;
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!g_default[dev]) g_default[dev] = hh; else oz2_destroy(hh);
+    }
+    return oz2_dgemm_ex(g_default[dev], m, n, k, A, lda, B, ldb, C, ldc, N);
+}
+
+int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                   const double* B, int64_t ldb, double* C, int64_t ldc, int N) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(m, n, k, N);
+    if (rc) return rc;
+    if (lda < (k > 0 ? k : 1) || ldb < (n > 0 ? n : 1) || ldc < (n > 0 ? n : 1)) return OZ2_ERR_INVALID_ARG;
+    if (m == 0 || n == 0) return OZ2_OK;
+    DevGuard g(h->device);
+    // device staging buffers live after the dgemm workspace
+    Layout L = layout_for(m, n, k, N);
+    size_t bytesA = sizeof(double) * (size_t)m * (size_t)(k > 0 ? k : 1);
+    size_t bytesB = sizeof(double) * (size_t)(k > 0 ? k : 1) * (size_t)n;
+    size_t bytesC = sizeof(double) * (size_t)m * (size_t)n;
+    size_t offA = (size_t)round_up((int64_t)L.total, 256);
+    size_t offB = (size_t)round_up((int64_t)(offA + bytesA), 256);
+    size_t offC = (size_t)round_up((int64_t)(offB + bytesB), 256);
+    size_t total = offC + bytesC;
+    uint8_t* ws;
+    if ((rc = get_workspace(h, total, &ws))) return rc;
+    double* dA = (double*)(ws + offA);
+    double* dB = (double*)(ws + offB);
+    double* dC = (double*)(ws + offC);
+    if (k > 0) {
+        if (cudaMemcpy2DAsync(dA, sizeof(double) * k, A, sizeof(double) * lda, sizeof(double) * k, m,
+                              cudaMemcpyHostToDevice, h->stream) != cudaSuccess) return OZ2_ERR_CUDA;
+        if (cudaMemcpy2DAsync(dB, sizeof(double) * n, B, sizeof(double) * ldb, sizeof(double) * n, k,
+                              cudaMemcpyHostToDevice, h->stream) != cudaSuccess) return OZ2_ERR_CUDA;
+    }
+    // the dgemm workspace is the prefix [0, L.total): run with it as a user workspace
+    void* save_ptr = h->ws_user;
+    size_t save_bytes = h->ws_user_bytes;
+    h->ws_user = ws;
+    h->ws_user_bytes = L.total;
+    rc = oz2_dgemm_ex(h, m, n, k, dA, k > 0 ? k : 1, dB, n, dC, n, N);
+    h->ws_user = save_ptr;
+    h->ws_user_bytes = save_bytes;
+    if (rc) return rc;
+    if (cudaMemcpy2DAsync(C, sizeof(double) * ldc, dC, sizeof(double) * n, sizeof(double) * n, m,
+                          cudaMemcpyDeviceToHost, h->stream) != cudaSuccess) return OZ2_ERR_CUDA;
+    return cudaStreamSynchronize(h->stream) == cudaSuccess ? OZ2_OK : OZ2_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,7 @@
+// liboz2.cu -- the library is compiled as one translation unit so that the
+// __constant__ tables are shared by every kernel without relocatable device code.
+#include "oz2_device.cuh"
+#include "scale.cu"
+#include "gemm.cu"
+#include "crt.cu"
+#include "api.cu"

@@ -1,0 +1,181 @@
+// oz2_device.cuh -- device-side helpers shared by the sm_100a kernels:
+// the __constant__ tables, exponent extraction, mbarrier / TMA / tcgen05 PTX.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "oz2_tables.h"
+
+#define OZ2_EXP_NONFINITE_DEV INT32_MIN
+
+// per-N constants, filled once per device by api.cu (the library is one
+// translation unit, liboz2.cu, so this is the single definition)
+__constant__ Oz2Table c_tab[OZ2_MAX_MODULI + 1];
+
+namespace oz2 {
+
+// ---------------------------------------------------------------------------
+// binary64 decomposition: x = mant * 2^ex with integer mant (exact), and
+// ilogb(x) = floor(log2|x|) (correct for subnormals).  class: 0 zero,
+// 1 finite non-zero, 2 Inf/NaN.
+// ---------------------------------------------------------------------------
+struct Dec { uint64_t mant; int ex; int ilogb; int cls; };
+
+__device__ __forceinline__ Dec decompose(double x) {
+    uint64_t b = (uint64_t)__double_as_longlong(x);
+    int ef = (int)((b >> 52) & 0x7ff);
+    uint64_t fr = b & 0xfffffffffffffull;
+    Dec d;
+    if (ef == 0x7ff) { d.cls = 2; d.mant = 0; d.ex = 0; d.ilogb = 0; return d; }
+    if (ef == 0) {
+        d.mant = fr; d.ex = -1074;
+        d.cls = fr ? 1 : 0;
+        d.ilogb = fr ? (63 - __clzll((long long)fr)) - 1074 : INT32_MIN;
+    } else {
+        d.mant = fr | (1ull << 52); d.ex = ef - 1075; d.cls = 1; d.ilogb = ef - 1023;
+    }
+    return d;
+}
+
+// x * 2^e exactly when the result is >= 1 in magnitude (two steps outside the
+// normal exponent range so the first step never rounds).
+__device__ __forceinline__ double scale_pow2(double x, int e) {
+    if (e > 1023) {
+        x *= __longlong_as_double((long long)(1023 + 1023) << 52);
+        e -= 1023;
+    } else if (e < -1022) {
+        x *= __longlong_as_double((long long)(1) << 52);        // 2^-1022
+        e += 1022;
+        if (e < -1022) return 0.0 * x;                            // |result| < 1 (see R12 note)
+    }
+    return x * __longlong_as_double((long long)(e + 1023) << 52);
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory addresses, mbarriers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}"
+        :: "r"(bar), "r"(parity) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// TMA (cp.async.bulk.tensor) 3-D tile load, completion on an mbarrier
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, uint32_t bar,
+                                            int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];"
+        :: "r"(dst), "l"((uint64_t)tmap), "r"(c0), "r"(c1), "r"(c2), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
+    asm volatile("prefetch.tensormap [%0];" :: "l"((uint64_t)tmap) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05: TMEM allocation, MMA, commit, loads, fences
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 :: "r"(dst_smem), "r"(ncols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(taddr), "r"(ncols) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T, int8 x int8 -> int32 (kind::i8)
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+        :: "r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+// arrive on an mbarrier when all prior tcgen05.mma of this thread complete
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(bar) : "memory");
+}
+// 32 lanes x 32 bit, 32 consecutive columns per thread
+__device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+          "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, 128-byte swizzle: 8-row x 128-byte
+// swizzle atoms stacked at SBO = 1024 bytes (tile base 1024-aligned).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);          // start address  [0,14)
+    d |= (uint64_t)1 << 16;                              // LBO (unused for SW128 K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;                    // SBO            [32,46)
+    d |= (uint64_t)1 << 46;                              // version = 1    [46,48)
+    d |= (uint64_t)2 << 61;                              // SWIZZLE_128B   [61,64)
+    return d;
+}
+// instruction descriptor, kind::i8: s8 x s8 -> s32, both K-major, M x N
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+    return (2u << 4)                 // c_format = S32
+         | (1u << 7)                 // a_format = signed int8
+         | (1u << 10)                // b_format = signed int8
+         | ((uint32_t)(N >> 3) << 17)
+         | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ uint32_t dp4a_uu(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+// low bytes of four 32-bit values -> one word (byte i from v_i)
+__device__ __forceinline__ uint32_t pack_lo_bytes(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3) {
+    uint32_t a = prmt(v0, v1, 0x0040u);
+    uint32_t b = prmt(v2, v3, 0x0040u);
+    return prmt(a, b, 0x5410u);
+}
+
+}  // namespace oz2

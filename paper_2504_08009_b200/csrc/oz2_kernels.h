@@ -1,0 +1,36 @@
+// oz2_kernels.h -- host-side launchers of the sm_100a kernels (api.cu calls these).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace oz2 {
+
+int host_T(int N);   // floor(L/2) for N moduli (host copy of the table)
+
+// scale.cu -- Alg. 1 lines 1-5
+// what: 1 = exponents e, 2 = residues (given e), 3 = both (one pass per row)
+void launch_rows(const double* A, int64_t m, int64_t k, int64_t lda, int N, int what, int mode,
+                 int kstar, int32_t* e, int8_t* res, int64_t ldr, cudaStream_t st);
+void launch_trunc_rows(const double* A, int64_t m, int64_t k, int64_t lda, const int32_t* e,
+                       double* out, cudaStream_t st);
+size_t cols_stats_bytes(int64_t k, int64_t n);
+void launch_cols_exponents(const double* B, int64_t k, int64_t n, int64_t ldb, int N, int mode,
+                           int kstar, int32_t* f, void* scratch, cudaStream_t st);
+void launch_cols_residues(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f, int N,
+                          int8_t* res, int64_t ldr, cudaStream_t st);
+void launch_trunc_cols(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
+                       double* out, cudaStream_t st);
+
+// gemm.cu -- Alg. 1 line 6 on tcgen05 (kind::i8)
+struct GemmOut {
+    int32_t* cprod;        // raw int32 products [N][m][n] (mode RAW), else NULL
+};
+int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
+                  int N, int32_t* cprod, int num_sms, cudaStream_t st);
+
+// crt.cu -- Alg. 1 lines 7-10
+void launch_crt(const int32_t* cprod, int64_t m, int64_t n, const int32_t* e, const int32_t* f,
+                int N, double* C, int64_t ldc, cudaStream_t st);
+
+}  // namespace oz2

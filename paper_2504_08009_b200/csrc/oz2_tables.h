@@ -1,0 +1,33 @@
+// oz2_tables.h -- per-N constants of Algorithm 1 as the kernels consume them.
+//
+// Built on the host by tables.cpp (independent of oracle/) and copied to
+// __constant__ memory once per device.  Indexed by N (2..20).
+#pragma once
+#include <stdint.h>
+
+#define OZ2_MAX_MODULI 20
+
+struct Oz2Table {
+    int32_t N;           // number of moduli
+    int32_t P;           // number of 40-bit pieces of M (1..4)
+    int32_t L;           // floor(log2(M/2 - 1))        (Eq. 16 with q dropped)
+    int32_t T;           // floor(L/2): FAST bound ||2^e a||_2 <= 2^T   (reading R4)
+    int32_t m[OZ2_MAX_MODULI];        // moduli, Eq. (18) + reading R1
+    uint32_t magic[OZ2_MAX_MODULI];   // ceil(2^32 / m): floor(y/m) = umulhi(y, magic) for y < 2^24
+    int32_t h[OZ2_MAX_MODULI];        // (m - 1) / 2 (odd m): symmetric offset
+    uint32_t cw[3][OZ2_MAX_MODULI];   // byte b of cw[w][t] = 2^(8(4w+b)) mod m_t
+    int32_t g64[OZ2_MAX_MODULI];      // (-2^64) mod m_t in [0, m_t)
+    int32_t g96[OZ2_MAX_MODULI];      // (-2^96) mod m_t in [0, m_t)
+    double W[4][OZ2_MAX_MODULI];      // w_t = M y_t / m_t = sum_p W[p][t] 2^(40p), W < 2^40
+    double Mp[4];                     // M = sum_p Mp[p] 2^(40p)
+    double invM;                      // 2^(40(P-2)) / M  (P >= 2),  1/M  (P == 1)
+    double inv_m[OZ2_MAX_MODULI];     // 1.0 / m_t
+    uint64_t Mw[3];                   // M, 192-bit little endian
+    uint64_t Mhalf[3];                // M / 2
+    int32_t y[OZ2_MAX_MODULI];        // least positive inverse of M_t mod m_t (host only)
+};
+
+// Fill tabs[2..20]; tabs[0], tabs[1] are zeroed.  Returns 0 on success.
+int oz2_build_tables(Oz2Table tabs[OZ2_MAX_MODULI + 1]);
+// Eq. (17): max{kappa : q 4^kappa <= M/2 - 1} or -1.
+int oz2_host_eq17_k(int N, int64_t q);

@@ -1,0 +1,337 @@
+"""Thin ctypes binding of liboz2.so (include/oz2.h) for torch tensors.
+
+Argument marshalling only: every stage of the path runs in the library's
+sm_100a kernels.  torch provides device memory (outputs and the workspace, via
+its caching allocator) and the stream (torch.cuda.current_stream()).  If the
+library is missing, every call raises -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liboz2.so")
+
+OK = 0
+MODE_FAST = 0
+MODE_EQ17 = 1
+EXP_NONFINITE = -(2**31)
+MAX_K = 2**17
+
+# every symbol include/oz2.h declares (checked by tests/test_abi.py)
+SYMBOLS = [
+    "oz2_create", "oz2_destroy", "oz2_set_stream", "oz2_set_mode", "oz2_set_workspace",
+    "oz2_workspace_bytes", "oz2_dgemm", "oz2_dgemm_ex", "oz2_dgemm_host", "oz2_scale_rows",
+    "oz2_scale_cols", "oz2_trunc_rows", "oz2_trunc_cols", "oz2_residues_rows", "oz2_residues_cols",
+    "oz2_modmul", "oz2_crt", "oz2_tables", "oz2_eq17_k", "oz2_strerror", "oz2_version",
+]
+
+
+class Oz2Error(RuntimeError):
+    def __init__(self, code: int, what: str = ""):
+        msg = lib().oz2_strerror(code).decode() if _lib is not None else str(code)
+        super().__init__(f"{what}: liboz2 error {code} ({msg})")
+        self.code = code
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib() -> ctypes.CDLL:
+    """Load liboz2.so (raises OSError if it has not been built)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise OSError(f"{LIB_PATH} not found: build it with "
+                                  "`python -m paper_2504_08009_b200.build` (no CPU fallback)")
+                L = ctypes.CDLL(LIB_PATH)
+                P, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+                L.oz2_create.argtypes = [ctypes.POINTER(P), i32]
+                L.oz2_destroy.argtypes = [P]
+                L.oz2_set_stream.argtypes = [P, P]
+                L.oz2_set_mode.argtypes = [P, i32]
+                L.oz2_set_workspace.argtypes = [P, P, sz]
+                L.oz2_workspace_bytes.argtypes = [i64, i64, i64, i32]
+                L.oz2_workspace_bytes.restype = sz
+                L.oz2_dgemm.argtypes = [i64, i64, i64, P, i64, P, i64, P, i64, i32]
+                L.oz2_dgemm_ex.argtypes = [P, i64, i64, i64, P, i64, P, i64, P, i64, i32]
+                L.oz2_dgemm_host.argtypes = [P, i64, i64, i64, P, i64, P, i64, P, i64, i32]
+                L.oz2_scale_rows.argtypes = [P, i64, i64, P, i64, i32, P]
+                L.oz2_scale_cols.argtypes = [P, i64, i64, P, i64, i32, P]
+                L.oz2_trunc_rows.argtypes = [P, i64, i64, P, i64, P, P]
+                L.oz2_trunc_cols.argtypes = [P, i64, i64, P, i64, P, P]
+                L.oz2_residues_rows.argtypes = [P, i64, i64, P, i64, P, i32, P, i64]
+                L.oz2_residues_cols.argtypes = [P, i64, i64, P, i64, P, i32, P, i64]
+                L.oz2_modmul.argtypes = [P, i64, i64, i64, P, P, i64, i32, P]
+                L.oz2_crt.argtypes = [P, i64, i64, P, P, P, i32, P, i64]
+                L.oz2_tables.argtypes = [i32, P, P, P, P, P, P, P]
+                L.oz2_eq17_k.argtypes = [i32, i64]
+                L.oz2_strerror.argtypes = [i32]
+                L.oz2_strerror.restype = ctypes.c_char_p
+                L.oz2_version.argtypes = []
+                _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != OK:
+        raise Oz2Error(rc, what)
+
+
+def _mode_id(mode) -> int:
+    if isinstance(mode, int):
+        return mode
+    return {"fast": MODE_FAST, "eq17": MODE_EQ17}[mode.lower()]
+
+
+# ---------------------------------------------------------------------------
+# constants (host only, no GPU)
+# ---------------------------------------------------------------------------
+def tables(N: int) -> dict:
+    m = np.zeros(N, np.int32)
+    y = np.zeros(N, np.int32)
+    W = np.zeros(4 * N, np.float64)
+    Mp = np.zeros(4, np.float64)
+    P, L, T = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    c = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    _check(lib().oz2_tables(N, c(m), c(y), c(W), c(Mp), ctypes.byref(P), ctypes.byref(L),
+                            ctypes.byref(T)), "oz2_tables")
+    return {"moduli": [int(v) for v in m], "y": [int(v) for v in y],
+            "W": W.reshape(4, N)[:P.value].copy(), "Mp": Mp[:P.value].copy(),
+            "P": P.value, "L": L.value, "T": T.value}
+
+
+def eq17_k(N: int, q: int) -> int:
+    return int(lib().oz2_eq17_k(N, int(q)))
+
+
+def workspace_bytes(m: int, n: int, k: int, N: int) -> int:
+    return int(lib().oz2_workspace_bytes(m, n, k, N))
+
+
+# ---------------------------------------------------------------------------
+# handles (one per device), workspace from torch
+# ---------------------------------------------------------------------------
+class Handle:
+    def __init__(self, device: int):
+        import torch
+
+        self.device = int(device)
+        h = ctypes.c_void_p()
+        _check(lib().oz2_create(ctypes.byref(h), self.device), "oz2_create")
+        self._h = h
+        self._ws = None
+        self._torch = torch
+
+    @property
+    def ptr(self):
+        return self._h
+
+    def prepare(self, mode, ws_bytes: int = 0):
+        torch = self._torch
+        _check(lib().oz2_set_mode(self._h, _mode_id(mode)), "oz2_set_mode")
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        _check(lib().oz2_set_stream(self._h, ctypes.c_void_p(stream)), "oz2_set_stream")
+        if ws_bytes:
+            if self._ws is None or self._ws.numel() < ws_bytes:
+                self._ws = None
+                self._ws = torch.empty(ws_bytes, dtype=torch.uint8, device=f"cuda:{self.device}")
+            self._ws.record_stream(torch.cuda.current_stream(self.device))
+            _check(lib().oz2_set_workspace(self._h, ctypes.c_void_p(self._ws.data_ptr()), self._ws.numel()),
+                   "oz2_set_workspace")
+        else:
+            _check(lib().oz2_set_workspace(self._h, None, 0), "oz2_set_workspace")
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) is not None and _lib is not None:
+                _lib.oz2_destroy(self._h)
+        except Exception:
+            pass
+
+
+_handles: dict = {}
+
+
+def handle(device=None) -> Handle:
+    import torch
+
+    dev = torch.cuda.current_device() if device is None else int(device)
+    if dev not in _handles:
+        _handles[dev] = Handle(dev)
+    return _handles[dev]
+
+
+def _vp(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _rowmajor(x, dtype):
+    import torch
+
+    assert x.is_cuda, "liboz2 takes CUDA tensors (no CPU fallback)"
+    assert x.dim() == 2 and x.dtype == dtype, (x.shape, x.dtype)
+    if x.stride(1) != 1 or x.stride(0) < max(1, x.shape[1]):
+        x = x.contiguous()
+    return x
+
+
+def _ld(x):
+    return max(int(x.stride(0)), max(1, int(x.shape[1])))
+
+
+def ld_res_for(k: int) -> int:
+    return max(16, (k + 15) // 16 * 16)
+
+
+# ---------------------------------------------------------------------------
+# main entry point
+# ---------------------------------------------------------------------------
+def dgemm(A, B, num_moduli: int = 14, mode="fast", out=None):
+    """C = A @ B (float64, CUDA) by Ozaki scheme II with `num_moduli` INT8 GEMMs."""
+    import torch
+
+    A = _rowmajor(A, torch.float64)
+    B = _rowmajor(B, torch.float64)
+    m, k = A.shape
+    k2, n = B.shape
+    if k != k2:
+        raise ValueError(f"inner dimensions differ: {A.shape} @ {B.shape}")
+    C = out if out is not None else torch.empty((m, n), dtype=torch.float64, device=A.device)
+    assert C.stride(1) == 1 and C.shape == (m, n)
+    h = handle(A.device.index)
+    h.prepare(mode, workspace_bytes(m, n, k, num_moduli))
+    _check(lib().oz2_dgemm_ex(h.ptr, m, n, k, _vp(A), _ld(A), _vp(B), _ld(B), _vp(C), _ld(C),
+                              num_moduli), "oz2_dgemm_ex")
+    return C
+
+
+def dgemm_host(A: np.ndarray, B: np.ndarray, num_moduli: int = 14, mode="fast", out=None,
+               device=None) -> np.ndarray:
+    """End-to-end through oz2_dgemm_host: host (ideally pinned) buffers in and out."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    B = np.ascontiguousarray(B, dtype=np.float64)
+    m, k = A.shape
+    n = B.shape[1]
+    C = out if out is not None else np.empty((m, n), np.float64)
+    h = handle(device)
+    ws = workspace_bytes(m, n, k, num_moduli) + 8 * (m * max(k, 1) + max(k, 1) * n + m * n) + 4096
+    h.prepare(mode, ws)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    _check(lib().oz2_dgemm_host(h.ptr, m, n, k, p(A), max(k, 1), p(B), max(n, 1), p(C), max(n, 1),
+                                num_moduli), "oz2_dgemm_host")
+    return C
+
+
+# ---------------------------------------------------------------------------
+# split API (stage parity tests)
+# ---------------------------------------------------------------------------
+def scale_rows(A, N: int, mode="fast"):
+    import torch
+
+    A = _rowmajor(A, torch.float64)
+    m, k = A.shape
+    e = torch.empty(m, dtype=torch.int32, device=A.device)
+    h = handle(A.device.index)
+    h.prepare(mode)
+    _check(lib().oz2_scale_rows(h.ptr, m, k, _vp(A), _ld(A), N, _vp(e)), "oz2_scale_rows")
+    return e
+
+
+def scale_cols(B, N: int, mode="fast"):
+    import torch
+
+    B = _rowmajor(B, torch.float64)
+    k, n = B.shape
+    f = torch.empty(n, dtype=torch.int32, device=B.device)
+    h = handle(B.device.index)
+    h.prepare(mode, 1 << 20 if k * n == 0 else 16 * n * ((k + 255) // 256) + 4 * n + 4096)
+    _check(lib().oz2_scale_cols(h.ptr, k, n, _vp(B), _ld(B), N, _vp(f)), "oz2_scale_cols")
+    return f
+
+
+def trunc_rows(A, e):
+    import torch
+
+    A = _rowmajor(A, torch.float64)
+    m, k = A.shape
+    out = torch.empty((m, k), dtype=torch.float64, device=A.device)
+    h = handle(A.device.index)
+    h.prepare("fast")
+    _check(lib().oz2_trunc_rows(h.ptr, m, k, _vp(A), _ld(A), _vp(e.contiguous()), _vp(out)), "oz2_trunc_rows")
+    return out
+
+
+def trunc_cols(B, f):
+    import torch
+
+    B = _rowmajor(B, torch.float64)
+    k, n = B.shape
+    out = torch.empty((n, k), dtype=torch.float64, device=B.device)
+    h = handle(B.device.index)
+    h.prepare("fast")
+    _check(lib().oz2_trunc_cols(h.ptr, k, n, _vp(B), _ld(B), _vp(f.contiguous()), _vp(out)), "oz2_trunc_cols")
+    return out
+
+
+def residues_rows(A, e, N: int, ld_res: int | None = None):
+    """int8 planes [N][m][ld_res]; entries [k, ld_res) of each row are unspecified."""
+    import torch
+
+    A = _rowmajor(A, torch.float64)
+    m, k = A.shape
+    ldr = ld_res or ld_res_for(k)
+    out = torch.zeros((N, m, ldr), dtype=torch.int8, device=A.device)
+    h = handle(A.device.index)
+    h.prepare("fast")
+    _check(lib().oz2_residues_rows(h.ptr, m, k, _vp(A), _ld(A), _vp(e.contiguous()), N, _vp(out), ldr),
+           "oz2_residues_rows")
+    return out
+
+
+def residues_cols(B, f, N: int, ld_res: int | None = None):
+    """int8 planes [N][n][ld_res] holding B'^T (K-major)."""
+    import torch
+
+    B = _rowmajor(B, torch.float64)
+    k, n = B.shape
+    ldr = ld_res or ld_res_for(k)
+    out = torch.zeros((N, n, ldr), dtype=torch.int8, device=B.device)
+    h = handle(B.device.index)
+    h.prepare("fast")
+    _check(lib().oz2_residues_cols(h.ptr, k, n, _vp(B), _ld(B), _vp(f.contiguous()), N, _vp(out), ldr),
+           "oz2_residues_cols")
+    return out
+
+
+def modmul(Ares, Bres, k: int):
+    """int32 [N][m][n] = Ares[t] @ Bres[t]^T over the first k columns, on tcgen05."""
+    import torch
+
+    N, m, ldr = Ares.shape
+    n = Bres.shape[1]
+    assert Bres.shape[0] == N and Bres.shape[2] == ldr and Ares.is_contiguous() and Bres.is_contiguous()
+    out = torch.empty((N, m, n), dtype=torch.int32, device=Ares.device)
+    h = handle(Ares.device.index)
+    h.prepare("fast")
+    _check(lib().oz2_modmul(h.ptr, m, n, k, _vp(Ares), _vp(Bres), ldr, N, _vp(out)), "oz2_modmul")
+    return out
+
+
+def crt(Cprod, e, f, out=None):
+    import torch
+
+    N, m, n = Cprod.shape
+    C = out if out is not None else torch.empty((m, n), dtype=torch.float64, device=Cprod.device)
+    h = handle(Cprod.device.index)
+    h.prepare("fast")
+    _check(lib().oz2_crt(h.ptr, m, n, _vp(Cprod.contiguous()), _vp(e.contiguous()), _vp(f.contiguous()), N,
+                         _vp(C), _ld(C)), "oz2_crt")
+    return C

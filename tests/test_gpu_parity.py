@@ -1,0 +1,203 @@
+"""GPU parity: every stage of the CUDA path (through the C ABI) against the
+oracle, element by element, bit for bit.
+
+Sizes span several 128 x 256 output tiles and 128-byte K stages with ragged
+tails; edge cases cover k = 1, single rows/columns, zero and non-finite rows,
+the int32 exactness boundary k = 2^17 - 1, every N in 2..20 and both scaling
+modes.  Large configurations are checked on sampled rows/columns: e_i depends
+only on row i of A and f_j only on column j of B, so the oracle's result on a
+row/column subset is exactly the corresponding block of C.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2504_08009_b200.inputs import phi_matrix_np, phi_matrix_torch, SEED_A, SEED_B
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def oz2():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2504_08009_b200 import build, oz2 as o
+    build.build()
+    return o
+
+
+def _bits(x):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    return x.view(np.int64)
+
+
+def assert_bitwise(got, ref, what):
+    got = np.asarray(got)
+    ref = np.asarray(ref)
+    assert got.shape == ref.shape, (what, got.shape, ref.shape)
+    if got.dtype == np.float64:
+        diff = _bits(got) != _bits(ref)
+        # NaN payloads may differ; NaN positions must not
+        diff &= ~(np.isnan(got) & np.isnan(ref))
+    else:
+        diff = got != ref
+    nbad = int(diff.sum())
+    if nbad:
+        idx = np.argwhere(diff)[:5]
+        detail = [(tuple(i), got[tuple(i)], ref[tuple(i)]) for i in idx]
+        raise AssertionError(f"{what}: {nbad} of {diff.size} differ, e.g. {detail}")
+
+
+def _stages(oz2, oracle, A, B, N, mode):
+    m, k = A.shape
+    n = B.shape[1]
+    mo = oracle.MODE_FAST if mode == "fast" else oracle.MODE_EQ17
+    dA = torch.from_numpy(A).to(DEV)
+    dB = torch.from_numpy(B).to(DEV)
+    e = oz2.scale_rows(dA, N, mode)
+    f = oz2.scale_cols(dB, N, mode)
+    e_ref = oracle.scale_rows(A, N, mo)
+    f_ref = oracle.scale_cols(B, N, mo)
+    assert_bitwise(e.cpu().numpy(), e_ref, "e (Alg.1 line 1, rows)")
+    assert_bitwise(f.cpu().numpy(), f_ref, "f (Alg.1 line 1, cols)")
+    Ap = oz2.trunc_rows(dA, e)
+    BpT = oz2.trunc_cols(dB, f)
+    Ap_ref = oracle.trunc_rows(A, e_ref)
+    BpT_ref = oracle.trunc_cols(B, f_ref)
+    assert_bitwise(Ap.cpu().numpy(), Ap_ref, "A' (line 2)")
+    assert_bitwise(BpT.cpu().numpy(), BpT_ref, "B' (line 3)")
+    Ar = oz2.residues_rows(dA, e, N)
+    Br = oz2.residues_cols(dB, f, N)
+    Ar_ref = oracle.residues(Ap_ref, N)
+    Br_ref = oracle.residues(BpT_ref, N)
+    assert_bitwise(Ar[:, :, :k].cpu().numpy(), Ar_ref, "A residues (line 4)")
+    assert_bitwise(Br[:, :, :k].cpu().numpy(), Br_ref, "B residues (line 5)")
+    Cp = oz2.modmul(Ar, Br, k)
+    Cp_ref = oracle.modmul(Ar_ref, Br_ref)
+    assert_bitwise(Cp.cpu().numpy(), Cp_ref, "C'_t (line 6, tcgen05)")
+    C = oz2.crt(Cp, e, f)
+    C_ref = oracle.crt(Cp_ref, e_ref, f_ref)
+    assert_bitwise(C.cpu().numpy(), C_ref, "C (lines 7-10)")
+    C2 = oz2.dgemm(dA, dB, N, mode)
+    assert_bitwise(C2.cpu().numpy(), oracle.dgemm(A, B, N, mo), "C (oz2_dgemm end to end)")
+
+
+@pytest.mark.parametrize("m,n,k,N,phi,mode", [
+    (64, 64, 64, 14, 0.5, "fast"),          # config c1
+    (130, 300, 333, 14, 1.0, "fast"),       # 2x2 tiles, ragged M, N, K
+    (257, 513, 700, 8, 2.0, "fast"),        # 3x3 tiles, 3 K-chunks of the FAST rule
+    (128, 256, 128, 16, 0.5, "fast"),       # exact tile
+    (100, 200, 256, 17, 1.0, "fast"),       # 96-bit residue path
+    (77, 90, 129, 20, 4.0, "fast"),
+    (33, 47, 300, 2, 0.5, "fast"),
+    (70, 80, 200, 5, 0.5, "fast"),          # P = 1 CRT
+    (70, 80, 200, 11, 1.0, "fast"),
+    (64, 64, 64, 14, 0.5, "eq17"),
+    (150, 260, 400, 20, 1.0, "eq17"),
+])
+def test_stage_parity(oz2, oracle, m, n, k, N, phi, mode):
+    A = phi_matrix_np(m, k, phi, seed=1000 + m)
+    B = phi_matrix_np(k, n, phi, seed=2000 + n)
+    _stages(oz2, oracle, A, B, N, mode)
+
+
+@pytest.mark.parametrize("N", list(range(2, 21)))
+def test_dgemm_every_N(oz2, oracle, N):
+    m, n, k = 140, 270, 260
+    A = phi_matrix_np(m, k, 1.0, seed=7 + N)
+    B = phi_matrix_np(k, n, 1.0, seed=8 + N)
+    C = oz2.dgemm(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), N)
+    assert_bitwise(C.cpu().numpy(), oracle.dgemm(A, B, N), f"dgemm N={N}")
+
+
+def test_edge_shapes_and_values(oz2, oracle):
+    cases = [(1, 1, 1), (1, 300, 5), (300, 1, 17), (5, 7, 1), (129, 257, 31), (3, 3, 16)]
+    for (m, n, k) in cases:
+        A = phi_matrix_np(m, k, 1.0, seed=m * 7 + k)
+        B = phi_matrix_np(k, n, 1.0, seed=n * 11 + k)
+        _stages(oz2, oracle, A, B, 14, "fast")
+    m, n, k = 90, 100, 300
+    A = phi_matrix_np(m, k, 1.0, seed=5)
+    B = phi_matrix_np(k, n, 1.0, seed=6)
+    A[3] = 0.0                              # zero row
+    B[:, 7] = 0.0                           # zero column
+    A[5, 10] = np.nan                       # non-finite row
+    B[20, 9] = -np.inf                      # non-finite column
+    A[8] *= 2.0 ** -1070                    # subnormal row
+    B[:, 11] *= 2.0 ** 900                  # huge column
+    A[12, :] = 2.0 ** 60                    # constant row
+    _stages(oz2, oracle, A, B, 14, "fast")
+    _stages(oz2, oracle, A, B, 18, "fast")
+
+
+def test_int32_boundary_k(oz2, oracle):
+    # k = 2^17 - 1 with all residues -128 gives 2^31 - 16384
+    k = 2**17 - 1
+    m, n, N = 8, 8, 3
+    ldr = (k + 15) // 16 * 16
+    Ar = torch.full((N, m, ldr), -128, dtype=torch.int8, device=DEV)
+    Br = torch.full((N, n, ldr), -128, dtype=torch.int8, device=DEV)
+    Cp = oz2.modmul(Ar, Br, k).cpu().numpy()
+    assert (Cp == 2**31 - 16384).all()
+    rng = np.random.Generator(np.random.PCG64(3))
+    Ar_np = rng.integers(-128, 128, size=(N, m, k)).astype(np.int8)
+    Br_np = rng.integers(-128, 128, size=(N, n, k)).astype(np.int8)
+    Ar = torch.zeros((N, m, ldr), dtype=torch.int8, device=DEV)
+    Br = torch.zeros((N, n, ldr), dtype=torch.int8, device=DEV)
+    Ar[:, :, :k] = torch.from_numpy(Ar_np).to(DEV)
+    Br[:, :, :k] = torch.from_numpy(Br_np).to(DEV)
+    assert_bitwise(oz2.modmul(Ar, Br, k).cpu().numpy(), oracle.modmul(Ar_np, Br_np), "modmul k=2^17-1")
+
+
+def test_errors_fail_loudly(oz2):
+    A = torch.ones((4, 4), dtype=torch.float64, device=DEV)
+    with pytest.raises(oz2.Oz2Error):
+        oz2.dgemm(A, A, 21)
+    with pytest.raises(oz2.Oz2Error):
+        oz2.dgemm(A, A, 1)
+    big = torch.ones((1, 2**17), dtype=torch.float64, device=DEV)
+    with pytest.raises(oz2.Oz2Error):
+        oz2.dgemm(big, big.T.contiguous(), 14)
+    with pytest.raises(oz2.Oz2Error):        # EQ17 budget < 1 (N = 2, k = 20000)
+        w = torch.ones((2, 20000), dtype=torch.float64, device=DEV)
+        oz2.dgemm(w, w.T.contiguous(), 2, mode="eq17")
+    Z = oz2.dgemm(torch.ones((3, 0), dtype=torch.float64, device=DEV),
+                  torch.ones((0, 5), dtype=torch.float64, device=DEV), 14)
+    assert (Z.cpu().numpy() == 0).all()
+
+
+def test_host_entry_point(oz2, oracle):
+    A = phi_matrix_np(100, 200, 0.5, seed=1)
+    B = phi_matrix_np(200, 150, 0.5, seed=2)
+    C = oz2.dgemm_host(A, B, 14)
+    assert_bitwise(C, oracle.dgemm(A, B, 14), "oz2_dgemm_host")
+
+
+def test_strided_operands(oz2, oracle):
+    A = phi_matrix_np(70, 300, 1.0, seed=11)
+    B = phi_matrix_np(300, 90, 1.0, seed=12)
+    Abig = torch.zeros((70, 333), dtype=torch.float64, device=DEV)
+    Bbig = torch.zeros((300, 101), dtype=torch.float64, device=DEV)
+    Abig[:, :300] = torch.from_numpy(A).to(DEV)
+    Bbig[:, :90] = torch.from_numpy(B).to(DEV)
+    C = oz2.dgemm(Abig[:, :300], Bbig[:, :90], 14)           # lda = 333, ldb = 101 (odd: unaligned rows)
+    assert_bitwise(C.cpu().numpy(), oracle.dgemm(A, B, 14), "strided dgemm")
+
+
+@pytest.mark.parametrize("n,N", [(4096, 14), (4096, 8), (4096, 20)])
+def test_c2_sampled(oz2, oracle, n, N):
+    """config c2 (4096^3): sampled 48 x 48 block + 2 full rows, bitwise."""
+    A = phi_matrix_torch(n, n, 1.0, SEED_A, device=DEV)
+    B = phi_matrix_torch(n, n, 1.0, SEED_B, device=DEV)
+    C = oz2.dgemm(A, B, N).cpu().numpy()
+    rng = np.random.Generator(np.random.PCG64(3))
+    rows = np.sort(rng.choice(n, 48, replace=False))
+    cols = np.sort(rng.choice(n, 48, replace=False))
+    An = A[torch.from_numpy(rows).to(DEV)].cpu().numpy()
+    Bn = B[:, torch.from_numpy(cols).to(DEV)].cpu().numpy()
+    assert_bitwise(C[np.ix_(rows, cols)], oracle.dgemm(An, Bn, N), f"c2 sampled N={N}")
+    full_rows = rows[:2]
+    Ar = A[torch.from_numpy(full_rows).to(DEV)].cpu().numpy()
+    assert_bitwise(C[full_rows], oracle.dgemm(Ar, B.cpu().numpy(), N), f"c2 full rows N={N}")

@@ -31,6 +31,7 @@ def test_smod_bruteforce(oracle):
             r = oracle.smod(a, m)
             assert (r - a) % m == 0
             assert -m <= 2 * r < m, (a, m, r)
+            assert oracle.smod_long(a, m) == r
 
 
 def test_moduli_table_is_eq18(oracle):
