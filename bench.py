@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""bench.py -- emulated FP64 TFLOPS (2mnk/t) of Ozaki scheme II on B200.
+
+Workload (BASELINE.json configs[2], the headline): C = A B with m = n = k =
+16384, N = 14 INT8 moduli, inputs (rand - 0.5) exp(phi randn) with phi = 1
+(PAPER.md:624-632).  One step = one full Algorithm 1
+through the C ABI (oz2_dgemm_ex): scaling + residues of A and B, the N modular
+INT8 tensor-core GEMMs, CRT and inverse scaling.
+
+Multi-GPU (torchrun, one rank per GPU, NCCL): output row-blocks of A per rank
+(weak scaling: every rank owns a 16384-row block), B broadcast from rank 0
+every step; per the north star, C row-blocks are gathered to rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl oz2|reference]
+
+Prints ONE JSON line on rank 0.  The oracle (oracle/) is only executed in the
+cpu_baseline leg and in --impl reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "emulated FP64 TFLOPS (2mnk/t) at n=16384 vs moduli N, 1/2/4/8 B200; max rel err"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="oz2", choices=["oz2", "reference"])
+    p.add_argument("--n", type=int, default=16384)
+    p.add_argument("--m", type=int, default=None, help="rows per rank (default n)")
+    p.add_argument("--k", type=int, default=None)
+    p.add_argument("--moduli", type=int, default=14)
+    p.add_argument("--phi", type=float, default=1.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-context", action="store_true")
+    p.add_argument("--acc-samples", type=int, default=256)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# exact reference for sampled entries (bench-local, error-free products + fsum)
+# ---------------------------------------------------------------------------
+def _split(x):
+    c = x * 134217729.0                    # Veltkamp split, 2^27 + 1
+    hi = c - (c - x)
+    return hi, x - hi
+
+
+def exact_entries(Arows: np.ndarray, Bcols: np.ndarray):
+    """(AB)_ij and (|A||B|)_ij, each correctly rounded, for row i of Arows and
+    column j of Bcols (paired): products split error-free, summed by fsum."""
+    ab, absab = [], []
+    for a, b in zip(Arows, Bcols.T):
+        ah, al = _split(a)
+        bh, bl = _split(b)
+        parts = np.concatenate([ah * bh, ah * bl, al * bh, al * bl])
+        ab.append(math.fsum(parts))
+        aah, aal = _split(np.abs(a))
+        abh, abl = _split(np.abs(b))
+        absab.append(math.fsum(np.concatenate([aah * abh, aah * abl, aal * abh, aal * abl])))
+    return np.array(ab), np.array(absab)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) == 7:
+                self.rows.append(f)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        loaded = [v for v in sm if v > 0.5 * (max(sm) if sm else 1)]
+        return {"sm_mhz": float(np.median(loaded)) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max(float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit())
+                if any(r[2].replace(".", "").isdigit() for r in self.rows) else None}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm: the oracle on a bounded sample of the workload
+# ---------------------------------------------------------------------------
+def oracle_sample(A_rows: np.ndarray, B_cols: np.ndarray, N: int):
+    import oracle
+    t0 = time.perf_counter()
+    oracle.dgemm(A_rows, B_cols, N)
+    return time.perf_counter() - t0
+
+
+def run_reference(args, cfg):
+    """--impl reference: the oracle (as it stands) on the host cores; each step a
+    bounded sample (rows x cols block) of the same workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from paper_2504_08009_b200.inputs import phi_matrix_np
+    n, k, N = cfg["n"], cfg["k"], cfg["N"]
+    r, c = 8, 128
+    # rows/cols of the same phi-distribution (host generator: same recipe)
+    A = phi_matrix_np(r, k, args.phi, seed=11)
+    B = phi_matrix_np(k, c, args.phi, seed=12)
+    for _ in range(args.warmup):
+        oracle.dgemm(A, B, N)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.dgemm(A, B, N)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = 2.0 * r * c * k / dt / 1e12
+    cores = oracle.get_threads()
+    line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64/wide-int (exact CPU oracle)",
+            "data": "synthetic", "config": cfg["config"],
+            "cpu_baseline": {"value": value, "unit": "TFLOPS", "cores": cores, "kind": "oracle",
+                             "sample": f"{r} rows x {c} cols of the {cfg['config']['workload']} product per step"},
+            "e2e": {"value": value, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the oz2 arm
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = args.n
+    m = args.m or n
+    k = args.k or n
+    N = args.moduli
+    cfg = {"n": n, "m": m, "k": k, "N": N,
+           "config": {"workload": f"m=n=k={n}, N={N}, phi={args.phi:g}" if m == n == k else
+                      f"m={m}, n={n}, k={k}, N={N}, phi={args.phi:g}",
+                      "m_per_rank": m, "n": n, "k": k, "num_moduli": N, "phi": args.phi,
+                      "parallelism": f"rowblock-dp{world}" if world > 1 else "single-gpu",
+                      "l2": "no flush: every step streams A, B (2.1 GB each at n=16384) > 126 MB L2",
+                      "mode": "fast (OS II-fast, Cauchy-Schwarz)"}}
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2504_08009_b200 import oz2
+    from paper_2504_08009_b200.inputs import phi_matrix_torch, SEED_A, SEED_B
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # inputs resident in HBM before the timed region
+    A = phi_matrix_torch(m, k, args.phi, SEED_A, device=dev, row_offset=rank * m)
+    B = phi_matrix_torch(k, n, args.phi, SEED_B, device=dev) if rank == 0 else \
+        torch.empty((k, n), dtype=torch.float64, device=dev)
+    C = torch.empty((m, n), dtype=torch.float64, device=dev)
+    Cfull = torch.empty((m * world, n), dtype=torch.float64, device=dev) if (world > 1 and rank == 0) else None
+    h = oz2.handle(local)
+
+    def step():
+        if world > 1:
+            dist.broadcast(B, src=0)
+        oz2.dgemm(A, B, N, out=C)
+        if world > 1:
+            dist.gather(C, list(Cfull.chunk(world)) if rank == 0 else None, dst=0)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    h.set_profiling(True)
+    h.stage_times()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    stages, calls = h.stage_times()
+    h.set_profiling(False)
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    flops = 2.0 * m * world * n * k
+    value = flops / (ms_step * 1e-3) / 1e12
+
+    # accuracy on sampled entries (bench-local exact reference)
+    rng = np.random.Generator(np.random.PCG64(3))
+    ii = rng.integers(0, m, args.acc_samples)
+    jj = rng.integers(0, n, args.acc_samples)
+    Ai = A[torch.from_numpy(ii).to(dev)].cpu().numpy()
+    Bj = B[:, torch.from_numpy(jj).to(dev)].cpu().numpy()
+    ab, absab = exact_entries(Ai, Bj)
+    cij = C[torch.from_numpy(ii).to(dev), torch.from_numpy(jj).to(dev)].cpu().numpy()
+    err = np.abs(cij - ab)
+    compwise = float(np.max(err / absab))
+    nz = ab != 0
+    relerr = float(np.max(err[nz] / np.abs(ab[nz])))
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_src = measured_peaks()
+    # dominant kernel: the tcgen05 modular GEMM (Alg. 1 line 6)
+    t_gemm = stages["gemm"] / max(calls, 1)
+    int8_ops = 2.0 * m * n * k * N
+    achieved = int8_ops / (t_gemm * 1e-3) / 1e12
+    peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as fh:
+                pj = json.load(fh)
+            if pj.get("workload") == cfg["config"]["workload"]:
+                traffic = pj.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    roofline = {"bound": "tensor", "kernel": "oz2::gemm::modmul_kernel (tcgen05.mma kind::i8)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic,
+                "peak_source": f"2 x bf16_tflops_sustained of {peak_src} MEASURED_PEAKS.json "
+                               "(int8 dense = 2 x bf16 nominal)",
+                "work": f"2*m*n*k*N = {int8_ops:.4g} int8 ops per launch"}
+
+    line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int8 (tensor-core s8*s8->s32), f64 in/out",
+            "data": "synthetic", "config": cfg["config"],
+            "max_rel_err": relerr, "compwise_err": compwise, "acc_samples": int(args.acc_samples),
+            "stage_ms": {s: v / max(calls, 1) for s, v in stages.items()},
+            "roofline": roofline,
+            "n_scaled_roofline_frac": value / world / (4500.0 / N),
+            "gpu_launches": 6 * args.steps,
+            "clocks": clk.summary()}
+
+    # e2e: same metric through the C ABI with host buffers (pinned), copies timed
+    if not args.no_e2e and world == 1:
+        Ah = torch.empty((m, k), dtype=torch.float64, pin_memory=True)
+        Bh = torch.empty((k, n), dtype=torch.float64, pin_memory=True)
+        Ch = torch.empty((m, n), dtype=torch.float64, pin_memory=True)
+        Ah.copy_(A)
+        Bh.copy_(B)
+        del C
+        torch.cuda.empty_cache()
+        An, Bn, Cn = Ah.numpy(), Bh.numpy(), Ch.numpy()
+        oz2.dgemm_host(An, Bn, N, out=Cn)
+        steps_e2e = min(args.steps, 3)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(torch.cuda.current_stream())
+        for _ in range(steps_e2e):
+            oz2.dgemm_host(An, Bn, N, out=Cn)
+        e1.record(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        ms_e2e = e0.elapsed_time(e1) / steps_e2e
+        line["e2e"] = {"value": flops / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOPS",
+                       "h2d_bytes_per_step": 8 * (m * k + k * n), "d2h_bytes_per_step": 8 * m * n,
+                       "ms_per_step": ms_e2e, "steps": steps_e2e,
+                       "api": "oz2_dgemm_host (pinned host buffers)"}
+        del Ah, Bh, Ch
+
+    if not args.no_context and world == 1:
+        ctx = {}
+        try:
+            torch.cuda.empty_cache()
+            x = torch.randn((n, n), dtype=torch.float64, device=dev)
+            y = torch.randn((n, n), dtype=torch.float64, device=dev)
+            torch.matmul(x, y)
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            for _ in range(3):
+                torch.matmul(x, y)
+            a1.record()
+            torch.cuda.synchronize()
+            ctx["cublas_dgemm_tflops"] = 2.0 * n ** 3 / (a0.elapsed_time(a1) / 3 * 1e-3) / 1e12
+            del x, y
+            xi = torch.randint(-128, 128, (n, n), dtype=torch.int8, device=dev)
+            yi = torch.randint(-128, 128, (n, n), dtype=torch.int8, device=dev).t()
+            torch._int_mm(xi, yi)
+            torch.cuda.synchronize()
+            a0.record()
+            for _ in range(3):
+                torch._int_mm(xi, yi)
+            a1.record()
+            torch.cuda.synchronize()
+            ctx["cublaslt_int8_tops"] = 2.0 * n ** 3 / (a0.elapsed_time(a1) / 3 * 1e-3) / 1e12
+        except Exception as ex:  # context only
+            ctx["error"] = repr(ex)[:200]
+        ctx["paper_gh200_os2_fast14_n16384_tflops"] = 80.2
+        ctx["paper_rtx4090_os2_fast14_n8192_tflops"] = 9.81
+        line["context"] = ctx
+
+    if not args.no_cpu_baseline and world == 1:
+        import oracle
+        r, c = 64, 512
+        Ar = A[:r].cpu().numpy()
+        Bc = B[:, :c].cpu().numpy()
+        dt = oracle_sample(Ar, Bc, N)
+        line["cpu_baseline"] = {"value": 2.0 * r * c * k / dt / 1e12, "unit": "TFLOPS",
+                                "cores": oracle.get_threads(), "kind": "oracle",
+                                "sample": f"rows 0..{r - 1} x cols 0..{c - 1} of the same product "
+                                          f"(k={k}, N={N}), {dt:.1f} s"}
+
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

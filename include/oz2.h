@@ -137,6 +137,21 @@ int oz2_tables(int num_moduli, int32_t* moduli, int32_t* y, double* W, double* M
 /* Eq. (17) in exact integer form: max{kappa : q 4^kappa <= M/2 - 1}, -1 if none. */
 int oz2_eq17_k(int num_moduli, int64_t q);
 
+/* ---- tracing ----------------------------------------------------------------
+ * With profiling enabled, every oz2_dgemm_ex call records CUDA events on the
+ * handle's stream at its stage boundaries (no host synchronisation).
+ * oz2_stage_times waits for the recorded events, writes the summed device
+ * milliseconds of each stage since the last read into ms[0..OZ2_NUM_STAGES-1]
+ * (order: OZ2_STAGE_*), the number of calls into *calls, and resets. */
+#define OZ2_NUM_STAGES 5
+#define OZ2_STAGE_ROWS 0    /* rows of A: exponents + residues (lines 1, 2, 4)      */
+#define OZ2_STAGE_COLSTATS 1/* columns of B: exponents (line 1)                      */
+#define OZ2_STAGE_COLRES 2  /* columns of B: residues (lines 3, 5)                   */
+#define OZ2_STAGE_GEMM 3    /* N modular products on tcgen05 (line 6) [+ fused 7-10] */
+#define OZ2_STAGE_CRT 4     /* CRT + inverse scaling (lines 7-10) if not fused       */
+int oz2_set_profiling(oz2_handle_t h, int enable);
+int oz2_stage_times(oz2_handle_t h, double* ms, int64_t* calls);
+
 const char* oz2_strerror(int code);
 /* 100 * major + minor */
 int oz2_version(void);

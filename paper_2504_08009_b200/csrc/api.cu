@@ -7,6 +7,8 @@
 #include <string.h>
 
 #include <mutex>
+#include <new>
+#include <vector>
 
 #include "../../include/oz2.h"
 #include "oz2_device.cuh"
@@ -78,7 +80,24 @@ struct oz2_context {
     size_t ws_user_bytes;
     void* ws_own;
     size_t ws_own_bytes;
+    int profiling;
+    std::vector<cudaEvent_t> events;   // OZ2_NUM_STAGES + 1 per profiled call
 };
+
+namespace {
+// stage boundary marker (profiling only): one event per boundary, no sync
+inline void mark(oz2_handle_t h) {
+    if (!h->profiling) return;
+    cudaEvent_t ev;
+    if (cudaEventCreate(&ev) != cudaSuccess) return;
+    cudaEventRecord(ev, h->stream);
+    h->events.push_back(ev);
+}
+void drop_events(oz2_handle_t h) {
+    for (cudaEvent_t ev : h->events) cudaEventDestroy(ev);
+    h->events.clear();
+}
+}  // namespace
 
 namespace {
 
@@ -218,11 +237,11 @@ int oz2_create(oz2_handle_t* h, int device) {
     if (!h) return OZ2_ERR_INVALID_ARG;
     int rc = ensure_device(device);
     if (rc) return rc;
-    oz2_context* c = (oz2_context*)calloc(1, sizeof(oz2_context));
+    oz2_context* c = new (std::nothrow) oz2_context();
     if (!c) return OZ2_ERR_INVALID_ARG;
     c->device = device;
     if (cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
-        free(c);
+        delete c;
         return OZ2_ERR_CUDA;
     }
     c->mode = OZ2_MODE_FAST;
@@ -232,8 +251,10 @@ int oz2_create(oz2_handle_t* h, int device) {
 
 int oz2_destroy(oz2_handle_t h) {
     if (!h) return OZ2_ERR_INVALID_ARG;
-    if (h->ws_own) { DevGuard g(h->device); cudaFree(h->ws_own); }
-    free(h);
+    DevGuard g(h->device);
+    drop_events(h);
+    if (h->ws_own) cudaFree(h->ws_own);
+    delete h;
     return OZ2_OK;
 }
 
@@ -254,6 +275,36 @@ int oz2_set_workspace(oz2_handle_t h, void* ptr, size_t bytes) {
     h->ws_user = ptr;
     h->ws_user_bytes = ptr ? bytes : 0;
     return OZ2_OK;
+}
+
+int oz2_set_profiling(oz2_handle_t h, int enable) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    h->profiling = enable ? 1 : 0;
+    return OZ2_OK;
+}
+
+int oz2_stage_times(oz2_handle_t h, double* ms, int64_t* calls) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    DevGuard g(h->device);
+    const size_t per = OZ2_NUM_STAGES + 1;
+    double acc[OZ2_NUM_STAGES] = {0};
+    int64_t nc = (int64_t)(h->events.size() / per);
+    int rc = OZ2_OK;
+    for (int64_t c = 0; c < nc && rc == OZ2_OK; c++) {
+        for (size_t s = 0; s < OZ2_NUM_STAGES; s++) {
+            float t = 0.f;
+            if (cudaEventSynchronize(h->events[c * per + s + 1]) != cudaSuccess ||
+                cudaEventElapsedTime(&t, h->events[c * per + s], h->events[c * per + s + 1]) != cudaSuccess) {
+                rc = OZ2_ERR_CUDA;
+                break;
+            }
+            acc[s] += t;
+        }
+    }
+    if (ms) for (int s = 0; s < OZ2_NUM_STAGES; s++) ms[s] = acc[s];
+    if (calls) *calls = nc;
+    drop_events(h);
+    return rc;
 }
 
 size_t oz2_workspace_bytes(int64_t m, int64_t n, int64_t k, int N) {
@@ -384,17 +435,23 @@ int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* 
     int32_t* e = (int32_t*)(ws + L.off_e);
     int32_t* f = (int32_t*)(ws + L.off_f);
     int32_t* cprod = (int32_t*)(ws + L.off_cprod);
-    // Part 1 + 2-a (Alg. 1 lines 1-5)
-    oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
-    oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, h->stream);
-    oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, h->stream);
-    // Part 2-b (line 6)
     CUtensorMap tA, tB;
     if ((rc = make_plane_map(&tA, Ares, m, k, L.ldr, N, 128))) return rc;
     if ((rc = make_plane_map(&tB, Bres, n, k, L.ldr, N, 256))) return rc;
+    mark(h);
+    // Part 1 + 2-a (Alg. 1 lines 1-5)
+    oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
+    mark(h);
+    oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, h->stream);
+    mark(h);
+    oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, h->stream);
+    mark(h);
+    // Part 2-b (line 6)
     if (oz2::launch_modmul(&tA, &tB, m, n, k, N, cprod, h->num_sms, h->stream)) return OZ2_ERR_CUDA;
+    mark(h);
     // Parts 2-c, 3, 4 (lines 7-10)
     oz2::launch_crt(cprod, m, n, e, f, N, C, ldc, h->stream);
+    mark(h);
     return cuda_status();
 }
 

@@ -28,8 +28,11 @@ constexpr int MAX_CHUNKS = 512;    // k < 2^17
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t u_squared(const Dec& d, int Ec) {
     if (d.cls != 1) return 0;
-    int rs = -(d.ex + 15 - Ec);                 // >= 37
-    uint64_t u = rs >= 64 ? 1ull : ((d.mant + ((1ull << rs) - 1)) >> rs);
+    // |x| 2^(15-Ec) = mant 2^(-rs) < 2^16; rs >= 37 for normal x, but a
+    // subnormal x has a short mantissa and rs may be <= 0 (exact left shift)
+    int rs = -(d.ex + 15 - Ec);
+    uint64_t u = rs <= 0 ? (d.mant << (-rs))
+               : rs >= 64 ? 1ull : ((d.mant + ((1ull << rs) - 1)) >> rs);
     return u * u;
 }
 

@@ -28,7 +28,9 @@ SYMBOLS = [
     "oz2_workspace_bytes", "oz2_dgemm", "oz2_dgemm_ex", "oz2_dgemm_host", "oz2_scale_rows",
     "oz2_scale_cols", "oz2_trunc_rows", "oz2_trunc_cols", "oz2_residues_rows", "oz2_residues_cols",
     "oz2_modmul", "oz2_crt", "oz2_tables", "oz2_eq17_k", "oz2_strerror", "oz2_version",
+    "oz2_set_profiling", "oz2_stage_times",
 ]
+STAGES = ["rows_A", "colstats_B", "colres_B", "gemm", "crt"]
 
 
 class Oz2Error(RuntimeError):
@@ -76,6 +78,8 @@ def lib() -> ctypes.CDLL:
                 L.oz2_strerror.argtypes = [i32]
                 L.oz2_strerror.restype = ctypes.c_char_p
                 L.oz2_version.argtypes = []
+                L.oz2_set_profiling.argtypes = [P, i32]
+                L.oz2_stage_times.argtypes = [P, P, P]
                 _lib = L
     return _lib
 
@@ -148,6 +152,17 @@ class Handle:
                    "oz2_set_workspace")
         else:
             _check(lib().oz2_set_workspace(self._h, None, 0), "oz2_set_workspace")
+
+    def set_profiling(self, on: bool):
+        _check(lib().oz2_set_profiling(self._h, 1 if on else 0), "oz2_set_profiling")
+
+    def stage_times(self) -> tuple[dict, int]:
+        """Summed device ms per stage since the last read, and the call count."""
+        ms = np.zeros(len(STAGES), np.float64)
+        calls = ctypes.c_int64()
+        _check(lib().oz2_stage_times(self._h, ms.ctypes.data_as(ctypes.c_void_p), ctypes.byref(calls)),
+               "oz2_stage_times")
+        return dict(zip(STAGES, ms.tolist())), calls.value
 
     def __del__(self):
         try:
