@@ -105,10 +105,10 @@ inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
     int64_t ldr;
-    size_t off_Ares, off_Bres, off_e, off_f, off_stats, off_cprod, total;
+    size_t off_Ares, off_Bres, off_e, off_f, off_stats, off_scratch, total;
 };
 
-Layout layout_for(int64_t m, int64_t n, int64_t k, int N) {
+Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms) {
     Layout L;
     L.ldr = round_up(k > 0 ? k : 1, 16);
     size_t off = 0;
@@ -118,7 +118,7 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int N) {
     L.off_e = take(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));
     L.off_f = take(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
     L.off_stats = take(oz2::cols_stats_bytes(k, n));
-    L.off_cprod = take(sizeof(int32_t) * (size_t)N * (size_t)m * (size_t)n);
+    L.off_scratch = take(oz2::fused_scratch_bytes(m, n, N, num_sms));
     L.total = off;
     return L;
 }
@@ -309,7 +309,13 @@ int oz2_stage_times(oz2_handle_t h, double* ms, int64_t* calls) {
 
 size_t oz2_workspace_bytes(int64_t m, int64_t n, int64_t k, int N) {
     if (m < 0 || n < 0 || k < 0 || N < 2 || N > OZ2_MAX_MODULI) return 0;
-    return layout_for(m, n, k, N).total;
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+        cudaGetLastError();
+        sms = 160;                                   // conservative (> 148) without a device
+    }
+    return layout_for(m, n, k, N, sms).total;
 }
 
 // ---------------------------------------------------------------------------
@@ -419,22 +425,22 @@ int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* 
     if (rc) return rc;
     if (lda < (k > 0 ? k : 1) || ldb < (n > 0 ? n : 1) || ldc < (n > 0 ? n : 1)) return OZ2_ERR_INVALID_ARG;
     if (m == 0 || n == 0) return OZ2_OK;
-    if (!A || !B || !C) return OZ2_ERR_INVALID_ARG;
-    int kstar;
-    if ((rc = kstar_for(h, N, k, &kstar))) return rc;
+    if (!C || (k > 0 && (!A || !B))) return OZ2_ERR_INVALID_ARG;
+    int kstar = 0;
+    if (k > 0 && (rc = kstar_for(h, N, k, &kstar))) return rc;
     DevGuard g(h->device);
     if (k == 0) {
         cudaError_t e = cudaMemset2DAsync(C, sizeof(double) * ldc, 0, sizeof(double) * n, m, h->stream);
         return e == cudaSuccess ? OZ2_OK : OZ2_ERR_CUDA;
     }
-    Layout L = layout_for(m, n, k, N);
+    Layout L = layout_for(m, n, k, N, h->num_sms);
     uint8_t* ws;
     if ((rc = get_workspace(h, L.total, &ws))) return rc;
     int8_t* Ares = (int8_t*)(ws + L.off_Ares);
     int8_t* Bres = (int8_t*)(ws + L.off_Bres);
     int32_t* e = (int32_t*)(ws + L.off_e);
     int32_t* f = (int32_t*)(ws + L.off_f);
-    int32_t* cprod = (int32_t*)(ws + L.off_cprod);
+    uint8_t* scratch = ws + L.off_scratch;
     CUtensorMap tA, tB;
     if ((rc = make_plane_map(&tA, Ares, m, k, L.ldr, N, 128))) return rc;
     if ((rc = make_plane_map(&tB, Bres, n, k, L.ldr, N, 256))) return rc;
@@ -446,12 +452,11 @@ int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* 
     mark(h);
     oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, h->stream);
     mark(h);
-    // Part 2-b (line 6)
-    if (oz2::launch_modmul(&tA, &tB, m, n, k, N, cprod, h->num_sms, h->stream)) return OZ2_ERR_CUDA;
+    // Part 2-b (line 6) with Parts 2-c, 3, 4 (lines 7-10) fused into the epilogue
+    if (oz2::launch_modmul_fused(&tA, &tB, m, n, k, N, scratch, e, f, C, ldc, h->num_sms, h->stream))
+        return OZ2_ERR_CUDA;
     mark(h);
-    // Parts 2-c, 3, 4 (lines 7-10)
-    oz2::launch_crt(cprod, m, n, e, f, N, C, ldc, h->stream);
-    mark(h);
+    mark(h);                                          // (no separate CRT stage)
     return cuda_status();
 }
 
@@ -479,7 +484,7 @@ int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
     if (m == 0 || n == 0) return OZ2_OK;
     DevGuard g(h->device);
     // device staging buffers live after the dgemm workspace
-    Layout L = layout_for(m, n, k, N);
+    Layout L = layout_for(m, n, k, N, h->num_sms);
     size_t bytesA = sizeof(double) * (size_t)m * (size_t)(k > 0 ? k : 1);
     size_t bytesB = sizeof(double) * (size_t)(k > 0 ? k : 1) * (size_t)n;
     size_t bytesC = sizeof(double) * (size_t)m * (size_t)n;

@@ -91,22 +91,30 @@ __device__ __forceinline__ double u192_to_double_scaled(U192 X, int sc) {
     return ldexp(r, sc);                                 // subnormal / extreme: one rounding
 }
 
+// line 7: c'' = c' - floor(c'/m_t) m_t in [0, m_t), for |c'| <= 2^31
 template <int NM>
-__device__ __forceinline__ double crt_element(const int32_t (&cp)[NM], int ei, int fj) {
+__device__ __forceinline__ uint32_t reduce_line7(int32_t c, int t) {
+    const Oz2Table& T = c_tab[NM];
+    const double v = (double)c;
+    const double mt = (double)T.m[t];
+    double q = floor(v * T.inv_m[t]);                // off by at most one
+    double r = fma(-q, mt, v);                        // exact
+    r = r < 0.0 ? r + mt : r;
+    r = r >= mt ? r - mt : r;
+    return (uint32_t)__double2uint_rz(r);
+}
+
+// lines 8-10 from the reduced residues r_t = c''_t in [0, m_t)
+template <int NM>
+__device__ __forceinline__ double crt_from_residues(const uint32_t (&r)[NM], int ei, int fj) {
     const Oz2Table& T = c_tab[NM];
     constexpr int P = NM <= 5 ? 1 : (NM <= 10 ? 2 : (NM <= 15 ? 3 : 4));
     double S[4] = {0.0, 0.0, 0.0, 0.0};
     #pragma unroll
     for (int t = 0; t < NM; t++) {
-        // line 7: least non-negative residue
-        const double v = (double)cp[t];
-        double q = floor(v * T.inv_m[t]);
-        double r = fma(-q, (double)T.m[t], v);
-        if (r < 0.0) r += (double)T.m[t];
-        if (r >= (double)T.m[t]) r -= (double)T.m[t];
-        // line 8: exact piece sums
+        const double rt = (double)r[t];
         #pragma unroll
-        for (int p = 0; p < P; p++) S[p] = fma(r, T.W[p][t], S[p]);
+        for (int p = 0; p < P; p++) S[p] = fma(rt, T.W[p][t], S[p]);       // exact piece sums
     }
     // line 9: Q = floor(S/M + 1/2) from the top two pieces (possibly off by one)
     double top = P >= 2 ? fma(S[P - 1], 0x1p40, S[P - 2]) : S[0];
@@ -123,6 +131,14 @@ __device__ __forceinline__ double crt_element(const int32_t (&cp)[NM], int ei, i
     else if (!u192_ge(X, u192_neg(Mh))) X = u192_add(X, Mw);              // X < -M/2
     if (ei == OZ2_EXP_NONFINITE_DEV || fj == OZ2_EXP_NONFINITE_DEV) return __longlong_as_double(0x7ff8000000000000ll);
     return u192_to_double_scaled(X, -(ei + fj));
+}
+
+template <int NM>
+__device__ __forceinline__ double crt_element(const int32_t (&cp)[NM], int ei, int fj) {
+    uint32_t r[NM];
+    #pragma unroll
+    for (int t = 0; t < NM; t++) r[t] = reduce_line7<NM>(cp[t], t);
+    return crt_from_residues<NM>(r, ei, fj);
 }
 
 template <int NM>

@@ -2,6 +2,6 @@
 // __constant__ tables are shared by every kernel without relocatable device code.
 #include "oz2_device.cuh"
 #include "scale.cu"
-#include "gemm.cu"
 #include "crt.cu"
+#include "gemm.cu"
 #include "api.cu"
