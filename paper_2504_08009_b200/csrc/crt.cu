@@ -91,17 +91,22 @@ __device__ __forceinline__ double u192_to_double_scaled(U192 X, int sc) {
     return ldexp(r, sc);                                 // subnormal / extreme: one rounding
 }
 
-// line 7: c'' = c' - floor(c'/m_t) m_t in [0, m_t), for |c'| <= 2^31
+// line 7: c'' = c' - floor(c'/m_t) m_t in [0, m_t), for any int32 c', in
+// integer arithmetic: u = c' mod 2^32 = hi 2^16 + lo, y = hi (2^16 mod m_t) + lo
+// (+ (-2^32) mod m_t when c' < 0) == c' (mod m_t), y < 2^24, then the magic
+// multiply gives floor(y / m_t) exactly.
 template <int NM>
 __device__ __forceinline__ uint32_t reduce_line7(int32_t c, int t) {
     const Oz2Table& T = c_tab[NM];
-    const double v = (double)c;
-    const double mt = (double)T.m[t];
-    double q = floor(v * T.inv_m[t]);                // off by at most one
-    double r = fma(-q, mt, v);                        // exact
-    r = r < 0.0 ? r + mt : r;
-    r = r >= mt ? r - mt : r;
-    return (uint32_t)__double2uint_rz(r);
+    const uint32_t u = (uint32_t)c;
+    const uint32_t y = (u >> 16) * T.k16[t] + (u & 0xffffu) + ((uint32_t)(c >> 31) & T.g32[t]);
+    const uint32_t q = __umulhi(y, T.magic[t]);
+    return y - q * (uint32_t)T.m[t];
+}
+
+// exact uint32 (< 2^52) -> double without the conversion pipe
+__device__ __forceinline__ double u32_to_double(uint32_t r) {
+    return __hiloint2double(0x43300000, (int)r) - 4503599627370496.0;   // (2^52 + r) - 2^52
 }
 
 // lines 8-10 from the reduced residues r_t = c''_t in [0, m_t)
@@ -112,7 +117,7 @@ __device__ __forceinline__ double crt_from_residues(const uint32_t (&r)[NM], int
     double S[4] = {0.0, 0.0, 0.0, 0.0};
     #pragma unroll
     for (int t = 0; t < NM; t++) {
-        const double rt = (double)r[t];
+        const double rt = u32_to_double(r[t]);
         #pragma unroll
         for (int p = 0; p < P; p++) S[p] = fma(rt, T.W[p][t], S[p]);       // exact piece sums
     }

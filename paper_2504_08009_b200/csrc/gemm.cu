@@ -26,6 +26,7 @@
 #include "oz2_kernels.h"
 
 #include <algorithm>
+#include <stdlib.h>
 
 namespace oz2 {
 namespace gemm {
@@ -58,6 +59,8 @@ struct Params {
     int m, n, k, N;
     int num_tm, num_tn, num_kb;
     int max_slots;                  // tiles per CTA per group (scratch slots)
+    int group_tm;                   // tile rows per schedule group
+    int tile_major;                 // 1: all N moduli of a tile back to back
     int32_t* cprod;                 // RAW: [N][m][n]
     uint8_t* scratch;               // FUSED: [grid][max_slots][N][BM*BN]
     double* C;                      // FUSED
@@ -66,11 +69,25 @@ struct Params {
     const int32_t* f;
 };
 
-// Visit every work unit (tm, tn, t, slot, last) of this CTA in schedule order.
+// Visit every work unit (tm, tn, t, slot) of this CTA in schedule order.
+//  modulus-outer (default): for each group of group_tm tile rows, for t, for the
+//    group's tiles j = blockIdx.x + i * gridDim.x (slot i);
+//  tile-major: for each tile j = blockIdx.x + i * gridDim.x (grouped raster), for t (slot 0).
 template <typename F>
 __device__ __forceinline__ void for_each_unit(const Params& p, F&& fn) {
-    for (int g0 = 0; g0 < p.num_tm; g0 += GROUP_TM) {
-        const int gtm = min(GROUP_TM, p.num_tm - g0);
+    if (p.tile_major) {
+        const int tiles = p.num_tm * p.num_tn;
+        for (int j = blockIdx.x; j < tiles; j += gridDim.x) {
+            const int gsz = p.group_tm * p.num_tn;
+            const int g0 = (j / gsz) * p.group_tm;
+            const int gtm = min(p.group_tm, p.num_tm - g0);
+            const int jj = j % gsz;
+            for (int t = 0; t < p.N; t++) fn(g0 + jj % gtm, jj / gtm, t, 0);
+        }
+        return;
+    }
+    for (int g0 = 0; g0 < p.num_tm; g0 += p.group_tm) {
+        const int gtm = min(p.group_tm, p.num_tm - g0);
         const int gtiles = gtm * p.num_tn;
         for (int t = 0; t < p.N; t++) {
             int slot = 0;
@@ -282,34 +299,37 @@ static int launch_nm(const CUtensorMap* tmA, const CUtensorMap* tmB, const Param
 
 }  // namespace gemm
 
-static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int grid) {
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_sms, int* grid_out) {
     using namespace gemm;
     Params p{};
     p.m = (int)m; p.n = (int)n; p.k = (int)k; p.N = N;
     p.num_tm = (int)((m + BM - 1) / BM);
     p.num_tn = (int)((n + BN - 1) / BN);
     p.num_kb = (int)((k + BK - 1) / BK);
-    const int gtiles = min(GROUP_TM, p.num_tm) * p.num_tn;
-    p.max_slots = (gtiles + grid - 1) / grid;
+    p.group_tm = std::max(1, env_int("OZ2_GROUP_TM", GROUP_TM));     // tuning knobs (experiments)
+    p.tile_major = env_int("OZ2_TILE_MAJOR", 0);
+    const int gtiles = p.tile_major ? p.num_tm * p.num_tn : std::min(p.group_tm, p.num_tm) * p.num_tn;
+    const int grid = gtiles < num_sms ? gtiles : num_sms;
+    p.max_slots = p.tile_major ? 1 : (gtiles + grid - 1) / grid;
+    *grid_out = grid;
     return p;
 }
 
-static int grid_for(int64_t m, int64_t n, int num_sms) {
-    using namespace gemm;
-    const int64_t gt = (int64_t)std::min<int64_t>(GROUP_TM, (m + BM - 1) / BM) * ((n + BN - 1) / BN);
-    return (int)(gt < num_sms ? gt : num_sms);
-}
-
 size_t fused_scratch_bytes(int64_t m, int64_t n, int N, int num_sms) {
-    const int grid = grid_for(m, n, num_sms);
-    gemm::Params p = make_params(m, n, 1, N, grid);
+    int grid;
+    gemm::Params p = make_params(m, n, 1, N, num_sms, &grid);
     return (size_t)grid * p.max_slots * N * gemm::TILE_BYTES;
 }
 
 int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                   int N, int32_t* cprod, int num_sms, cudaStream_t st) {
-    const int grid = grid_for(m, n, num_sms);
-    gemm::Params p = make_params(m, n, k, N, grid);
+    int grid;
+    gemm::Params p = make_params(m, n, k, N, num_sms, &grid);
     p.cprod = cprod;
     return gemm::launch_nm<0>(tmA, tmB, p, grid, st);
 }
@@ -317,8 +337,8 @@ int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int
 int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                         int N, uint8_t* scratch, const int32_t* e, const int32_t* f, double* C, int64_t ldc,
                         int num_sms, cudaStream_t st) {
-    const int grid = grid_for(m, n, num_sms);
-    gemm::Params p = make_params(m, n, k, N, grid);
+    int grid;
+    gemm::Params p = make_params(m, n, k, N, num_sms, &grid);
     p.scratch = scratch; p.e = e; p.f = f; p.C = C; p.ldc = ldc;
     switch (N) {
 #define OZ2_CASE(NN) case NN: return gemm::launch_nm<NN>(tmA, tmB, p, grid, st);

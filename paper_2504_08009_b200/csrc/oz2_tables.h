@@ -16,6 +16,8 @@ struct Oz2Table {
     uint32_t magic[OZ2_MAX_MODULI];   // ceil(2^32 / m): floor(y/m) = umulhi(y, magic) for y < 2^24
     int32_t h[OZ2_MAX_MODULI];        // (m - 1) / 2 (odd m): symmetric offset
     uint32_t cw[3][OZ2_MAX_MODULI];   // byte b of cw[w][t] = 2^(8(4w+b)) mod m_t
+    uint32_t k16[OZ2_MAX_MODULI];     // 2^16 mod m_t
+    uint32_t g32[OZ2_MAX_MODULI];     // (-2^32) mod m_t in [0, m_t)
     int32_t g64[OZ2_MAX_MODULI];      // (-2^64) mod m_t in [0, m_t)
     int32_t g96[OZ2_MAX_MODULI];      // (-2^96) mod m_t in [0, m_t)
     double W[4][OZ2_MAX_MODULI];      // w_t = M y_t / m_t = sum_p W[p][t] 2^(40p), W < 2^40

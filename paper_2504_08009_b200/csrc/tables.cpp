@@ -117,6 +117,8 @@ int oz2_build_tables(Oz2Table tabs[OZ2_MAX_MODULI + 1]) {
                 for (int b = 0; b < 4; b++) packed |= (uint32_t)pow2_mod(8 * (4 * w + b), m) << (8 * b);
                 T.cw[w][t] = packed;
             }
+            T.k16[t] = (uint32_t)pow2_mod(16, m);
+            T.g32[t] = (uint32_t)((m - pow2_mod(32, m)) % m);
             T.g64[t] = (int32_t)((m - pow2_mod(64, m)) % m);
             T.g96[t] = (int32_t)((m - pow2_mod(96, m)) % m);
             uint32_t rem;
