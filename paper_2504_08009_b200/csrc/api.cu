@@ -399,7 +399,7 @@ int oz2_modmul(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const int8_t* Ar
     }
     CUtensorMap tA, tB;
     if ((rc = make_plane_map(&tA, Ares, m, k, ld_res, N, 128))) return rc;
-    if ((rc = make_plane_map(&tB, Bres, n, k, ld_res, N, 256))) return rc;
+    if ((rc = make_plane_map(&tB, Bres, n, k, ld_res, N, 256 / oz2::gemm_cta_group()))) return rc;
     if (oz2::launch_modmul(&tA, &tB, m, n, k, N, Cprod, h->num_sms, h->stream)) return OZ2_ERR_CUDA;
     return cuda_status();
 }
@@ -443,7 +443,7 @@ int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* 
     uint8_t* scratch = ws + L.off_scratch;
     CUtensorMap tA, tB;
     if ((rc = make_plane_map(&tA, Ares, m, k, L.ldr, N, 128))) return rc;
-    if ((rc = make_plane_map(&tB, Bres, n, k, L.ldr, N, 256))) return rc;
+    if ((rc = make_plane_map(&tB, Bres, n, k, L.ldr, N, 256 / oz2::gemm_cta_group()))) return rc;
     mark(h);
     // Part 1 + 2-a (Alg. 1 lines 1-5)
     oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
