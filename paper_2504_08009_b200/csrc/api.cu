@@ -105,7 +105,7 @@ inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
     int64_t ldr;
-    size_t off_Ares, off_Bres, off_e, off_f, off_stats, off_scratch, total;
+    size_t off_Ares, off_Bres, off_e, off_f, off_stats, off_scratch, off_sync, total;
 };
 
 Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms) {
@@ -119,6 +119,7 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms) {
     L.off_f = take(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
     L.off_stats = take(oz2::cols_stats_bytes(k, n));
     L.off_scratch = take(oz2::fused_scratch_bytes(m, n, N, num_sms));
+    L.off_sync = take(256);
     L.total = off;
     return L;
 }
@@ -400,7 +401,9 @@ int oz2_modmul(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const int8_t* Ar
     CUtensorMap tA, tB;
     if ((rc = make_plane_map(&tA, Ares, m, k, ld_res, N, 128))) return rc;
     if ((rc = make_plane_map(&tB, Bres, n, k, ld_res, N, 256 / oz2::gemm_cta_group()))) return rc;
-    if (oz2::launch_modmul(&tA, &tB, m, n, k, N, Cprod, h->num_sms, h->stream)) return OZ2_ERR_CUDA;
+    uint8_t* ws;
+    if ((rc = get_workspace(h, 256, &ws))) return rc;
+    if (oz2::launch_modmul(&tA, &tB, m, n, k, N, Cprod, (uint32_t*)ws, h->num_sms, h->stream)) return OZ2_ERR_CUDA;
     return cuda_status();
 }
 
@@ -453,7 +456,8 @@ int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* 
     oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, h->stream);
     mark(h);
     // Part 2-b (line 6) with Parts 2-c, 3, 4 (lines 7-10) fused into the epilogue
-    if (oz2::launch_modmul_fused(&tA, &tB, m, n, k, N, scratch, e, f, C, ldc, h->num_sms, h->stream))
+    if (oz2::launch_modmul_fused(&tA, &tB, m, n, k, N, scratch, e, f, C, ldc, (uint32_t*)(ws + L.off_sync),
+                                 h->num_sms, h->stream))
         return OZ2_ERR_CUDA;
     mark(h);
     mark(h);                                          // (no separate CRT stage)

@@ -78,6 +78,10 @@ struct Params {
     int64_t ldc;
     const int32_t* e;
     const int32_t* f;
+    uint32_t* sync_ctr;             // global progress counter (zeroed before launch), or NULL
+    int sync_kb;                    // k-blocks per progress step
+    int sync_lag;                   // steps a CTA may run ahead of the slowest
+    int sync_steps_max;             // progress steps of the busiest CTA
 };
 
 // Visit every work unit (tm, tn, t, slot) of cluster `cid` (of `ncl`) in schedule order.
@@ -189,10 +193,18 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         // ===================== TMA producer (every CTA) =====================
         if (lane == 0) {
             int stage = 0; uint32_t ph = 0;
+            int step = 0, kb_in_step = 0;          // progress steps issued by this CTA
+            const uint32_t nctas = gridDim.x;
             for_each_unit(p, cid, ncl, [&](int tm, int tn, int t, int) {
                 const int arow = tm * C_::TILE_M + (int)rank * BM;
                 const int brow = tn * BN + (int)rank * C_::B_ROWS;
                 for (int kb = 0; kb < p.num_kb; kb++) {
+                    if (p.sync_ctr && kb_in_step == 0 && step > p.sync_lag) {
+                        // stay within sync_lag steps of the slowest CTA: the grid then
+                        // streams each (wave, modulus) K-slab through L2 roughly once
+                        const uint32_t need = (uint32_t)(step - p.sync_lag) * nctas;
+                        while (ld_acquire_gpu(p.sync_ctr) < need) __nanosleep(64);
+                    }
                     mbar_wait(smem_u32(&s.empty[stage]), ph ^ 1);
                     const uint32_t fb = smem_u32(&s.full[stage]);
                     if (leader) mbar_expect_tx(fb, CG * (C_::A_BYTES + C_::B_BYTES));
@@ -205,8 +217,15 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         tma_load_3d(smem_u32(s.b[stage]), &tmB, fb, kb * BK, brow, t);
                     }
                     if (++stage == C_::STAGES) { stage = 0; ph ^= 1; }
+                    if (p.sync_ctr && ++kb_in_step == p.sync_kb) {
+                        kb_in_step = 0;
+                        step++;
+                        red_add_release_gpu(p.sync_ctr, 1);
+                    }
                 }
             });
+            if (p.sync_ctr && step < p.sync_steps_max)            // retire: never hold others back
+                red_add_release_gpu(p.sync_ctr, (uint32_t)(p.sync_steps_max - step));
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA) =====================
@@ -374,6 +393,21 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
     const int nclusters = num_sms / cg;
     const int ncl = gtiles < nclusters ? gtiles : nclusters;
     p.max_slots = p.tile_major ? 1 : (gtiles + ncl - 1) / ncl;
+    p.sync_kb = env_int("OZ2_SYNC_KB", 32);
+    p.sync_lag = env_int("OZ2_SYNC_LAG", 1);
+    {
+        // busiest CTA: its tiles x N moduli x num_kb k-blocks, in sync_kb steps
+        const int64_t tiles = (int64_t)p.num_tm * p.num_tn;
+        int64_t max_tiles = 0;
+        if (p.tile_major) {
+            max_tiles = (tiles + ncl - 1) / ncl;
+        } else {
+            for (int g0 = 0; g0 < p.num_tm; g0 += p.group_tm)
+                max_tiles += ((int64_t)std::min(p.group_tm, p.num_tm - g0) * p.num_tn + ncl - 1) / ncl;
+        }
+        const int64_t kbs = max_tiles * N * p.num_kb;
+        p.sync_steps_max = p.sync_kb > 0 ? (int)((kbs + p.sync_kb - 1) / p.sync_kb) + 1 : 0;
+    }
     *grid_out = ncl * cg;
     return p;
 }
@@ -385,21 +419,25 @@ size_t fused_scratch_bytes(int64_t m, int64_t n, int N, int num_sms) {
 }
 
 int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
-                  int N, int32_t* cprod, int num_sms, cudaStream_t st) {
+                  int N, int32_t* cprod, uint32_t* sync_ctr, int num_sms, cudaStream_t st) {
     const int cg = gemm_cta_group();
     int grid;
     gemm::Params p = make_params(m, n, k, N, num_sms, cg, &grid);
     p.cprod = cprod;
+    p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
+    if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
     return cg == 2 ? gemm::launch_nm<0, 2>(tmA, tmB, p, grid, st) : gemm::launch_nm<0, 1>(tmA, tmB, p, grid, st);
 }
 
 int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                         int N, uint8_t* scratch, const int32_t* e, const int32_t* f, double* C, int64_t ldc,
-                        int num_sms, cudaStream_t st) {
+                        uint32_t* sync_ctr, int num_sms, cudaStream_t st) {
     const int cg = gemm_cta_group();
     int grid;
     gemm::Params p = make_params(m, n, k, N, num_sms, cg, &grid);
     p.scratch = scratch; p.e = e; p.f = f; p.C = C; p.ldc = ldc;
+    p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
+    if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
     switch (N) {
 #define OZ2_CASE(NN) case NN: return cg == 2 ? gemm::launch_nm<NN, 2>(tmA, tmB, p, grid, st) \
                                              : gemm::launch_nm<NN, 1>(tmA, tmB, p, grid, st);

@@ -212,6 +212,18 @@ __device__ __forceinline__ void mma_commit_cg2(uint32_t bar, uint16_t mask) {
                  :: "r"(bar), "h"(mask) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// global progress counter (keeps persistent CTAs in step for L2 reuse)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void red_add_release_gpu(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ uint32_t dp4a_uu(uint32_t a, uint32_t b, uint32_t c) {
     uint32_t d;
     asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));

@@ -25,12 +25,12 @@ void launch_trunc_cols(const double* B, int64_t k, int64_t n, int64_t ldb, const
 // gemm.cu -- Alg. 1 line 6 on tcgen05 (kind::i8)
 int gemm_cta_group();   // 1 or 2 (CTA pairs, cta_group::2)
 int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
-                  int N, int32_t* cprod, int num_sms, cudaStream_t st);
+                  int N, int32_t* cprod, uint32_t* sync_ctr, int num_sms, cudaStream_t st);
 // + Alg. 1 lines 7-10 fused into the epilogue (uint8 residue scratch, exact CRT)
 size_t fused_scratch_bytes(int64_t m, int64_t n, int N, int num_sms);
 int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                         int N, uint8_t* scratch, const int32_t* e, const int32_t* f, double* C, int64_t ldc,
-                        int num_sms, cudaStream_t st);
+                        uint32_t* sync_ctr, int num_sms, cudaStream_t st);
 
 // crt.cu -- Alg. 1 lines 7-10
 void launch_crt(const int32_t* cprod, int64_t m, int64_t n, const int32_t* e, const int32_t* f,

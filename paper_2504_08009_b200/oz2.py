@@ -335,7 +335,7 @@ def modmul(Ares, Bres, k: int):
     assert Bres.shape[0] == N and Bres.shape[2] == ldr and Ares.is_contiguous() and Bres.is_contiguous()
     out = torch.empty((N, m, n), dtype=torch.int32, device=Ares.device)
     h = handle(Ares.device.index)
-    h.prepare("fast")
+    h.prepare("fast", 4096)
     _check(lib().oz2_modmul(h.ptr, m, n, k, _vp(Ares), _vp(Bres), ldr, N, _vp(out)), "oz2_modmul")
     return out
 
