@@ -23,19 +23,6 @@ constexpr int KC = 256;            // FAST chunk length (reading R4)
 constexpr int ROW_THREADS = 256;
 constexpr int MAX_CHUNKS = 512;    // k < 2^17
 
-// ---------------------------------------------------------------------------
-// FAST-rule per-element contribution: u^2 with u = ceil(mant 2^(ex + 15 - Ec))
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t u_squared(const Dec& d, int Ec) {
-    if (d.cls != 1) return 0;
-    // |x| 2^(15-Ec) = mant 2^(-rs) < 2^16; rs >= 37 for normal x, but a
-    // subnormal x has a short mantissa and rs may be <= 0 (exact left shift)
-    int rs = -(d.ex + 15 - Ec);
-    uint64_t u = rs <= 0 ? (d.mant << (-rs))
-               : rs >= 64 ? 1ull : ((d.mant + ((1ull << rs) - 1)) >> rs);
-    return u * u;
-}
-
 __device__ __forceinline__ uint64_t ceil_shift(uint64_t S, int sh) {
     if (S == 0) return 0;
     if (sh >= 64) return 1;
@@ -94,8 +81,73 @@ __device__ __forceinline__ void to_words(double a, int e, uint32_t (&w)[3], bool
 }
 
 // ---------------------------------------------------------------------------
-// exponent of one row (CTA-wide); x(l) = X[l * s]; result broadcast via smem
+// memory helpers: L2 eviction-priority policies, streaming stores
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double2 ld2_hint(const double* a, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld1_hint(const double* a, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_cs_v2(void* a, uint32_t x, uint32_t y) {
+    asm volatile("st.global.cs.v2.b32 [%0], {%1, %2};" :: "l"(a), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void st_cs_v4(void* a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" :: "l"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// FAST-rule chunk statistics
+//   E_c = ilogb(max |x|): |x| orders like its bit pattern, so take the max of
+//   the sign-cleared bits (Inf/NaN patterns are larger than every finite one);
+//   S_c = sum u^2, u = ceil(|x| 2^(15-E_c)) (>= 1 for x != 0) in FP64: every u
+//   <= 2^16, so u^2 <= 2^32 and a 256-term sum <= 2^40 are exact.
+// ---------------------------------------------------------------------------
+constexpr uint64_t ABS_MASK = 0x7fffffffffffffffull;
+constexpr uint64_t INF_BITS = 0x7ff0000000000000ull;
+
+__device__ __forceinline__ int ilogb_bits(uint64_t b) {      // b != 0, finite, sign clear
+    const int ef = (int)(b >> 52);
+    return ef ? ef - 1023 : (63 - __clzll((long long)b)) - 1074;
+}
+__device__ __forceinline__ uint64_t warp_max64(uint64_t v) {
+    #pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+__device__ __forceinline__ double warp_sumd(double v) {
+    #pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+// 2^(15 - Ec) as s1 * s2 (s2 != 1 only for chunks of subnormals)
+__device__ __forceinline__ void u_scale(int Ec, double& s1, double& s2) {
+    const int sh = 15 - Ec;
+    if (sh <= 1000) { s1 = __longlong_as_double((long long)(sh + 1023) << 52); s2 = 1.0; }
+    else { s1 = 0x1p1000; s2 = __longlong_as_double((long long)(sh - 1000 + 1023) << 52); }
+}
+__device__ __forceinline__ double u_sq(double x, double s1, double s2) {
+    const double u = fmax(1.0, ceil(fabs(x) * s1 * s2));
+    return x != 0.0 ? u * u : 0.0;
+}
+
 struct RowSmem {
     int Ec[MAX_CHUNKS];
     unsigned long long Sc[MAX_CHUNKS];
@@ -103,99 +155,128 @@ struct RowSmem {
     int e;
 };
 
+// combine chunk statistics (warp 0): e = T + 15 - E - h, or EQ17 / zero / non-finite
 template <int MODE>
-__device__ int row_exponent(const double* __restrict__ X, int64_t k, int64_t s, int Tb, int kstar,
-                            RowSmem& sm) {
+__device__ __forceinline__ int combine_chunks(const int* Ec, const unsigned long long* Sc, int nch, int bad,
+                                              int Tb, int kstar) {
+    const int lane = threadIdx.x & 31;
+    int E = INT32_MIN;
+    for (int c = lane; c < nch; c += 32) E = max(E, Ec[c]);
+    E = warp_max(E);
+    int e;
+    if (E == INT32_MIN) {
+        e = 0;                                                // zero row / column
+    } else if (MODE == 0) {
+        uint64_t S = 0;
+        for (int c = lane; c < nch; c += 32)
+            if (Ec[c] != INT32_MIN) S += ceil_shift(Sc[c], 2 * (E - Ec[c]));
+        S = warp_sum64(S);
+        e = Tb + 15 - E - log4_ceil(S);
+    } else {
+        e = kstar - 1 - E;                                    // EQ17 (reading R5)
+    }
+    return bad ? OZ2_EXP_NONFINITE_DEV : e;
+}
+
+// exponent of one row (CTA-wide), first pass over the row; loads keep the row
+// in L2 (evict_last) for the residue pass that follows
+template <int MODE>
+__device__ int row_exponent(const double* __restrict__ X, int64_t k, int Tb, int kstar, RowSmem& sm) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     const int nch = (int)((k + KC - 1) / KC);
+    const bool vec = ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+    const uint64_t pol = l2_evict_last();
     if (threadIdx.x == 0) sm.bad = 0;
     __syncthreads();
     for (int c = warp; c < nch; c += nwarps) {
         double v[KC / 32];
-        int64_t base = (int64_t)c * KC;
-        #pragma unroll
-        for (int j = 0; j < KC / 32; j++) {
-            int64_t l = base + lane + 32 * j;
-            v[j] = l < k ? __ldg(X + l * s) : 0.0;
-        }
-        int E = INT32_MIN;
-        bool bad = false;
-        #pragma unroll
-        for (int j = 0; j < KC / 32; j++) {
-            Dec d = decompose(v[j]);
-            if (d.cls == 2) bad = true;
-            if (d.cls == 1) E = max(E, d.ilogb);
-        }
-        E = warp_max(E);
-        if (__any_sync(0xffffffffu, bad) && lane == 0) sm.bad = 1;
-        uint64_t S = 0;
-        if (MODE == 0 && E != INT32_MIN) {
+        const int64_t base = (int64_t)c * KC;
+        if (vec && base + KC <= k) {
             #pragma unroll
-            for (int j = 0; j < KC / 32; j++) S += u_squared(decompose(v[j]), E);
-            S = warp_sum64(S);
+            for (int j = 0; j < KC / 64; j++) {
+                const double2 p = ld2_hint(X + base + 2 * lane + 64 * j, pol);
+                v[2 * j] = p.x; v[2 * j + 1] = p.y;
+            }
+        } else {
+            #pragma unroll
+            for (int j = 0; j < KC / 32; j++) {
+                const int64_t l = base + lane + 32 * j;
+                v[j] = l < k ? ld1_hint(X + l, pol) : 0.0;
+            }
         }
-        if (lane == 0) { sm.Ec[c] = E; sm.Sc[c] = S; }
+        uint64_t mb = 0;
+        #pragma unroll
+        for (int j = 0; j < KC / 32; j++) {
+            const uint64_t b = (uint64_t)__double_as_longlong(v[j]) & ABS_MASK;
+            mb = b > mb ? b : mb;
+        }
+        mb = warp_max64(mb);
+        int Ec = INT32_MIN;
+        double S = 0.0;
+        if (mb >= INF_BITS) {
+            if (lane == 0) sm.bad = 1;
+        } else if (mb != 0) {
+            Ec = ilogb_bits(mb);
+            if (MODE == 0) {
+                double s1, s2;
+                u_scale(Ec, s1, s2);
+                #pragma unroll
+                for (int j = 0; j < KC / 32; j++) S += u_sq(v[j], s1, s2);
+                S = warp_sumd(S);
+            }
+        }
+        if (lane == 0) { sm.Ec[c] = Ec; sm.Sc[c] = (unsigned long long)S; }
     }
     __syncthreads();
     if (warp == 0) {
-        int E = INT32_MIN;
-        for (int c = lane; c < nch; c += 32) E = max(E, sm.Ec[c]);
-        E = warp_max(E);
-        int e;
-        if (E == INT32_MIN) {
-            e = 0;                                            // zero row
-        } else if (MODE == 0) {
-            uint64_t S = 0;
-            for (int c = lane; c < nch; c += 32)
-                if (sm.Ec[c] != INT32_MIN) S += ceil_shift(sm.Sc[c], 2 * (E - sm.Ec[c]));
-            S = warp_sum64(S);
-            e = Tb + 15 - E - log4_ceil(S);
-        } else {
-            e = kstar - 1 - E;                                // EQ17 (reading R5)
-        }
-        if (sm.bad) e = OZ2_EXP_NONFINITE_DEV;
+        const int e = combine_chunks<MODE>(sm.Ec, sm.Sc, nch, sm.bad, Tb, kstar);
         if (lane == 0) sm.e = e;
     }
     __syncthreads();
     return sm.e;
 }
 
-// residues of row i of A for all N moduli: planes out[t][i][l], 4 elements per thread
+// residues of one row for all N moduli: planes out[t][l], 8 elements per thread
+// per step (64 B loads, 8 B streaming stores per modulus; a warp covers 256
+// consecutive elements and writes 256 contiguous bytes of every plane)
 template <int NM, int WORDS>
 __device__ void row_residues(const double* __restrict__ X, int64_t k, int e, int8_t* __restrict__ out,
                              int64_t plane_stride) {
     const bool vec = ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-    for (int64_t l0 = 4 * (int64_t)threadIdx.x; l0 < k; l0 += 4 * (int64_t)blockDim.x) {
-        double a[4];
-        if (vec && l0 + 4 <= k) {
-            double2 p = __ldg(reinterpret_cast<const double2*>(X + l0));
-            double2 q = __ldg(reinterpret_cast<const double2*>(X + l0 + 2));
-            a[0] = p.x; a[1] = p.y; a[2] = q.x; a[3] = q.y;
+    const uint64_t pol = l2_evict_first();
+    for (int64_t l0 = 8 * (int64_t)threadIdx.x; l0 < k; l0 += 8 * (int64_t)blockDim.x) {
+        double a[8];
+        if (vec && l0 + 8 <= k) {
+            #pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const double2 p = ld2_hint(X + l0 + 2 * j, pol);
+                a[2 * j] = p.x; a[2 * j + 1] = p.y;
+            }
         } else {
             #pragma unroll
-            for (int j = 0; j < 4; j++) a[j] = (l0 + j < k) ? __ldg(X + l0 + j) : 0.0;
+            for (int j = 0; j < 8; j++) a[j] = (l0 + j < k) ? ld1_hint(X + l0 + j, pol) : 0.0;
         }
-        uint32_t w[4][3];
-        bool neg[4];
+        uint32_t w[8][3];
+        bool neg[8];
         #pragma unroll
-        for (int j = 0; j < 4; j++) to_words<WORDS>(a[j], e, w[j], neg[j]);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(out + l0);
+        for (int j = 0; j < 8; j++) to_words<WORDS>(a[j], e, w[j], neg[j]);
         // t = 0: m = 256, the low byte of x
-        dst[0] = pack_lo_bytes(w[0][0], w[1][0], w[2][0], w[3][0]);
+        st_cs_v2(out + l0, pack_lo_bytes(w[0][0], w[1][0], w[2][0], w[3][0]),
+                 pack_lo_bytes(w[4][0], w[5][0], w[6][0], w[7][0]));
         #pragma unroll
         for (int t = 1; t < NM; t++) {
-            uint32_t r0 = residue_odd<NM, WORDS>(t, w[0], neg[0]);
-            uint32_t r1 = residue_odd<NM, WORDS>(t, w[1], neg[1]);
-            uint32_t r2 = residue_odd<NM, WORDS>(t, w[2], neg[2]);
-            uint32_t r3 = residue_odd<NM, WORDS>(t, w[3], neg[3]);
-            *reinterpret_cast<uint32_t*>(out + t * plane_stride + l0) = pack_lo_bytes(r0, r1, r2, r3);
+            uint32_t r[8];
+            #pragma unroll
+            for (int j = 0; j < 8; j++) r[j] = residue_odd<NM, WORDS>(t, w[j], neg[j]);
+            st_cs_v2(out + t * plane_stride + l0, pack_lo_bytes(r[0], r[1], r[2], r[3]),
+                     pack_lo_bytes(r[4], r[5], r[6], r[7]));
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Row kernels (A: m x k, row-major, lda)
+// Row kernels (A: m x k, row-major, lda); one CTA per row
 // ---------------------------------------------------------------------------
 // what: 1 = exponents, 2 = residues (given e), 3 = both
 template <int NM, int WORDS, int MODE>
@@ -208,7 +289,7 @@ rows_kernel(const double* __restrict__ A, int64_t m, int64_t k, int64_t lda, int
     const double* X = A + i * lda;
     int e;
     if (what & 1) {
-        e = row_exponent<MODE>(X, k, 1, c_tab[NM].T, kstar, sm);
+        e = row_exponent<MODE>(X, k, c_tab[NM].T, kstar, sm);
         if (threadIdx.x == 0) e_io[i] = e;
     } else {
         e = e_io[i];
@@ -229,54 +310,55 @@ __global__ void trunc_rows_kernel(const double* __restrict__ A, int64_t m, int64
 // ---------------------------------------------------------------------------
 // Column kernels (B: k x n, row-major, ldb)
 // ---------------------------------------------------------------------------
-// chunk statistics: block (32 columns) x (one KC chunk), 8 warps x 32 rows
+// chunk statistics: block = 32 columns x one KC chunk; 16 warps x 16 rows
+constexpr int CS_WARPS = 16;
 template <int MODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(32 * CS_WARPS)
 cols_stats_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t ldb,
                   int32_t* __restrict__ Ec_out, unsigned long long* __restrict__ Sc_out,
                   int32_t* __restrict__ bad_out) {
-    __shared__ int sE[8][32];
-    __shared__ unsigned long long sS[8][32];
-    __shared__ int sBad[8][32];
+    __shared__ unsigned long long sMax[CS_WARPS][32];
+    __shared__ double sS[CS_WARPS][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t j = (int64_t)blockIdx.x * 32 + lane;
     const int64_t c = blockIdx.y;
-    const int64_t r0 = c * KC + warp * 32;
-    double v[32];
+    const int64_t r0 = c * KC + warp * (KC / CS_WARPS);
+    const uint64_t pol = l2_evict_first();
+    double v[KC / CS_WARPS];
     #pragma unroll
-    for (int q = 0; q < 32; q++) {
-        int64_t l = r0 + q;
-        v[q] = (j < n && l < k) ? __ldg(B + l * ldb + j) : 0.0;
+    for (int q = 0; q < KC / CS_WARPS; q++) {
+        const int64_t l = r0 + q;
+        v[q] = (j < n && l < k) ? ld1_hint(B + l * ldb + j, pol) : 0.0;
     }
-    int E = INT32_MIN;
-    int bad = 0;
+    uint64_t mb = 0;
     #pragma unroll
-    for (int q = 0; q < 32; q++) {
-        Dec d = decompose(v[q]);
-        if (d.cls == 2) bad = 1;
-        if (d.cls == 1) E = max(E, d.ilogb);
+    for (int q = 0; q < KC / CS_WARPS; q++) {
+        const uint64_t b = (uint64_t)__double_as_longlong(v[q]) & ABS_MASK;
+        mb = b > mb ? b : mb;
     }
-    sE[warp][lane] = E;
-    sBad[warp][lane] = bad;
+    sMax[warp][lane] = mb;
     __syncthreads();
-    int Ec = INT32_MIN;
+    uint64_t cm = 0;
     #pragma unroll
-    for (int w = 0; w < 8; w++) Ec = max(Ec, sE[w][lane]);
-    uint64_t S = 0;
-    if (MODE == 0 && Ec != INT32_MIN) {
+    for (int w = 0; w < CS_WARPS; w++) cm = sMax[w][lane] > cm ? sMax[w][lane] : cm;
+    double S = 0.0;
+    const bool finite_nz = cm != 0 && cm < INF_BITS;
+    const int Ec = finite_nz ? ilogb_bits(cm) : INT32_MIN;
+    if (MODE == 0 && finite_nz) {
+        double s1, s2;
+        u_scale(Ec, s1, s2);
         #pragma unroll
-        for (int q = 0; q < 32; q++) S += u_squared(decompose(v[q]), Ec);
+        for (int q = 0; q < KC / CS_WARPS; q++) S += u_sq(v[q], s1, s2);
     }
     sS[warp][lane] = S;
     __syncthreads();
     if (warp == 0 && j < n) {
-        uint64_t St = 0;
-        int b = 0;
+        double St = 0.0;
         #pragma unroll
-        for (int w = 0; w < 8; w++) { St += sS[w][lane]; b |= sBad[w][lane]; }
+        for (int w = 0; w < CS_WARPS; w++) St += sS[w][lane];
         Ec_out[c * n + j] = Ec;
-        Sc_out[c * n + j] = St;
-        if (b) atomicOr(bad_out + j, 1);
+        Sc_out[c * n + j] = (unsigned long long)St;
+        if (cm >= INF_BITS) atomicOr(bad_out + j, 1);
     }
 }
 
@@ -304,47 +386,56 @@ __global__ void cols_finalize_kernel(const int32_t* __restrict__ Ec, const unsig
     f[j] = bad[j] ? OZ2_EXP_NONFINITE_DEV : e;
 }
 
-// residues of B columns into K-major planes out[t][j][l]: thread = column j,
-// 16 consecutive l (one 16-byte store per modulus); block = 32 cols x 128 l
+// residues of B columns into K-major planes out[t][j][l].  Block = 32 columns
+// x 128 rows of B: thread (warp w, lane) converts column j0+lane, rows
+// l0+16w .. l0+16w+15; the residue bytes are transposed through shared memory
+// so that every plane row segment (128 contiguous bytes of K) is written by
+// one full-line warp store.
+constexpr int CR_ROWS = 128;
 template <int NM, int WORDS>
 __global__ void __launch_bounds__(256, 2)
 cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t ldb,
                      const int32_t* __restrict__ f, int8_t* __restrict__ out, int64_t ldr) {
+    // [t][col][128 bytes of k], 16-byte chunks XOR-swizzled by (col & 7)
+    extern __shared__ __align__(16) uint8_t sres[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t j = (int64_t)blockIdx.x * 32 + lane;
-    const int64_t l0 = (int64_t)blockIdx.y * 128 + warp * 16;
-    if (j >= n || l0 >= k) return;
-    const int e = f[j];
-    uint32_t w[16][3];
-    bool neg[16];
-    #pragma unroll
-    for (int q = 0; q < 16; q++) {
-        int64_t l = l0 + q;
-        double a = l < k ? __ldg(B + l * ldb + j) : 0.0;
-        to_words<WORDS>(a, e, w[q], neg[q]);
-    }
-    const int64_t plane = n * ldr;
-    int8_t* dst = out + j * ldr + l0;
-    // l0 < k <= ldr, all multiples of 16: the 16-byte store stays inside the row
+    const int64_t j0 = (int64_t)blockIdx.x * 32;
+    const int64_t l0 = (int64_t)blockIdx.y * CR_ROWS;
+    const int64_t j = j0 + lane;
+    const uint64_t pol = l2_evict_first();
     {
-        uint4 o;
-        o.x = pack_lo_bytes(w[0][0], w[1][0], w[2][0], w[3][0]);
-        o.y = pack_lo_bytes(w[4][0], w[5][0], w[6][0], w[7][0]);
-        o.z = pack_lo_bytes(w[8][0], w[9][0], w[10][0], w[11][0]);
-        o.w = pack_lo_bytes(w[12][0], w[13][0], w[14][0], w[15][0]);
-        *reinterpret_cast<uint4*>(dst) = o;
-    }
-    #pragma unroll
-    for (int t = 1; t < NM; t++) {
-        uint32_t r[16];
+        const int e = j < n ? f[j] : 0;
+        uint32_t w[16][3];
+        bool neg[16];
         #pragma unroll
-        for (int q = 0; q < 16; q++) r[q] = residue_odd<NM, WORDS>(t, w[q], neg[q]);
-        uint4 o;
-        o.x = pack_lo_bytes(r[0], r[1], r[2], r[3]);
-        o.y = pack_lo_bytes(r[4], r[5], r[6], r[7]);
-        o.z = pack_lo_bytes(r[8], r[9], r[10], r[11]);
-        o.w = pack_lo_bytes(r[12], r[13], r[14], r[15]);
-        *reinterpret_cast<uint4*>(dst + t * plane) = o;
+        for (int q = 0; q < 16; q++) {
+            const int64_t l = l0 + warp * 16 + q;
+            const double a = (j < n && l < k) ? ld1_hint(B + l * ldb + j, pol) : 0.0;
+            to_words<WORDS>(a, e, w[q], neg[q]);
+        }
+        const int chunk = warp ^ (lane & 7);                 // swizzled 16-byte chunk within the 128 B row
+        #pragma unroll
+        for (int t = 0; t < NM; t++) {
+            uint32_t r[16];
+            #pragma unroll
+            for (int q = 0; q < 16; q++) r[q] = t == 0 ? w[q][0] : residue_odd<NM, WORDS>(t, w[q], neg[q]);
+            uint4 o;
+            o.x = pack_lo_bytes(r[0], r[1], r[2], r[3]);
+            o.y = pack_lo_bytes(r[4], r[5], r[6], r[7]);
+            o.z = pack_lo_bytes(r[8], r[9], r[10], r[11]);
+            o.w = pack_lo_bytes(r[12], r[13], r[14], r[15]);
+            *reinterpret_cast<uint4*>(sres + ((size_t)(t * 32 + lane) * 128) + chunk * 16) = o;
+        }
+    }
+    __syncthreads();
+    // write out: each warp handles (t, col) rows; lane = 4-byte word of the 128-byte row
+    for (int rowi = warp; rowi < NM * 32; rowi += 8) {
+        const int t = rowi >> 5, col = rowi & 31;
+        if (j0 + col >= n) continue;
+        const int ch = (lane >> 2) ^ (col & 7);
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(sres + (size_t)rowi * 128 + ch * 16 + (lane & 3) * 4);
+        if (l0 + 4 * lane < ldr)                             // stay inside the plane row (ld_res)
+            *reinterpret_cast<uint32_t*>(out + (int64_t)t * n * ldr + (j0 + col) * ldr + l0 + 4 * lane) = v;
     }
 }
 
@@ -372,9 +463,17 @@ static void launch_rows_nm(const double* A, int64_t m, int64_t k, int64_t lda, i
 template <int NM>
 static void launch_cols_res_nm(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
                                int8_t* res, int64_t ldr, cudaStream_t st) {
-    dim3 grid((unsigned)((n + 31) / 32), (unsigned)((k + 127) / 128)), block(256);
+    dim3 grid((unsigned)((n + 31) / 32), (unsigned)((k + CR_ROWS - 1) / CR_ROWS)), block(256);
     constexpr int W = NM <= 16 ? 2 : 3;
-    cols_residues_kernel<NM, W><<<grid, block, 0, st>>>(B, k, n, ldb, f, res, ldr);
+    const size_t smem = (size_t)NM * 32 * 128;
+    static bool attr_done[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !attr_done[dev]) {
+        cudaFuncSetAttribute(cols_residues_kernel<NM, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_done[dev] = true;
+    }
+    cols_residues_kernel<NM, W><<<grid, block, smem, st>>>(B, k, n, ldb, f, res, ldr);
 }
 
 #define OZ2_DISPATCH_N(N, FN, ...)                                                   \
@@ -422,8 +521,8 @@ void launch_cols_exponents(const double* B, int64_t k, int64_t n, int64_t ldb, i
     int32_t* bad = Ec + nch * n;
     cudaMemsetAsync(bad, 0, sizeof(int32_t) * n, st);
     dim3 grid((unsigned)((n + 31) / 32), (unsigned)nch);
-    if (mode == 0) cols_stats_kernel<0><<<grid, 256, 0, st>>>(B, k, n, ldb, Ec, Sc, bad);
-    else cols_stats_kernel<1><<<grid, 256, 0, st>>>(B, k, n, ldb, Ec, Sc, bad);
+    if (mode == 0) cols_stats_kernel<0><<<grid, 32 * CS_WARPS, 0, st>>>(B, k, n, ldb, Ec, Sc, bad);
+    else cols_stats_kernel<1><<<grid, 32 * CS_WARPS, 0, st>>>(B, k, n, ldb, Ec, Sc, bad);
     unsigned g2 = (unsigned)((n + 255) / 256);
     if (mode == 0) cols_finalize_kernel<0><<<g2, 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, host_T(N), kstar, f);
     else cols_finalize_kernel<1><<<g2, 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, host_T(N), kstar, f);
