@@ -20,6 +20,9 @@ struct Oz2Table {
     uint32_t g32[OZ2_MAX_MODULI];     // (-2^32) mod m_t in [0, m_t)
     int32_t g64[OZ2_MAX_MODULI];      // (-2^64) mod m_t in [0, m_t)
     int32_t g96[OZ2_MAX_MODULI];      // (-2^96) mod m_t in [0, m_t)
+    uint32_t G63[OZ2_MAX_MODULI];     // (-2^63) mod m_t: undoes the 2^63 bias of 64-bit residue inputs
+    uint32_t G95[OZ2_MAX_MODULI];     // (-2^95) mod m_t: same for 96-bit inputs
+    uint64_t hmagic[OZ2_MAX_MODULI];  // h_t * magic_t: floor((y + h)/m) = (y * magic + hmagic) >> 32
     double W[4][OZ2_MAX_MODULI];      // w_t = M y_t / m_t = sum_p W[p][t] 2^(40p), W < 2^40
     double Mp[4];                     // M = sum_p Mp[p] 2^(40p)
     double invM;                      // 2^(40(P-2)) / M  (P >= 2),  1/M  (P == 1)

@@ -20,7 +20,7 @@
 namespace oz2 {
 
 constexpr int KC = 256;            // FAST chunk length (reading R4)
-constexpr int ROW_THREADS = 256;
+constexpr int ROW_THREADS = 512;   // fewer rows in flight: each row stays in L2 between its two passes
 constexpr int MAX_CHUNKS = 512;    // k < 2^17
 
 __device__ __forceinline__ uint64_t ceil_shift(uint64_t S, int sh) {
@@ -48,35 +48,42 @@ __device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
 }
 
 // ---------------------------------------------------------------------------
-// Residues of one integer (two's complement words) for modulus index t
+// Residues of one integer x, |x| < 2^62 (WORDS = 2) or < 2^94 (WORDS = 3),
+// held as U = x + 2^63 (resp. 2^95) in 32-bit words: the bias makes U >= 0, so
+// y = G_t + sum_b byte_b(U) (2^(8b) mod m_t) == x (mod m_t) with the per-modulus
+// constant G_t = (-2^63) mod m_t, 0 <= y < 2^20; then the symmetric residue of
+// Eq. (1) is y - m_t floor((y + h_t) / m_t) in [-h_t, h_t], where the floor is
+// one 64-bit multiply-add ((y magic_t + h_t magic_t) >> 32, exact since
+// (y + h_t)(magic_t m_t - 2^32) < 2^32).  The low byte is the int8 residue.
 // ---------------------------------------------------------------------------
 template <int NM, int WORDS>
-__device__ __forceinline__ uint32_t residue_odd(int t, const uint32_t (&w)[3], bool neg) {
+__device__ __forceinline__ uint32_t residue_odd(int t, const uint32_t (&w)[3]) {
     const Oz2Table& T = c_tab[NM];
-    uint32_t acc = (uint32_t)T.h[t] + (neg ? (uint32_t)(WORDS == 2 ? T.g64[t] : T.g96[t]) : 0u);
-    acc = dp4a_uu(w[0], T.cw[0][t], acc);
-    acc = dp4a_uu(w[1], T.cw[1][t], acc);
-    if (WORDS == 3) acc = dp4a_uu(w[2], T.cw[2][t], acc);
-    uint32_t q = __umulhi(acc, T.magic[t]);
-    return acc - q * (uint32_t)T.m[t] - (uint32_t)T.h[t];      // low byte = int8 residue
+    uint32_t y = dp4a_uu(w[0], T.cw[0][t], WORDS == 2 ? T.G63[t] : T.G95[t]);
+    y = dp4a_uu(w[1], T.cw[1][t], y);
+    if (WORDS == 3) y = dp4a_uu(w[2], T.cw[2][t], y);
+    const uint32_t q = (uint32_t)(((uint64_t)y * T.magic[t] + T.hmagic[t]) >> 32);
+    return y - q * (uint32_t)T.m[t];
 }
 
-// x = trunc(2^e a) split into words; returns false-y (zeros) for e = sentinel
+// U = trunc(2^e a) + 2^63 (WORDS = 2) or + 2^95 (WORDS = 3) as words; zeros
+// (residue 0 after the bias is undone... not used) for e = sentinel -> x = 0
 template <int WORDS>
-__device__ __forceinline__ void to_words(double a, int e, uint32_t (&w)[3], bool& neg) {
-    if (e == OZ2_EXP_NONFINITE_DEV) { w[0] = w[1] = w[2] = 0; neg = false; return; }
-    double v = trunc(scale_pow2(a, e));
+__device__ __forceinline__ void to_words(double a, int e, uint32_t (&w)[3]) {
+    double v = e == OZ2_EXP_NONFINITE_DEV ? 0.0 : scale_pow2(a, e);
     if (WORDS == 2) {
-        long long x = __double2ll_rz(v);
-        w[0] = (uint32_t)x; w[1] = (uint32_t)((unsigned long long)x >> 32); w[2] = 0;
-        neg = x < 0;
+        const long long x = __double2ll_rz(v);                  // trunc
+        w[0] = (uint32_t)x;
+        w[1] = (uint32_t)((unsigned long long)x >> 32) ^ 0x80000000u;
+        w[2] = 0;
     } else {
-        double hi = floor(v * 0x1p-32);              // exact
-        double lo = fma(-hi, 0x1p32, v);             // exact, in [0, 2^32)
-        long long h = __double2ll_rz(hi);
+        v = trunc(v);
+        const double hi = floor(v * 0x1p-32);                   // exact
+        const double lo = fma(-hi, 0x1p32, v);                  // exact, in [0, 2^32)
+        const long long h = __double2ll_rz(hi);
         w[0] = __double2uint_rz(lo);
-        w[1] = (uint32_t)h; w[2] = (uint32_t)((unsigned long long)h >> 32);
-        neg = v < 0.0;
+        w[1] = (uint32_t)h;
+        w[2] = (uint32_t)((unsigned long long)h >> 32) ^ 0x80000000u;
     }
 }
 
@@ -258,9 +265,8 @@ __device__ void row_residues(const double* __restrict__ X, int64_t k, int e, int
             for (int j = 0; j < 8; j++) a[j] = (l0 + j < k) ? ld1_hint(X + l0 + j, pol) : 0.0;
         }
         uint32_t w[8][3];
-        bool neg[8];
         #pragma unroll
-        for (int j = 0; j < 8; j++) to_words<WORDS>(a[j], e, w[j], neg[j]);
+        for (int j = 0; j < 8; j++) to_words<WORDS>(a[j], e, w[j]);
         // t = 0: m = 256, the low byte of x
         st_cs_v2(out + l0, pack_lo_bytes(w[0][0], w[1][0], w[2][0], w[3][0]),
                  pack_lo_bytes(w[4][0], w[5][0], w[6][0], w[7][0]));
@@ -268,7 +274,7 @@ __device__ void row_residues(const double* __restrict__ X, int64_t k, int e, int
         for (int t = 1; t < NM; t++) {
             uint32_t r[8];
             #pragma unroll
-            for (int j = 0; j < 8; j++) r[j] = residue_odd<NM, WORDS>(t, w[j], neg[j]);
+            for (int j = 0; j < 8; j++) r[j] = residue_odd<NM, WORDS>(t, w[j]);
             st_cs_v2(out + t * plane_stride + l0, pack_lo_bytes(r[0], r[1], r[2], r[3]),
                      pack_lo_bytes(r[4], r[5], r[6], r[7]));
         }
@@ -387,16 +393,17 @@ __global__ void cols_finalize_kernel(const int32_t* __restrict__ Ec, const unsig
 }
 
 // residues of B columns into K-major planes out[t][j][l].  Block = 32 columns
-// x 128 rows of B: thread (warp w, lane) converts column j0+lane, rows
-// l0+16w .. l0+16w+15; the residue bytes are transposed through shared memory
-// so that every plane row segment (128 contiguous bytes of K) is written by
-// one full-line warp store.
-constexpr int CR_ROWS = 128;
+// x 64 rows of B: thread (warp w, lane) converts column j0+lane, rows
+// l0+8w .. l0+8w+7 (coalesced 256-byte row loads across the warp); the residue
+// bytes are transposed through shared memory so that every 64-byte plane row
+// segment is written by 16 lanes of one warp store (full sectors, no
+// partial-sector read-modify-write in L2).
+constexpr int CR_ROWS = 64;
 template <int NM, int WORDS>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256)
 cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t ldb,
                      const int32_t* __restrict__ f, int8_t* __restrict__ out, int64_t ldr) {
-    // [t][col][128 bytes of k], 16-byte chunks XOR-swizzled by (col & 7)
+    // [t][col][64 bytes of k], 8-byte chunks XOR-swizzled by (col & 7)
     extern __shared__ __align__(16) uint8_t sres[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t j0 = (int64_t)blockIdx.x * 32;
@@ -405,37 +412,33 @@ cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t
     const uint64_t pol = l2_evict_first();
     {
         const int e = j < n ? f[j] : 0;
-        uint32_t w[16][3];
-        bool neg[16];
+        uint32_t w[8][3];
         #pragma unroll
-        for (int q = 0; q < 16; q++) {
-            const int64_t l = l0 + warp * 16 + q;
+        for (int q = 0; q < 8; q++) {
+            const int64_t l = l0 + warp * 8 + q;
             const double a = (j < n && l < k) ? ld1_hint(B + l * ldb + j, pol) : 0.0;
-            to_words<WORDS>(a, e, w[q], neg[q]);
+            to_words<WORDS>(a, e, w[q]);
         }
-        const int chunk = warp ^ (lane & 7);                 // swizzled 16-byte chunk within the 128 B row
+        const int chunk = warp ^ (lane & 7);                 // swizzled 8-byte chunk within the 64 B row
         #pragma unroll
         for (int t = 0; t < NM; t++) {
-            uint32_t r[16];
+            uint32_t r[8];
             #pragma unroll
-            for (int q = 0; q < 16; q++) r[q] = t == 0 ? w[q][0] : residue_odd<NM, WORDS>(t, w[q], neg[q]);
-            uint4 o;
-            o.x = pack_lo_bytes(r[0], r[1], r[2], r[3]);
-            o.y = pack_lo_bytes(r[4], r[5], r[6], r[7]);
-            o.z = pack_lo_bytes(r[8], r[9], r[10], r[11]);
-            o.w = pack_lo_bytes(r[12], r[13], r[14], r[15]);
-            *reinterpret_cast<uint4*>(sres + ((size_t)(t * 32 + lane) * 128) + chunk * 16) = o;
+            for (int q = 0; q < 8; q++) r[q] = t == 0 ? w[q][0] : residue_odd<NM, WORDS>(t, w[q]);
+            *reinterpret_cast<uint2*>(sres + ((size_t)(t * 32 + lane) * 64) + chunk * 8) =
+                make_uint2(pack_lo_bytes(r[0], r[1], r[2], r[3]), pack_lo_bytes(r[4], r[5], r[6], r[7]));
         }
     }
     __syncthreads();
-    // write out: each warp handles (t, col) rows; lane = 4-byte word of the 128-byte row
-    for (int rowi = warp; rowi < NM * 32; rowi += 8) {
+    // write out: 16 lanes per (t, col) row segment of 64 bytes, 2 segments per warp store
+    const int sub = lane >> 4, wl = lane & 15;
+    for (int rowi = 2 * warp + sub; rowi < NM * 32; rowi += 16) {
         const int t = rowi >> 5, col = rowi & 31;
         if (j0 + col >= n) continue;
-        const int ch = (lane >> 2) ^ (col & 7);
-        const uint32_t v = *reinterpret_cast<const uint32_t*>(sres + (size_t)rowi * 128 + ch * 16 + (lane & 3) * 4);
-        if (l0 + 4 * lane < ldr)                             // stay inside the plane row (ld_res)
-            *reinterpret_cast<uint32_t*>(out + (int64_t)t * n * ldr + (j0 + col) * ldr + l0 + 4 * lane) = v;
+        const int ch = (wl >> 1) ^ (col & 7);
+        const uint32_t v = *reinterpret_cast<const uint32_t*>(sres + (size_t)rowi * 64 + ch * 8 + (wl & 1) * 4);
+        if (l0 + 4 * wl < ldr)                               // stay inside the plane row (ld_res)
+            *reinterpret_cast<uint32_t*>(out + (int64_t)t * n * ldr + (j0 + col) * ldr + l0 + 4 * wl) = v;
     }
 }
 
@@ -465,7 +468,7 @@ static void launch_cols_res_nm(const double* B, int64_t k, int64_t n, int64_t ld
                                int8_t* res, int64_t ldr, cudaStream_t st) {
     dim3 grid((unsigned)((n + 31) / 32), (unsigned)((k + CR_ROWS - 1) / CR_ROWS)), block(256);
     constexpr int W = NM <= 16 ? 2 : 3;
-    const size_t smem = (size_t)NM * 32 * 128;
+    const size_t smem = (size_t)NM * 32 * CR_ROWS;
     static bool attr_done[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);

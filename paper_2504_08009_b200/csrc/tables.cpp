@@ -121,6 +121,9 @@ int oz2_build_tables(Oz2Table tabs[OZ2_MAX_MODULI + 1]) {
             T.g32[t] = (uint32_t)((m - pow2_mod(32, m)) % m);
             T.g64[t] = (int32_t)((m - pow2_mod(64, m)) % m);
             T.g96[t] = (int32_t)((m - pow2_mod(96, m)) % m);
+            T.G63[t] = (uint32_t)((m - pow2_mod(63, m)) % m);
+            T.G95[t] = (uint32_t)((m - pow2_mod(95, m)) % m);
+            T.hmagic[t] = (uint64_t)T.h[t] * (uint64_t)T.magic[t];
             uint32_t rem;
             Nat Mt = divmod_small(M, (uint32_t)m, &rem);
             if (rem) return 1;
