@@ -129,9 +129,9 @@ int oz2_crt(oz2_handle_t h, int64_t m, int64_t n, const int32_t* Cprod, const in
 
 /* ---- constants (host memory, no device needed) ----------------------------
  * moduli[N], y[N] (M_t y_t == 1 mod m_t, least positive), W[P*N] with
- * w_t = M y_t / m_t = sum_p W[p*N + t] 2^(40 p), 0 <= W < 2^40, Mp[P] the
+ * w_t = M y_t / m_t = sum_p W[p*N + t] 2^(38 p), 0 <= W < 2^38, Mp[P] the
  * same split of M, *P pieces, *L = floor(log2(M/2 - 1)), *T = floor(L/2).
- * Any output pointer may be NULL.  W must hold 4*N doubles, Mp 4. */
+ * Any output pointer may be NULL.  W must hold 5*N doubles, Mp 5. */
 int oz2_tables(int num_moduli, int32_t* moduli, int32_t* y, double* W, double* Mp,
                int32_t* P, int32_t* L, int32_t* T);
 /* Eq. (17) in exact integer form: max{kappa : q 4^kappa <= M/2 - 1}, -1 if none. */

@@ -30,8 +30,7 @@ EncodeTiledFn g_encode = nullptr;
 void build_tables_once() {
     g_tabs_ok = (oz2_build_tables(g_tabs) == 0);
     for (int N = 2; N <= OZ2_MAX_MODULI && g_tabs_ok; N++) {
-        int P = N <= 5 ? 1 : (N <= 10 ? 2 : (N <= 15 ? 3 : 4));     // kernels assume this
-        if (g_tabs[N].P != P) g_tabs_ok = false;
+        if (g_tabs[N].P != oz2::crt_pieces(N)) g_tabs_ok = false;   // kernels assume this
     }
 }
 
@@ -220,9 +219,9 @@ int oz2_tables(int N, int32_t* moduli, int32_t* y, double* W, double* Mp, int32_
     for (int i = 0; i < N; i++) {
         if (moduli) moduli[i] = t.m[i];
         if (y) y[i] = t.y[i];
-        if (W) for (int p = 0; p < 4; p++) W[p * N + i] = t.W[p][i];
+        if (W) for (int p = 0; p < OZ2_MAX_PIECES; p++) W[p * N + i] = t.W[p][i];
     }
-    if (Mp) for (int p = 0; p < 4; p++) Mp[p] = t.Mp[p];
+    if (Mp) for (int p = 0; p < OZ2_MAX_PIECES; p++) Mp[p] = t.Mp[p];
     if (P) *P = t.P;
     if (L) *L = t.L;
     if (T) *T = t.T;

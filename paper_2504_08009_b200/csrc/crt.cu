@@ -2,8 +2,8 @@
 // PAPER.md:496-502) on sm_100a, exactly:
 //   line 7:  c''_t = c'_t - floor(c'_t / m_t) m_t                 in [0, m_t)
 //   line 8:  S = sum_t c''_t w_t, w_t = M y_t / m_t, held as P FP64 piece sums
-//            S_p = sum_t c''_t W[p][t] (W < 2^40, c'' < 2^8, N <= 20 => every
-//            product < 2^48 and every partial sum < 2^53: exact)
+//            S_p = sum_t c''_t W[p][t] (W < 2^38, c'' < 2^8, N <= 20 => every
+//            product < 2^46 and every partial sum < 2^51: exact)
 //   line 9:  X = S - M floor(S/M + 1/2) (Eq. 1): Q from the top two pieces in
 //            FP64, X_p = S_p - Q M_p exact, X assembled as a 192-bit integer and
 //            corrected by +-M if Q was off by one (so X is exact for every S)
@@ -109,29 +109,60 @@ __device__ __forceinline__ double u32_to_double(uint32_t r) {
     return __hiloint2double(0x43300000, (int)r) - 4503599627370496.0;   // (2^52 + r) - 2^52
 }
 
-// lines 8-10 from the reduced residues r_t = c''_t in [0, m_t)
+// v * 2^s (v < 2^64, s a compile-time multiple of 38 below 192) added to Y, mod 2^192
+template <int S>
+__device__ __forceinline__ U192 u192_add_shl(U192 Y, uint64_t v) {
+    U192 x;
+    if (S == 0) { x.w0 = v; x.w1 = 0; x.w2 = 0; }
+    else if (S < 64) { x.w0 = v << S; x.w1 = v >> (64 - S); x.w2 = 0; }
+    else if (S == 64) { x.w0 = 0; x.w1 = v; x.w2 = 0; }
+    else if (S < 128) { x.w0 = 0; x.w1 = v << (S - 64); x.w2 = v >> (128 - S); }
+    else if (S == 128) { x.w0 = 0; x.w1 = 0; x.w2 = v; }
+    else { x.w0 = 0; x.w1 = 0; x.w2 = v << (S - 128); }
+    return u192_add(Y, x);
+}
+
+template <int P>
+__device__ __forceinline__ U192 assemble_biased(const uint64_t (&b)[5]) {
+    U192 Y = {0, 0, 0};
+    Y = u192_add_shl<0>(Y, b[0]);
+    if (P > 1) Y = u192_add_shl<38>(Y, b[1]);
+    if (P > 2) Y = u192_add_shl<76>(Y, b[2]);
+    if (P > 3) Y = u192_add_shl<114>(Y, b[3]);
+    if (P > 4) Y = u192_add_shl<152>(Y, b[4]);
+    return Y;
+}
+
+// lines 8-10 from the reduced residues r_t = c''_t in [0, m_t):
+//   S_p = sum_t r_t W[p][t] exactly (W < 2^38, r < 2^8, N <= 20: every partial
+//   sum < 2^51); Q ~ S/M rounded (from the top two pieces, within +-1 of
+//   floor(S/M + 1/2)); X_p = S_p - Q M_p with |X_p| < 2^51, so X_p + 1.5*2^52 is
+//   exact and its bit pattern is X_p + 0x4338000000000000: the pieces are
+//   summed as integers, the bias removed, and X corrected by +-M into
+//   [-M/2, M/2) -- the exact Eq. (1) result for every S.
 template <int NM>
 __device__ __forceinline__ double crt_from_residues(const uint32_t (&r)[NM], int ei, int fj) {
     const Oz2Table& T = c_tab[NM];
-    constexpr int P = NM <= 5 ? 1 : (NM <= 10 ? 2 : (NM <= 15 ? 3 : 4));
-    double S[4] = {0.0, 0.0, 0.0, 0.0};
+    constexpr int P = crt_pieces(NM);
+    constexpr double MAGIC = 6755399441055744.0;                 // 1.5 * 2^52
+    double S[P];
+    #pragma unroll
+    for (int p = 0; p < P; p++) S[p] = 0.0;
     #pragma unroll
     for (int t = 0; t < NM; t++) {
         const double rt = u32_to_double(r[t]);
         #pragma unroll
-        for (int p = 0; p < P; p++) S[p] = fma(rt, T.W[p][t], S[p]);       // exact piece sums
+        for (int p = 0; p < P; p++) S[p] = fma(rt, T.W[p][t], S[p]);       // exact
     }
-    // line 9: Q = floor(S/M + 1/2) from the top two pieces (possibly off by one)
-    double top = P >= 2 ? fma(S[P - 1], 0x1p40, S[P - 2]) : S[0];
-    double Q = floor(fma(top, T.invM, 0.5));
-    U192 X = u192_from_i64(0);
+    const double top = P >= 2 ? fma(S[P - 1], 0x1p38, S[P - 2]) : S[0];
+    const double Q = fma(top, T.invM, MAGIC) - MAGIC;                       // rint(S / M), approximately
+    uint64_t b[5] = {0, 0, 0, 0, 0};
     #pragma unroll
-    for (int p = 0; p < P; p++) {
-        long long xp = __double2ll_rn(fma(-Q, T.Mp[p], S[p]));        // exact, |.| < 2^53
-        X = u192_add(X, u192_shl_i64(xp, 40 * p));
-    }
-    U192 Mw = {T.Mw[0], T.Mw[1], T.Mw[2]};
-    U192 Mh = {T.Mhalf[0], T.Mhalf[1], T.Mhalf[2]};
+    for (int p = 0; p < P; p++) b[p] = (uint64_t)__double_as_longlong(fma(-Q, T.Mp[p], S[p] + MAGIC));
+    U192 X = assemble_biased<P>(b);
+    X = u192_add(X, u192_neg(U192{T.bias[0], T.bias[1], T.bias[2]}));
+    const U192 Mw = {T.Mw[0], T.Mw[1], T.Mw[2]};
+    const U192 Mh = {T.Mhalf[0], T.Mhalf[1], T.Mhalf[2]};
     if (u192_ge(X, Mh)) X = u192_add(X, u192_neg(Mw));                   // X >= M/2
     else if (!u192_ge(X, u192_neg(Mh))) X = u192_add(X, Mw);              // X < -M/2
     if (ei == OZ2_EXP_NONFINITE_DEV || fj == OZ2_EXP_NONFINITE_DEV) return __longlong_as_double(0x7ff8000000000000ll);

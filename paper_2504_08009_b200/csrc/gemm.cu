@@ -69,12 +69,10 @@ struct __align__(1024) Smem {
 struct Params {
     int m, n, k, N;
     int num_tm, num_tn, num_kb;     // tiles of TILE_M x BN
-    int max_slots;                  // tiles per CTA per group (scratch slots)
-    int group_tm;                   // tile rows per schedule group
-    int tile_major;                 // 1: all N moduli of a tile back to back
+    int group_tm;                   // tile rows per raster group
     int epi_nop;                    // experiment only: epilogue drains TMEM and does nothing else
     int32_t* cprod;                 // RAW: [N][m][n]
-    uint8_t* scratch;               // FUSED: [grid][max_slots][N][BM*BN]
+    uint8_t* scratch;               // FUSED: [grid][2 slots][N][BM*BN] uint8 residues
     double* C;                      // FUSED
     int64_t ldc;
     const int32_t* e;
@@ -85,27 +83,18 @@ struct Params {
     int sync_steps_max;             // progress steps of the busiest CTA
 };
 
-// Visit every work unit (tm, tn, t, slot) of cluster `cid` (of `ncl`) in schedule order.
+// Visit every work unit (tm, tn, t) of cluster `cid` (of `ncl`) in schedule
+// order: tiles j = cid, cid + ncl, ... (raster groups of group_tm tile rows so
+// concurrent tiles share A and B panels in L2), all N moduli of a tile back to back.
 template <typename F>
 __device__ __forceinline__ void for_each_unit(const Params& p, int cid, int ncl, F&& fn) {
-    if (p.tile_major) {
-        const int tiles = p.num_tm * p.num_tn;
-        const int gsz = p.group_tm * p.num_tn;
-        for (int j = cid; j < tiles; j += ncl) {
-            const int g0 = (j / gsz) * p.group_tm;
-            const int gtm = min(p.group_tm, p.num_tm - g0);
-            const int jj = j % gsz;
-            for (int t = 0; t < p.N; t++) fn(g0 + jj % gtm, jj / gtm, t, 0);
-        }
-        return;
-    }
-    for (int g0 = 0; g0 < p.num_tm; g0 += p.group_tm) {
+    const int tiles = p.num_tm * p.num_tn;
+    const int gsz = p.group_tm * p.num_tn;
+    for (int j = cid; j < tiles; j += ncl) {
+        const int g0 = (j / gsz) * p.group_tm;
         const int gtm = min(p.group_tm, p.num_tm - g0);
-        const int gtiles = gtm * p.num_tn;
-        for (int t = 0; t < p.N; t++) {
-            int slot = 0;
-            for (int j = cid; j < gtiles; j += ncl, slot++) fn(g0 + j % gtm, j / gtm, t, slot);
-        }
+        const int jj = j % gsz;
+        for (int t = 0; t < p.N; t++) fn(g0 + jj % gtm, jj / gtm, t);
     }
 }
 
@@ -122,31 +111,34 @@ __device__ __forceinline__ void reduce32(const uint32_t (&v)[32], int t, uint32_
     }
 }
 
-// lines 8-10 for this thread's row and 32-column chunk c of a finished tile
+// lines 8-10 for this thread's row and 8 columns [col0, col0 + 8) of a finished
+// tile (32-column chunk c, 8-column group hh) from its N residue bytes in scratch
 template <int NM>
-__device__ __forceinline__ void crt_chunk(const Params& p, const uint8_t* tile_scr, int c, int r, int row,
-                                          int col0, int ei) {
-    #pragma unroll 1
-    for (int hh = 0; hh < 4; hh++) {                       // 8 columns at a time
-        uint32_t wt[NM][2];
-        #pragma unroll
-        for (int tt = 0; tt < NM; tt++) {
-            const uint2 x = *reinterpret_cast<const uint2*>(
-                tile_scr + (size_t)tt * TILE_BYTES + ((size_t)(c * BM + r)) * 32 + hh * 8);
-            wt[tt][0] = x.x; wt[tt][1] = x.y;
-        }
-        double* crow = p.C + (int64_t)row * p.ldc + col0 + hh * 8;
-        const int ncol = p.n - (col0 + hh * 8);
-        const bool vec = ncol >= 8 && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
-        #pragma unroll
-        for (int j = 0; j < 8; j += 2) {
+__device__ __forceinline__ void crt_slice(const Params& p, const uint8_t* tile_scr, int c, int hh, int r,
+                                          int row, int col0, int ei) {
+    uint32_t wt[NM][2];
+    #pragma unroll
+    for (int tt = 0; tt < NM; tt++) {
+        const uint2 x = *reinterpret_cast<const uint2*>(
+            tile_scr + (size_t)tt * TILE_BYTES + ((size_t)(c * BM + r)) * 32 + hh * 8);
+        wt[tt][0] = x.x; wt[tt][1] = x.y;
+    }
+    double* crow = p.C + (int64_t)row * p.ldc + col0;
+    const int ncol = p.n - col0;
+    const bool vec = ncol >= 8 && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
+    #pragma unroll
+    for (int q = 0; q < 2; q++) {                      // word q of each residue row: columns 4q..4q+3
+        #pragma unroll 1
+        for (int pr = 0; pr < 2; pr++) {                // column pair (4q + 2pr, 4q + 2pr + 1)
+            const int j = 4 * q + 2 * pr;
             double o[2];
             #pragma unroll
             for (int jj = 0; jj < 2; jj++) {
                 uint32_t res[NM];
+                const uint32_t sel = 0x4440u | (uint32_t)(2 * pr + jj);
                 #pragma unroll
-                for (int tt = 0; tt < NM; tt++) res[tt] = (wt[tt][(j + jj) >> 2] >> (8 * ((j + jj) & 3))) & 0xffu;
-                const int col = col0 + hh * 8 + j + jj;
+                for (int tt = 0; tt < NM; tt++) res[tt] = prmt(wt[tt][q], 0u, sel);
+                const int col = col0 + j + jj;
                 const int fj = col < p.n ? __ldg(p.f + col) : 0;
                 o[jj] = crt_from_residues<NM>(res, ei, fj);
             }
@@ -196,7 +188,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             int stage = 0; uint32_t ph = 0;
             int step = 0, kb_in_step = 0;          // progress steps issued by this CTA
             const uint32_t nctas = gridDim.x;
-            for_each_unit(p, cid, ncl, [&](int tm, int tn, int t, int) {
+            for_each_unit(p, cid, ncl, [&](int tm, int tn, int t) {
                 const int arow = tm * C_::TILE_M + (int)rank * BM;
                 const int brow = tn * BN + (int)rank * C_::B_ROWS;
                 for (int kb = 0; kb < p.num_kb; kb++) {
@@ -234,7 +226,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const uint32_t idesc = idesc_i8(C_::TILE_M, BN);
             int stage = 0; uint32_t ph = 0;
             int acc = 0; uint32_t aph = 0;
-            for_each_unit(p, cid, ncl, [&](int, int, int, int) {
+            for_each_unit(p, cid, ncl, [&](int, int, int) {
                 mbar_wait(smem_u32(&s.tempty[acc]), aph ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
@@ -267,7 +259,20 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         for (int i = 0; i < 2; i++)
             tempty_leader[i] = CG == 2 ? mapa_shared(smem_u32(&s.tempty[i]), 0) : smem_u32(&s.tempty[i]);
         int acc = 0; uint32_t aph = 0;
-        for_each_unit(p, cid, ncl, [&](int tm, int tn, int t, int slot) {
+        bool pend = false;                                // a finished tile awaits lines 8-10
+        int ptm = 0, ptn = 0, pslot = 0, slot = 0;
+        auto run_slice = [&](int sl) {
+          if constexpr (FUSED) {
+            const int c = half * 4 + (sl >> 2), hh = sl & 3;
+            const int prow = ptm * C_::TILE_M + (int)rank * BM + r;
+            const int col0 = ptn * BN + c * 32 + hh * 8;
+            if (prow < p.m && col0 < p.n) {
+                const uint8_t* pscr = p.scratch + (((size_t)blockIdx.x * 2 + pslot) * NM) * TILE_BYTES;
+                crt_slice<NM>(p, pscr, c, hh, r, prow, col0, __ldg(p.e + prow));
+            }
+          }
+        };
+        for_each_unit(p, cid, ncl, [&](int tm, int tn, int t) {
             mbar_wait(smem_u32(&s.tfull[acc]), aph);
             tc_fence_after();
             const int row = tm * C_::TILE_M + (int)rank * BM + r;
@@ -315,7 +320,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 }
             } else {
                 // line 7 for the 4 chunks -> uint8 residues in this tile's scratch slot
-                uint8_t* tile_scr = p.scratch + (((size_t)blockIdx.x * p.max_slots + slot) * NM) * TILE_BYTES;
+                uint8_t* tile_scr = p.scratch + (((size_t)blockIdx.x * 2 + slot) * NM) * TILE_BYTES;
                 #pragma unroll
                 for (int cc = 0; cc < 4; cc++) {
                     const int c = half * 4 + cc;
@@ -333,19 +338,21 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     if (CG == 2) mbar_arrive_cluster(tempty_leader[acc]);
                     else mbar_arrive(tempty_leader[acc]);
                 }
-                if (t == NM - 1 && row < p.m) {
-                    // lines 8-10: exact CRT of the tile's N residues, scaled into C
-                    const int ei = __ldg(p.e + row);
-                    #pragma unroll 1
-                    for (int cc = 0; cc < 4; cc++) {
-                        const int c = half * 4 + cc;
-                        const int col0 = tn * BN + c * 32;
-                        if (col0 < p.n) crt_chunk<NM>(p, tile_scr, c, r, row, col0, ei);
-                    }
+                // lines 8-10 of the previous tile, 16 slices of 8 columns spread
+                // over this tile's N units (no burst that would hold TMEM back)
+                if (pend) {
+                    const int s0 = (t * 16) / NM, s1 = ((t + 1) * 16) / NM;
+                    for (int sl = s0; sl < s1; sl++) run_slice(sl);
+                }
+                if (t == NM - 1) {
+                    pend = true; ptm = tm; ptn = tn; pslot = slot; slot ^= 1;
                 }
             }
             if (++acc == 2) { acc = 0; aph ^= 1; }
         });
+        if constexpr (FUSED) {
+            if (pend) for (int sl = 0; sl < 16; sl++) run_slice(sl);    // the last tile
+        }
     }
 
     tc_fence_before();
@@ -403,25 +410,15 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
     p.num_tn = (int)((n + BN - 1) / BN);
     p.num_kb = (int)((k + BK - 1) / BK);
     p.group_tm = std::max(1, env_int("OZ2_GROUP_TM", GROUP_TM));
-    p.tile_major = env_int("OZ2_TILE_MAJOR", 1);
     p.epi_nop = env_int("OZ2_EPI_NOP", 0);
-    const int gtiles = p.tile_major ? p.num_tm * p.num_tn : std::min(p.group_tm, p.num_tm) * p.num_tn;
+    const int tiles = p.num_tm * p.num_tn;
     const int nclusters = num_sms / cg;
-    const int ncl = gtiles < nclusters ? gtiles : nclusters;
-    p.max_slots = p.tile_major ? 1 : (gtiles + ncl - 1) / ncl;
+    const int ncl = tiles < nclusters ? tiles : nclusters;
     p.sync_kb = env_int("OZ2_SYNC_KB", 32);
-    p.sync_lag = env_int("OZ2_SYNC_LAG", 1);
+    p.sync_lag = env_int("OZ2_SYNC_LAG", 0);
     {
         // busiest CTA: its tiles x N moduli x num_kb k-blocks, in sync_kb steps
-        const int64_t tiles = (int64_t)p.num_tm * p.num_tn;
-        int64_t max_tiles = 0;
-        if (p.tile_major) {
-            max_tiles = (tiles + ncl - 1) / ncl;
-        } else {
-            for (int g0 = 0; g0 < p.num_tm; g0 += p.group_tm)
-                max_tiles += ((int64_t)std::min(p.group_tm, p.num_tm - g0) * p.num_tn + ncl - 1) / ncl;
-        }
-        const int64_t kbs = max_tiles * N * p.num_kb;
+        const int64_t kbs = (int64_t)((tiles + ncl - 1) / ncl) * N * p.num_kb;
         p.sync_steps_max = p.sync_kb > 0 ? (int)((kbs + p.sync_kb - 1) / p.sync_kb) + 1 : 0;
     }
     *grid_out = ncl * cg;
@@ -430,8 +427,8 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
 
 size_t fused_scratch_bytes(int64_t m, int64_t n, int N, int num_sms) {
     int grid;
-    gemm::Params p = make_params(m, n, 1, N, num_sms, gemm_cta_group(), &grid);
-    return (size_t)grid * p.max_slots * N * gemm::TILE_BYTES;
+    make_params(m, n, 1, N, num_sms, gemm_cta_group(), &grid);
+    return (size_t)grid * 2 * N * gemm::TILE_BYTES;
 }
 
 int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,

@@ -6,6 +6,12 @@
 
 namespace oz2 {
 
+// number of 38-bit pieces of M = prod of the first N moduli (ceil(bitlen(M) / 38));
+// tables.cpp computes the same value and api.cu checks they agree
+__host__ __device__ constexpr int crt_pieces(int N) {
+    return N <= 4 ? 1 : (N <= 9 ? 2 : (N <= 14 ? 3 : (N <= 19 ? 4 : 5)));
+}
+
 int host_T(int N);   // floor(L/2) for N moduli (host copy of the table)
 
 // scale.cu -- Alg. 1 lines 1-5

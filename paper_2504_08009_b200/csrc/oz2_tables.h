@@ -6,10 +6,12 @@
 #include <stdint.h>
 
 #define OZ2_MAX_MODULI 20
+#define OZ2_PIECE_BITS 38   // CRT weights and M are split into 38-bit FP64 pieces
+#define OZ2_MAX_PIECES 5
 
 struct Oz2Table {
     int32_t N;           // number of moduli
-    int32_t P;           // number of 40-bit pieces of M (1..4)
+    int32_t P;           // number of 38-bit pieces of M (1..5)
     int32_t L;           // floor(log2(M/2 - 1))        (Eq. 16 with q dropped)
     int32_t T;           // floor(L/2): FAST bound ||2^e a||_2 <= 2^T   (reading R4)
     int32_t m[OZ2_MAX_MODULI];        // moduli, Eq. (18) + reading R1
@@ -23,9 +25,10 @@ struct Oz2Table {
     uint32_t G63[OZ2_MAX_MODULI];     // (-2^63) mod m_t: undoes the 2^63 bias of 64-bit residue inputs
     uint32_t G95[OZ2_MAX_MODULI];     // (-2^95) mod m_t: same for 96-bit inputs
     uint64_t hmagic[OZ2_MAX_MODULI];  // h_t * magic_t: floor((y + h)/m) = (y * magic + hmagic) >> 32
-    double W[4][OZ2_MAX_MODULI];      // w_t = M y_t / m_t = sum_p W[p][t] 2^(40p), W < 2^40
-    double Mp[4];                     // M = sum_p Mp[p] 2^(40p)
-    double invM;                      // 2^(40(P-2)) / M  (P >= 2),  1/M  (P == 1)
+    double W[OZ2_MAX_PIECES][OZ2_MAX_MODULI];  // w_t = M y_t / m_t = sum_p W[p][t] 2^(38p), W < 2^38
+    double Mp[OZ2_MAX_PIECES];        // M = sum_p Mp[p] 2^(38p)
+    double invM;                      // 2^(38(P-2)) / M  (P >= 2),  1/M  (P == 1)
+    uint64_t bias[3];                 // (0x4338000000000000 * sum_p 2^(38p)) mod 2^192 (piece-extraction bias)
     double inv_m[OZ2_MAX_MODULI];     // 1.0 / m_t
     uint64_t Mw[3];                   // M, 192-bit little endian
     uint64_t Mhalf[3];                // M / 2

@@ -98,14 +98,36 @@ int oz2_build_tables(Oz2Table tabs[OZ2_MAX_MODULI + 1]) {
         T.N = N;
         Nat M = product(N);
         int Mbits = M.bits();
-        T.P = (Mbits + 39) / 40;
+        T.P = (Mbits + OZ2_PIECE_BITS - 1) / OZ2_PIECE_BITS;
         Nat half = shr1(M);                            // M is even (m_1 = 256)
         T.L = sub_small(half, 1).bits() - 1;
         T.T = T.L / 2;
-        for (int p = 0; p < 4; p++) T.Mp[p] = (double)bits_at(M, 40 * p, 40);
+        for (int p = 0; p < OZ2_MAX_PIECES; p++) T.Mp[p] = (double)bits_at(M, OZ2_PIECE_BITS * p, OZ2_PIECE_BITS);
+        {
+            // bias = sum_p 0x4338000000000000 * 2^(38p) mod 2^192, as three 64-bit limbs
+            uint64_t b[3] = {0, 0, 0};
+            for (int p = 0; p < T.P; p++) {
+                const int sh = OZ2_PIECE_BITS * p;
+                const unsigned __int128 v = (unsigned __int128)0x4338000000000000ull;
+                uint64_t add[3] = {0, 0, 0};
+                // v << sh into 192 bits
+                for (int bit = 0; bit < 64; bit++)
+                    if ((uint64_t)(v >> bit) & 1ull) {
+                        const int pos = bit + sh;
+                        if (pos < 192) add[pos / 64] |= 1ull << (pos % 64);
+                    }
+                unsigned __int128 c = 0;
+                for (int w = 0; w < 3; w++) {
+                    c += (unsigned __int128)b[w] + add[w];
+                    b[w] = (uint64_t)c;
+                    c >>= 64;
+                }
+            }
+            for (int w = 0; w < 3; w++) T.bias[w] = b[w];
+        }
         for (int w = 0; w < 3; w++) { T.Mw[w] = bits_at(M, 64 * w, 64); T.Mhalf[w] = bits_at(half, 64 * w, 64); }
         double Md = to_double(M);
-        T.invM = T.P >= 2 ? ldexp(1.0, 40 * (T.P - 2)) / Md : 1.0 / Md;
+        T.invM = T.P >= 2 ? ldexp(1.0, OZ2_PIECE_BITS * (T.P - 2)) / Md : 1.0 / Md;
         for (int t = 0; t < N; t++) {
             int64_t m = kModuli[t];
             T.m[t] = (int32_t)m;
@@ -133,8 +155,8 @@ int oz2_build_tables(Oz2Table tabs[OZ2_MAX_MODULI + 1]) {
             if (y <= 0) return 2;
             T.y[t] = (int32_t)y;
             Nat w = mul_small(Mt, (uint32_t)y);
-            for (int p = 0; p < 4; p++) T.W[p][t] = (double)bits_at(w, 40 * p, 40);
-            if (w.bits() > 40 * T.P) return 3;
+            for (int p = 0; p < OZ2_MAX_PIECES; p++) T.W[p][t] = (double)bits_at(w, OZ2_PIECE_BITS * p, OZ2_PIECE_BITS);
+            if (w.bits() > OZ2_PIECE_BITS * T.P) return 3;
         }
     }
     return 0;

@@ -21,6 +21,7 @@ MODE_FAST = 0
 MODE_EQ17 = 1
 EXP_NONFINITE = -(2**31)
 MAX_K = 2**17
+PIECE_BITS = 38
 
 # every symbol include/oz2.h declares (checked by tests/test_abi.py)
 SYMBOLS = [
@@ -101,14 +102,14 @@ def _mode_id(mode) -> int:
 def tables(N: int) -> dict:
     m = np.zeros(N, np.int32)
     y = np.zeros(N, np.int32)
-    W = np.zeros(4 * N, np.float64)
-    Mp = np.zeros(4, np.float64)
+    W = np.zeros(5 * N, np.float64)
+    Mp = np.zeros(5, np.float64)
     P, L, T = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
     c = lambda a: a.ctypes.data_as(ctypes.c_void_p)
     _check(lib().oz2_tables(N, c(m), c(y), c(W), c(Mp), ctypes.byref(P), ctypes.byref(L),
                             ctypes.byref(T)), "oz2_tables")
     return {"moduli": [int(v) for v in m], "y": [int(v) for v in y],
-            "W": W.reshape(4, N)[:P.value].copy(), "Mp": Mp[:P.value].copy(),
+            "W": W.reshape(5, N)[:P.value].copy(), "Mp": Mp[:P.value].copy(),
             "P": P.value, "L": L.value, "T": T.value}
 
 

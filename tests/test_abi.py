@@ -57,12 +57,13 @@ def test_tables_match_oracle(oz2, oracle, N):
     assert t["y"] == c["y"]
     assert t["L"] == c["L"] and t["T"] == c["T"]
     P = t["P"]
-    assert P == (c["M"].bit_length() + 39) // 40
+    B = oz2.PIECE_BITS
+    assert P == (c["M"].bit_length() + B - 1) // B
     for tt in range(N):
-        w = sum(int(t["W"][p][tt]) << (40 * p) for p in range(P))
+        w = sum(int(t["W"][p][tt]) << (B * p) for p in range(P))
         assert w == c["w"][tt]
-        assert all(0 <= t["W"][p][tt] < 2**40 and float(t["W"][p][tt]).is_integer() for p in range(P))
-    assert sum(int(t["Mp"][p]) << (40 * p) for p in range(P)) == c["M"]
+        assert all(0 <= t["W"][p][tt] < 2**B and float(t["W"][p][tt]).is_integer() for p in range(P))
+    assert sum(int(t["Mp"][p]) << (B * p) for p in range(P)) == c["M"]
 
 
 def test_eq17_matches_oracle(oz2, oracle):
