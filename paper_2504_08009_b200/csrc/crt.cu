@@ -14,83 +14,6 @@
 
 namespace oz2 {
 
-struct U192 { uint64_t w0, w1, w2; };
-
-__device__ __forceinline__ U192 u192_from_i64(long long v) {
-    U192 r; r.w0 = (uint64_t)v; r.w1 = r.w2 = v < 0 ? ~0ull : 0ull; return r;
-}
-__device__ __forceinline__ U192 u192_add(U192 a, U192 b) {
-    U192 r;
-    r.w0 = a.w0 + b.w0;
-    uint64_t c0 = r.w0 < a.w0;
-    uint64_t t = a.w1 + b.w1;
-    uint64_t c1 = t < a.w1;
-    r.w1 = t + c0;
-    c1 += r.w1 < t;
-    r.w2 = a.w2 + b.w2 + c1;
-    return r;
-}
-__device__ __forceinline__ U192 u192_neg(U192 a) {
-    U192 r; r.w0 = ~a.w0; r.w1 = ~a.w1; r.w2 = ~a.w2;
-    return u192_add(r, u192_from_i64(1));
-}
-// v * 2^s for a signed 64-bit v, 0 <= s < 128, as a 192-bit two's complement
-__device__ __forceinline__ U192 u192_shl_i64(long long v, int s) {
-    U192 x = u192_from_i64(v);
-    if (s >= 64) { x.w2 = x.w1; x.w1 = x.w0; x.w0 = 0; s -= 64; }
-    if (s > 0) {
-        x.w2 = (x.w2 << s) | (x.w1 >> (64 - s));
-        x.w1 = (x.w1 << s) | (x.w0 >> (64 - s));
-        x.w0 <<= s;
-    }
-    return x;
-}
-__device__ __forceinline__ bool u192_neg_p(U192 a) { return (long long)a.w2 < 0; }
-// signed compare a >= b
-__device__ __forceinline__ bool u192_ge(U192 a, U192 b) {
-    if ((long long)a.w2 != (long long)b.w2) return (long long)a.w2 > (long long)b.w2;
-    if (a.w1 != b.w1) return a.w1 > b.w1;
-    return a.w0 >= b.w0;
-}
-
-// logical right shift, 0 <= s < 192
-__device__ __forceinline__ U192 u192_shr(U192 a, int s) {
-    if (s >= 128) { a.w0 = a.w2 >> (s - 128); a.w1 = 0; a.w2 = 0; return a; }
-    if (s >= 64) { a.w0 = a.w1; a.w1 = a.w2; a.w2 = 0; s -= 64; }
-    if (s) {
-        a.w0 = (a.w0 >> s) | (a.w1 << (64 - s));
-        a.w1 = (a.w1 >> s) | (a.w2 << (64 - s));
-        a.w2 >>= s;
-    }
-    return a;
-}
-
-// 2^-(e+f) RN(X)   (Alg. 1 line 10, reading R10)
-__device__ __forceinline__ double u192_to_double_scaled(U192 X, int sc) {
-    const bool neg = u192_neg_p(X);
-    if (neg) X = u192_neg(X);
-    double r;
-    if (X.w2 == 0 && X.w1 == 0) {
-        r = __ull2double_rn(X.w0);                       // correctly rounded
-    } else {
-        const int bl = X.w2 ? 192 - __clzll((long long)X.w2) : 128 - __clzll((long long)X.w1);
-        const int sh = bl - 64;                          // 1 .. 127
-        const uint64_t top = u192_shr(X, sh).w0;         // the 64 leading bits
-        uint64_t low;                                    // the sh dropped bits, != 0 ?
-        if (sh < 64) low = X.w0 & ((1ull << sh) - 1);
-        else low = X.w0 | (X.w1 & ((1ull << (sh - 64)) - 1));
-        // 64 -> 53 bits drops 11: a sticky bit OR-ed into bit 0 rounds correctly
-        r = __ull2double_rn(top | (low ? 1ull : 0ull));
-        r = r * __longlong_as_double((long long)(sh + 1023) << 52);   // exact
-    }
-    if (neg) r = -r;
-    if (sc >= -1022 && sc <= 1023) {
-        const double p = r * __longlong_as_double((long long)(sc + 1023) << 52);
-        if (fabs(p) >= 0x1p-1022 || r == 0.0) return p;  // exact
-    }
-    return ldexp(r, sc);                                 // subnormal / extreme: one rounding
-}
-
 // line 7: c'' = c' - floor(c'/m_t) m_t in [0, m_t), for any int32 c', in
 // integer arithmetic: u = c' mod 2^32 = hi 2^16 + lo, y = hi (2^16 mod m_t) + lo
 // (+ (-2^32) mod m_t when c' < 0) == c' (mod m_t), y < 2^24, then the magic
@@ -109,28 +32,112 @@ __device__ __forceinline__ double u32_to_double(uint32_t r) {
     return __hiloint2double(0x43300000, (int)r) - 4503599627370496.0;   // (2^52 + r) - 2^52
 }
 
-// v * 2^s (v < 2^64, s a compile-time multiple of 38 below 192) added to Y, mod 2^192
-template <int S>
-__device__ __forceinline__ U192 u192_add_shl(U192 Y, uint64_t v) {
-    U192 x;
-    if (S == 0) { x.w0 = v; x.w1 = 0; x.w2 = 0; }
-    else if (S < 64) { x.w0 = v << S; x.w1 = v >> (64 - S); x.w2 = 0; }
-    else if (S == 64) { x.w0 = 0; x.w1 = v; x.w2 = 0; }
-    else if (S < 128) { x.w0 = 0; x.w1 = v << (S - 64); x.w2 = v >> (128 - S); }
-    else if (S == 128) { x.w0 = 0; x.w1 = 0; x.w2 = v; }
-    else { x.w0 = 0; x.w1 = 0; x.w2 = v << (S - 128); }
-    return u192_add(Y, x);
+// ---------------------------------------------------------------------------
+// multi-limb integers (L = 4: 128 bit, L = 6: 192 bit) with PTX carry chains
+// ---------------------------------------------------------------------------
+template <int L> struct Limbs { uint32_t w[L]; };
+
+__device__ __forceinline__ void add4(Limbs<4>& a, const Limbs<4>& b) {
+    asm("add.cc.u32 %0, %0, %4;\n\taddc.cc.u32 %1, %1, %5;\n\taddc.cc.u32 %2, %2, %6;\n\taddc.u32 %3, %3, %7;"
+        : "+r"(a.w[0]), "+r"(a.w[1]), "+r"(a.w[2]), "+r"(a.w[3]) : "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]));
+}
+__device__ __forceinline__ void sub4(Limbs<4>& a, const Limbs<4>& b) {
+    asm("sub.cc.u32 %0, %0, %4;\n\tsubc.cc.u32 %1, %1, %5;\n\tsubc.cc.u32 %2, %2, %6;\n\tsubc.u32 %3, %3, %7;"
+        : "+r"(a.w[0]), "+r"(a.w[1]), "+r"(a.w[2]), "+r"(a.w[3]) : "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]));
+}
+__device__ __forceinline__ void add6(Limbs<6>& a, const Limbs<6>& b) {
+    asm("add.cc.u32 %0, %0, %6;\n\taddc.cc.u32 %1, %1, %7;\n\taddc.cc.u32 %2, %2, %8;\n\t"
+        "addc.cc.u32 %3, %3, %9;\n\taddc.cc.u32 %4, %4, %10;\n\taddc.u32 %5, %5, %11;"
+        : "+r"(a.w[0]), "+r"(a.w[1]), "+r"(a.w[2]), "+r"(a.w[3]), "+r"(a.w[4]), "+r"(a.w[5])
+        : "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]), "r"(b.w[4]), "r"(b.w[5]));
+}
+__device__ __forceinline__ void sub6(Limbs<6>& a, const Limbs<6>& b) {
+    asm("sub.cc.u32 %0, %0, %6;\n\tsubc.cc.u32 %1, %1, %7;\n\tsubc.cc.u32 %2, %2, %8;\n\t"
+        "subc.cc.u32 %3, %3, %9;\n\tsubc.cc.u32 %4, %4, %10;\n\tsubc.u32 %5, %5, %11;"
+        : "+r"(a.w[0]), "+r"(a.w[1]), "+r"(a.w[2]), "+r"(a.w[3]), "+r"(a.w[4]), "+r"(a.w[5])
+        : "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]), "r"(b.w[4]), "r"(b.w[5]));
+}
+template <int L> __device__ __forceinline__ void ladd(Limbs<L>& a, const Limbs<L>& b) {
+    if constexpr (L == 4) add4(a, b); else add6(a, b);
+}
+template <int L> __device__ __forceinline__ void lsub(Limbs<L>& a, const Limbs<L>& b) {
+    if constexpr (L == 4) sub4(a, b); else sub6(a, b);
+}
+template <int L> __device__ __forceinline__ Limbs<L> lzero() {
+    Limbs<L> z;
+    #pragma unroll
+    for (int i = 0; i < L; i++) z.w[i] = 0;
+    return z;
+}
+template <int L> __device__ __forceinline__ Limbs<L> lconst(const uint64_t (&v)[3]) {
+    Limbs<L> z;
+    #pragma unroll
+    for (int i = 0; i < L; i++) z.w[i] = (uint32_t)(v[i / 2] >> (32 * (i & 1)));
+    return z;
+}
+// (vh:vl) * 2^(38 p) placed into L limbs (bits beyond 32 L dropped: arithmetic mod 2^(32 L))
+template <int L, int P>
+__device__ __forceinline__ Limbs<L> place(uint32_t vl, uint32_t vh) {
+    constexpr int S = 38 * P, q = S / 32, r = S % 32;
+    Limbs<L> x = lzero<L>();
+    if constexpr (r == 0) {
+        if (q < L) x.w[q] = vl;
+        if (q + 1 < L) x.w[q + 1] = vh;
+    } else {
+        if (q < L) x.w[q] = vl << r;
+        if (q + 1 < L) x.w[q + 1] = __funnelshift_l(vl, vh, r);
+        if (q + 2 < L) x.w[q + 2] = vh >> (32 - r);
+    }
+    return x;
 }
 
-template <int P>
-__device__ __forceinline__ U192 assemble_biased(const uint64_t (&b)[5]) {
-    U192 Y = {0, 0, 0};
-    Y = u192_add_shl<0>(Y, b[0]);
-    if (P > 1) Y = u192_add_shl<38>(Y, b[1]);
-    if (P > 2) Y = u192_add_shl<76>(Y, b[2]);
-    if (P > 3) Y = u192_add_shl<114>(Y, b[3]);
-    if (P > 4) Y = u192_add_shl<152>(Y, b[4]);
-    return Y;
+// 2^sc * RN(X) for a signed L-limb integer X (reading R10: round, then scale)
+template <int L>
+__device__ __forceinline__ double limbs_to_double_scaled(Limbs<L> X, int sc) {
+    const bool neg = (int32_t)X.w[L - 1] < 0;
+    Limbs<L> mag = lzero<L>();
+    lsub<L>(mag, X);                                       // -X
+    #pragma unroll
+    for (int i = 0; i < L; i++) mag.w[i] = neg ? mag.w[i] : X.w[i];
+    // 64-bit words, least significant first
+    uint64_t w[L / 2];
+    #pragma unroll
+    for (int i = 0; i < L / 2; i++) w[i] = ((uint64_t)mag.w[2 * i + 1] << 32) | mag.w[2 * i];
+    double r;
+    int sh = 0;
+    // the highest non-zero 64-bit word
+    int lead = 0;
+    #pragma unroll
+    for (int i = 1; i < L / 2; i++) if (w[i]) lead = i;
+    if (lead == 0) {
+        r = __ull2double_rn(w[0]);                          // exact rounding of a 64-bit integer
+    } else {
+        const uint64_t hi = w[lead], lo = w[lead - 1];
+        const int lz = __clzll((long long)hi);
+        const uint64_t top = lz ? (hi << lz) | (lo >> (64 - lz)) : hi;   // the 64 leading bits
+        uint64_t below = lo << lz;                         // bits below the window in this word
+        #pragma unroll
+        for (int i = 0; i < L / 2 - 2; i++) if (i < lead - 1) below |= w[i];
+        sh = 64 * lead - lz;
+        r = __ull2double_rn(top | (below ? 1ull : 0ull));   // sticky below the round bit
+    }
+    if (neg) r = -r;
+    const int s2 = sc + sh;
+    if (s2 >= -1022 && s2 <= 1023) {
+        const double p = r * __longlong_as_double((long long)(s2 + 1023) << 52);
+        if (fabs(p) >= 0x1p-1022 || r == 0.0) return p;     // exact
+    }
+    return ldexp(ldexp(r, sh), sc);                         // rare: extreme exponents (one rounding)
+}
+
+template <int P, int L>
+__device__ __forceinline__ Limbs<L> assemble_biased(const uint64_t (&b)[5]) {
+    Limbs<L> X = place<L, 0>((uint32_t)b[0], (uint32_t)(b[0] >> 32));
+    if constexpr (P > 1) ladd<L>(X, place<L, 1>((uint32_t)b[1], (uint32_t)(b[1] >> 32)));
+    if constexpr (P > 2) ladd<L>(X, place<L, 2>((uint32_t)b[2], (uint32_t)(b[2] >> 32)));
+    if constexpr (P > 3) ladd<L>(X, place<L, 3>((uint32_t)b[3], (uint32_t)(b[3] >> 32)));
+    if constexpr (P > 4) ladd<L>(X, place<L, 4>((uint32_t)b[4], (uint32_t)(b[4] >> 32)));
+    return X;
 }
 
 // lines 8-10 from the reduced residues r_t = c''_t in [0, m_t):
@@ -138,12 +145,13 @@ __device__ __forceinline__ U192 assemble_biased(const uint64_t (&b)[5]) {
 //   sum < 2^51); Q ~ S/M rounded (from the top two pieces, within +-1 of
 //   floor(S/M + 1/2)); X_p = S_p - Q M_p with |X_p| < 2^51, so X_p + 1.5*2^52 is
 //   exact and its bit pattern is X_p + 0x4338000000000000: the pieces are
-//   summed as integers, the bias removed, and X corrected by +-M into
-//   [-M/2, M/2) -- the exact Eq. (1) result for every S.
+//   summed as integers (mod 2^128, or 2^192 for N >= 16), the bias removed,
+//   and X corrected by +-M into [-M/2, M/2) -- the exact Eq. (1) result.
 template <int NM>
 __device__ __forceinline__ double crt_from_residues(const uint32_t (&r)[NM], int ei, int fj) {
     const Oz2Table& T = c_tab[NM];
     constexpr int P = crt_pieces(NM);
+    constexpr int L = NM <= 15 ? 4 : 6;                          // |X| < M/2 < 2^118 (N <= 15)
     constexpr double MAGIC = 6755399441055744.0;                 // 1.5 * 2^52
     double S[P];
     #pragma unroll
@@ -159,14 +167,17 @@ __device__ __forceinline__ double crt_from_residues(const uint32_t (&r)[NM], int
     uint64_t b[5] = {0, 0, 0, 0, 0};
     #pragma unroll
     for (int p = 0; p < P; p++) b[p] = (uint64_t)__double_as_longlong(fma(-Q, T.Mp[p], S[p] + MAGIC));
-    U192 X = assemble_biased<P>(b);
-    X = u192_add(X, u192_neg(U192{T.bias[0], T.bias[1], T.bias[2]}));
-    const U192 Mw = {T.Mw[0], T.Mw[1], T.Mw[2]};
-    const U192 Mh = {T.Mhalf[0], T.Mhalf[1], T.Mhalf[2]};
-    if (u192_ge(X, Mh)) X = u192_add(X, u192_neg(Mw));                   // X >= M/2
-    else if (!u192_ge(X, u192_neg(Mh))) X = u192_add(X, Mw);              // X < -M/2
+    Limbs<L> X = assemble_biased<P, L>(b);
+    lsub<L>(X, lconst<L>(T.bias));
+    // Eq. (1) range [-M/2, M/2): Q is within one of the exact quotient
+    Limbs<L> D = X;
+    lsub<L>(D, lconst<L>(T.Mhalf));                              // X - M/2
+    Limbs<L> E = X;
+    ladd<L>(E, lconst<L>(T.Mhalf));                              // X + M/2
+    if ((int32_t)D.w[L - 1] >= 0) lsub<L>(X, lconst<L>(T.Mw));
+    else if ((int32_t)E.w[L - 1] < 0) ladd<L>(X, lconst<L>(T.Mw));
     if (ei == OZ2_EXP_NONFINITE_DEV || fj == OZ2_EXP_NONFINITE_DEV) return __longlong_as_double(0x7ff8000000000000ll);
-    return u192_to_double_scaled(X, -(ei + fj));
+    return limbs_to_double_scaled<L>(X, -(ei + fj));
 }
 
 template <int NM>
