@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <stdlib.h>
+#include <stdio.h>
 
 namespace oz2 {
 namespace gemm {
@@ -71,6 +72,7 @@ struct Params {
     int num_tm, num_tn, num_kb;     // tiles of TILE_M x BN
     int group_tm;                   // tile rows per raster group
     int epi_nop;                    // experiment only: epilogue drains TMEM and does nothing else
+    unsigned long long* dbg;        // experiment only: per-CTA wait-cycle counters (or NULL)
     int32_t* cprod;                 // RAW: [N][m][n]
     uint8_t* scratch;               // FUSED: [grid][2 slots][N][BM*BN] uint8 residues
     double* C;                      // FUSED
@@ -164,6 +166,8 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
     const bool leader = rank == 0;
     const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
+    long long dbg_fence = 0, dbg_empty = 0, dbg_tempty = 0, dbg_full = 0;
+    const long long dbg_t0 = clock64();
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
@@ -196,9 +200,13 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         // stay within sync_lag steps of the slowest CTA: the grid then
                         // streams each (wave, modulus) K-slab through L2 roughly once
                         const uint32_t need = (uint32_t)(step - p.sync_lag) * nctas;
+                        const long long t0 = p.dbg ? clock64() : 0;
                         while (ld_acquire_gpu(p.sync_ctr) < need) __nanosleep(64);
+                        if (p.dbg) dbg_fence += clock64() - t0;
                     }
-                    mbar_wait(smem_u32(&s.empty[stage]), ph ^ 1);
+                    { const long long t0 = p.dbg ? clock64() : 0;
+                      mbar_wait(smem_u32(&s.empty[stage]), ph ^ 1);
+                      if (p.dbg) dbg_empty += clock64() - t0; }
                     const uint32_t fb = smem_u32(&s.full[stage]);
                     if (leader) mbar_expect_tx(fb, CG * (C_::A_BYTES + C_::B_BYTES));
                     if (CG == 2) {
@@ -227,11 +235,15 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             int stage = 0; uint32_t ph = 0;
             int acc = 0; uint32_t aph = 0;
             for_each_unit(p, cid, ncl, [&](int, int, int) {
-                mbar_wait(smem_u32(&s.tempty[acc]), aph ^ 1);
+                { const long long t0 = p.dbg ? clock64() : 0;
+                  mbar_wait(smem_u32(&s.tempty[acc]), aph ^ 1);
+                  if (p.dbg) dbg_tempty += clock64() - t0; }
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
                 for (int kb = 0; kb < p.num_kb; kb++) {
-                    mbar_wait(smem_u32(&s.full[stage]), ph);
+                    { const long long t0 = p.dbg ? clock64() : 0;
+                      mbar_wait(smem_u32(&s.full[stage]), ph);
+                      if (p.dbg) dbg_full += clock64() - t0; }
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(s.a[stage]), b0 = smem_u32(s.b[stage]);
                     #pragma unroll
@@ -355,6 +367,11 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         }
     }
 
+    if (p.dbg && lane == 0 && warp == 0) {
+        p.dbg[blockIdx.x * 8 + 0] = dbg_fence; p.dbg[blockIdx.x * 8 + 1] = dbg_empty;
+        p.dbg[blockIdx.x * 8 + 4] = clock64() - dbg_t0;
+    }
+    if (p.dbg && lane == 0 && warp == 1) { p.dbg[blockIdx.x * 8 + 2] = dbg_tempty; p.dbg[blockIdx.x * 8 + 3] = dbg_full; }
     tc_fence_before();
     __syncthreads();
     if (CG == 2) cluster_sync();                      // peer done with remote barriers / TMEM
@@ -451,6 +468,27 @@ int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t 
     p.scratch = scratch; p.e = e; p.f = f; p.C = C; p.ldc = ldc;
     p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
     if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
+    static unsigned long long* dbg = nullptr;
+    const bool want_dbg = env_int("OZ2_GEMM_DEBUG", 0) != 0;
+    if (want_dbg) {
+        if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 8 * 1024);
+        cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 8 * 1024, st);
+        p.dbg = dbg;
+    }
+    struct DbgPrint {
+        bool on; unsigned long long* d; int grid; cudaStream_t st;
+        ~DbgPrint() {
+            if (!on) return;
+            unsigned long long h[8 * 1024];
+            cudaStreamSynchronize(st);
+            cudaMemcpy(h, d, sizeof(unsigned long long) * 8 * grid, cudaMemcpyDeviceToHost);
+            double sf = 0, se = 0, st_ = 0, sfu = 0, tot = 0;
+            for (int i = 0; i < grid; i++) { sf += h[8*i]; se += h[8*i+1]; st_ += h[8*i+2]; sfu += h[8*i+3]; tot += h[8*i+4]; }
+            fprintf(stderr, "[oz2 gemm dbg] per-CTA mean cycles: total %.3g  producer fence %.3g  producer empty %.3g  "
+                            "mma tempty %.3g  mma full %.3g (leaders only count mma)\n",
+                    tot / grid, sf / grid, se / grid, st_ / (grid / 2.0), sfu / (grid / 2.0));
+        }
+    } dbgp{want_dbg, dbg, grid, st};
     switch (N) {
 #define OZ2_CASE(NN) case NN: return cg == 2 ? gemm::launch_nm<NN, 2>(tmA, tmB, p, grid, st) \
                                              : gemm::launch_nm<NN, 1>(tmA, tmB, p, grid, st);
