@@ -73,6 +73,7 @@ struct Params {
     int group_tm;                   // tile rows per raster group
     int epi_nop;                    // experiment only: epilogue drains TMEM and does nothing else
     unsigned long long* dbg;        // experiment only: per-CTA wait-cycle counters (or NULL)
+    int pf_dist;                    // k-blocks of L2 prefetch ahead of the TMA loads
     int32_t* cprod;                 // RAW: [N][m][n]
     uint8_t* scratch;               // FUSED: [grid][2 slots][N][BM*BN] uint8 residues
     double* C;                      // FUSED
@@ -88,15 +89,22 @@ struct Params {
 // Visit every work unit (tm, tn, t) of cluster `cid` (of `ncl`) in schedule
 // order: tiles j = cid, cid + ncl, ... (raster groups of group_tm tile rows so
 // concurrent tiles share A and B panels in L2), all N moduli of a tile back to back.
+__device__ __forceinline__ void tile_coords(const Params& p, int j, int& tm, int& tn) {
+    const int gsz = p.group_tm * p.num_tn;
+    const int g0 = (j / gsz) * p.group_tm;
+    const int gtm = min(p.group_tm, p.num_tm - g0);
+    const int jj = j % gsz;
+    tm = g0 + jj % gtm;
+    tn = jj / gtm;
+}
+
 template <typename F>
 __device__ __forceinline__ void for_each_unit(const Params& p, int cid, int ncl, F&& fn) {
     const int tiles = p.num_tm * p.num_tn;
-    const int gsz = p.group_tm * p.num_tn;
     for (int j = cid; j < tiles; j += ncl) {
-        const int g0 = (j / gsz) * p.group_tm;
-        const int gtm = min(p.group_tm, p.num_tm - g0);
-        const int jj = j % gsz;
-        for (int t = 0; t < p.N; t++) fn(g0 + jj % gtm, jj / gtm, t);
+        int tm, tn;
+        tile_coords(p, j, tm, tn);
+        for (int t = 0; t < p.N; t++) fn(tm, tn, t);
     }
 }
 
@@ -192,6 +200,18 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             int stage = 0; uint32_t ph = 0;
             int step = 0, kb_in_step = 0;          // progress steps issued by this CTA
             const uint32_t nctas = gridDim.x;
+            // L2 prefetch cursor, pf_dist k-blocks ahead in this CTA's load sequence
+            const int tiles = p.num_tm * p.num_tn;
+            int pj = cid, pt = 0, pkb = 0;
+            auto prefetch_next = [&]() {
+                if (pj >= tiles) return;
+                int ptm, ptn;
+                tile_coords(p, pj, ptm, ptn);
+                tma_prefetch_3d(&tmA, pkb * BK, ptm * C_::TILE_M + (int)rank * BM, pt);
+                tma_prefetch_3d(&tmB, pkb * BK, ptn * BN + (int)rank * C_::B_ROWS, pt);
+                if (++pkb == p.num_kb) { pkb = 0; if (++pt == p.N) { pt = 0; pj += ncl; } }
+            };
+            for (int i = 0; i < p.pf_dist; i++) prefetch_next();
             for_each_unit(p, cid, ncl, [&](int tm, int tn, int t) {
                 const int arow = tm * C_::TILE_M + (int)rank * BM;
                 const int brow = tn * BN + (int)rank * C_::B_ROWS;
@@ -218,6 +238,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         tma_load_3d(smem_u32(s.b[stage]), &tmB, fb, kb * BK, brow, t);
                     }
                     if (++stage == C_::STAGES) { stage = 0; ph ^= 1; }
+                    if (p.pf_dist) prefetch_next();
                     if (p.sync_ctr && ++kb_in_step == p.sync_kb) {
                         kb_in_step = 0;
                         step++;
@@ -428,6 +449,7 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
     p.num_kb = (int)((k + BK - 1) / BK);
     p.group_tm = std::max(1, env_int("OZ2_GROUP_TM", GROUP_TM));
     p.epi_nop = env_int("OZ2_EPI_NOP", 0);
+    p.pf_dist = env_int("OZ2_PF_DIST", 16);
     const int tiles = p.num_tm * p.num_tn;
     const int nclusters = num_sms / cg;
     const int ncl = tiles < nclusters ? tiles : nclusters;

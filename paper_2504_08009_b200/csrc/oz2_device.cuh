@@ -88,6 +88,11 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, uint
         " [%0], [%1, {%2, %3, %4}], [%5];"
         :: "r"(dst), "l"((uint64_t)tmap), "r"(c0), "r"(c1), "r"(c2), "r"(bar) : "memory");
 }
+// bring a 3-D tile into L2 only (no shared memory, no completion)
+__device__ __forceinline__ void tma_prefetch_3d(const void* tmap, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+                 :: "l"((uint64_t)tmap), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" :: "l"((uint64_t)tmap) : "memory");
 }
