@@ -449,7 +449,7 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
     p.num_kb = (int)((k + BK - 1) / BK);
     p.group_tm = std::max(1, env_int("OZ2_GROUP_TM", GROUP_TM));
     p.epi_nop = env_int("OZ2_EPI_NOP", 0);
-    p.pf_dist = env_int("OZ2_PF_DIST", 16);
+    p.pf_dist = env_int("OZ2_PF_DIST", 0);       // measured: L2 prefetch slows the GEMM (TMA contention)
     const int tiles = p.num_tm * p.num_tn;
     const int nclusters = num_sms / cg;
     const int ncl = tiles < nclusters ? tiles : nclusters;
