@@ -215,15 +215,17 @@ def main():
     B = phi_matrix_torch(k, n, args.phi, SEED_B, device=dev) if rank == 0 else \
         torch.empty((k, n), dtype=torch.float64, device=dev)
     C = torch.empty((m, n), dtype=torch.float64, device=dev)
-    Cfull = torch.empty((m * world, n), dtype=torch.float64, device=dev) if (world > 1 and rank == 0) else None
     h = oz2.handle(local)
+
+    from paper_2504_08009_b200.dist import dgemm_rowblock
 
     def step():
         if world > 1:
-            dist.broadcast(B, src=0)
-        oz2.dgemm(A, B, N, out=C)
-        if world > 1:
-            dist.gather(C, list(Cfull.chunk(world)) if rank == 0 else None, dst=0)
+            # B broadcast from rank 0, local row block, C gathered to rank 0 (NCCL)
+            dgemm_rowblock(A, B, N, "fast", m_total=m * world,
+                           local_fn=lambda a, b, nm, md: oz2.dgemm(a, b, nm, md, out=C))
+        else:
+            oz2.dgemm(A, B, N, out=C)
 
     for _ in range(max(3, args.warmup)):
         step()
