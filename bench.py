@@ -309,7 +309,7 @@ def main():
             "stage_ms": {s: v / max(calls, 1) for s, v in stages.items()},
             "roofline": roofline,
             "n_scaled_roofline_frac": value / world / (4500.0 / N),
-            "gpu_launches": 6 * args.steps,
+            "gpu_launches": 5 * args.steps,   # rows, cols_stats, cols_finalize, cols_residues, modmul
             "clocks": clk.summary()}
 
     # e2e: same metric through the C ABI with host buffers (pinned), copies timed
