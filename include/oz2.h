@@ -128,12 +128,13 @@ int oz2_crt(oz2_handle_t h, int64_t m, int64_t n, const int32_t* Cprod, const in
             const int32_t* f, int num_moduli, double* C, int64_t ldc);
 
 /* ---- constants (host memory, no device needed) ----------------------------
- * moduli[N], y[N] (M_t y_t == 1 mod m_t, least positive), W[P*N] with
- * w_t = M y_t / m_t = sum_p W[p*N + t] 2^(38 p), 0 <= W < 2^38, Mp[P] the
- * same split of M, *P pieces, *L = floor(log2(M/2 - 1)), *T = floor(L/2).
- * Any output pointer may be NULL.  W must hold 5*N doubles, Mp 5. */
-int oz2_tables(int num_moduli, int32_t* moduli, int32_t* y, double* W, double* Mp,
-               int32_t* P, int32_t* L, int32_t* T);
+ * moduli[N], y[N] (M_t y_t == 1 mod m_t, least positive), w_words[5*N] with
+ * w_t = M y_t / m_t = sum_x w_words[5*t + x] 2^(32 x) (the CRT weights of Alg. 1
+ * line 8), M_words[5] the same split of M = prod m_t,
+ * *nbytes = bytes of M (the kernels' dp4a limbs of w_t),
+ * *L = floor(log2(M/2 - 1)), *T = floor(L/2).  Any output pointer may be NULL. */
+int oz2_tables(int num_moduli, int32_t* moduli, int32_t* y, uint32_t* w_words, uint32_t* M_words,
+               int32_t* nbytes, int32_t* L, int32_t* T);
 /* Eq. (17) in exact integer form: max{kappa : q 4^kappa <= M/2 - 1}, -1 if none. */
 int oz2_eq17_k(int num_moduli, int64_t q);
 

@@ -30,7 +30,9 @@ EncodeTiledFn g_encode = nullptr;
 void build_tables_once() {
     g_tabs_ok = (oz2_build_tables(g_tabs) == 0);
     for (int N = 2; N <= OZ2_MAX_MODULI && g_tabs_ok; N++) {
-        if (g_tabs[N].P != oz2::crt_pieces(N)) g_tabs_ok = false;   // kernels assume this
+        if (g_tabs[N].JB != oz2::crt_bytes(N) || g_tabs[N].WS != oz2::crt_swords(N) ||
+            g_tabs[N].WX != oz2::crt_words(N))
+            g_tabs_ok = false;                                       // kernels assume these
     }
 }
 
@@ -195,7 +197,7 @@ oz2_handle_t g_default[64] = {nullptr};
 
 extern "C" {
 
-int oz2_version(void) { return 100; }
+int oz2_version(void) { return 110; }
 
 const char* oz2_strerror(int code) {
     switch (code) {
@@ -211,7 +213,8 @@ const char* oz2_strerror(int code) {
     }
 }
 
-int oz2_tables(int N, int32_t* moduli, int32_t* y, double* W, double* Mp, int32_t* P, int32_t* L, int32_t* T) {
+int oz2_tables(int N, int32_t* moduli, int32_t* y, uint32_t* w_words, uint32_t* M_words, int32_t* nbytes,
+               int32_t* L, int32_t* T) {
     std::call_once(g_tabs_once, build_tables_once);
     if (!g_tabs_ok) return OZ2_ERR_INVALID_ARG;
     if (N < 2 || N > OZ2_MAX_MODULI) return OZ2_ERR_NUM_MODULI;
@@ -219,10 +222,10 @@ int oz2_tables(int N, int32_t* moduli, int32_t* y, double* W, double* Mp, int32_
     for (int i = 0; i < N; i++) {
         if (moduli) moduli[i] = t.m[i];
         if (y) y[i] = t.y[i];
-        if (W) for (int p = 0; p < OZ2_MAX_PIECES; p++) W[p * N + i] = t.W[p][i];
+        if (w_words) for (int x = 0; x < OZ2_MAX_WORDS; x++) w_words[OZ2_MAX_WORDS * i + x] = t.w32[i][x];
     }
-    if (Mp) for (int p = 0; p < OZ2_MAX_PIECES; p++) Mp[p] = t.Mp[p];
-    if (P) *P = t.P;
+    if (M_words) for (int x = 0; x < OZ2_MAX_WORDS; x++) M_words[x] = t.M32[x];
+    if (nbytes) *nbytes = t.JB;
     if (L) *L = t.L;
     if (T) *T = t.T;
     return OZ2_OK;

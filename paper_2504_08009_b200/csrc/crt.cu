@@ -27,165 +27,201 @@ __device__ __forceinline__ uint32_t reduce_line7(int32_t c, int t) {
     return y - q * (uint32_t)T.m[t];
 }
 
-// exact uint32 (< 2^52) -> double without the conversion pipe
-__device__ __forceinline__ double u32_to_double(uint32_t r) {
-    return __hiloint2double(0x43300000, (int)r) - 4503599627370496.0;   // (2^52 + r) - 2^52
-}
-
 // ---------------------------------------------------------------------------
-// multi-limb integers (L = 4: 128 bit, L = 6: 192 bit) with PTX carry chains
+// multi-word (32-bit) two's-complement integers, PTX carry chains
 // ---------------------------------------------------------------------------
-template <int L> struct Limbs { uint32_t w[L]; };
-
-__device__ __forceinline__ void add4(Limbs<4>& a, const Limbs<4>& b) {
-    asm("add.cc.u32 %0, %0, %4;\n\taddc.cc.u32 %1, %1, %5;\n\taddc.cc.u32 %2, %2, %6;\n\taddc.u32 %3, %3, %7;"
-        : "+r"(a.w[0]), "+r"(a.w[1]), "+r"(a.w[2]), "+r"(a.w[3]) : "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]));
-}
-__device__ __forceinline__ void sub4(Limbs<4>& a, const Limbs<4>& b) {
-    asm("sub.cc.u32 %0, %0, %4;\n\tsubc.cc.u32 %1, %1, %5;\n\tsubc.cc.u32 %2, %2, %6;\n\tsubc.u32 %3, %3, %7;"
-        : "+r"(a.w[0]), "+r"(a.w[1]), "+r"(a.w[2]), "+r"(a.w[3]) : "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]));
-}
-__device__ __forceinline__ void add6(Limbs<6>& a, const Limbs<6>& b) {
-    asm("add.cc.u32 %0, %0, %6;\n\taddc.cc.u32 %1, %1, %7;\n\taddc.cc.u32 %2, %2, %8;\n\t"
-        "addc.cc.u32 %3, %3, %9;\n\taddc.cc.u32 %4, %4, %10;\n\taddc.u32 %5, %5, %11;"
-        : "+r"(a.w[0]), "+r"(a.w[1]), "+r"(a.w[2]), "+r"(a.w[3]), "+r"(a.w[4]), "+r"(a.w[5])
-        : "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]), "r"(b.w[4]), "r"(b.w[5]));
-}
-__device__ __forceinline__ void sub6(Limbs<6>& a, const Limbs<6>& b) {
-    asm("sub.cc.u32 %0, %0, %6;\n\tsubc.cc.u32 %1, %1, %7;\n\tsubc.cc.u32 %2, %2, %8;\n\t"
-        "subc.cc.u32 %3, %3, %9;\n\tsubc.cc.u32 %4, %4, %10;\n\tsubc.u32 %5, %5, %11;"
-        : "+r"(a.w[0]), "+r"(a.w[1]), "+r"(a.w[2]), "+r"(a.w[3]), "+r"(a.w[4]), "+r"(a.w[5])
-        : "r"(b.w[0]), "r"(b.w[1]), "r"(b.w[2]), "r"(b.w[3]), "r"(b.w[4]), "r"(b.w[5]));
-}
-template <int L> __device__ __forceinline__ void ladd(Limbs<L>& a, const Limbs<L>& b) {
-    if constexpr (L == 4) add4(a, b); else add6(a, b);
-}
-template <int L> __device__ __forceinline__ void lsub(Limbs<L>& a, const Limbs<L>& b) {
-    if constexpr (L == 4) sub4(a, b); else sub6(a, b);
-}
-template <int L> __device__ __forceinline__ Limbs<L> lzero() {
-    Limbs<L> z;
-    #pragma unroll
-    for (int i = 0; i < L; i++) z.w[i] = 0;
-    return z;
-}
-template <int L> __device__ __forceinline__ Limbs<L> lconst(const uint64_t (&v)[3]) {
-    Limbs<L> z;
-    #pragma unroll
-    for (int i = 0; i < L; i++) z.w[i] = (uint32_t)(v[i / 2] >> (32 * (i & 1)));
-    return z;
-}
-// (vh:vl) * 2^(38 p) placed into L limbs (bits beyond 32 L dropped: arithmetic mod 2^(32 L))
-template <int L, int P>
-__device__ __forceinline__ Limbs<L> place(uint32_t vl, uint32_t vh) {
-    constexpr int S = 38 * P, q = S / 32, r = S % 32;
-    Limbs<L> x = lzero<L>();
-    if constexpr (r == 0) {
-        if (q < L) x.w[q] = vl;
-        if (q + 1 < L) x.w[q + 1] = vh;
+// a -= b, a += b modulo 2^(32 W); one asm statement per chain (the carry flag
+// does not survive between asm statements)
+template <int W>
+__device__ __forceinline__ void mw_sub(uint32_t (&a)[W], const uint32_t* b) {
+    if constexpr (W == 1) {
+        a[0] -= b[0];
+    } else if constexpr (W == 2) {
+        asm("sub.cc.u32 %0, %0, %2;\n\tsubc.u32 %1, %1, %3;"
+            : "+r"(a[0]), "+r"(a[1])
+            : "r"(b[0]), "r"(b[1]));
+    } else if constexpr (W == 3) {
+        asm("sub.cc.u32 %0, %0, %3;\n\tsubc.cc.u32 %1, %1, %4;\n\tsubc.u32 %2, %2, %5;"
+            : "+r"(a[0]), "+r"(a[1]), "+r"(a[2])
+            : "r"(b[0]), "r"(b[1]), "r"(b[2]));
+    } else if constexpr (W == 4) {
+        asm("sub.cc.u32 %0, %0, %4;\n\tsubc.cc.u32 %1, %1, %5;\n\tsubc.cc.u32 %2, %2, %6;\n\tsubc.u32 %3, %3, %7;"
+            : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3])
+            : "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]));
+    } else if constexpr (W == 5) {
+        asm("sub.cc.u32 %0, %0, %5;\n\tsubc.cc.u32 %1, %1, %6;\n\tsubc.cc.u32 %2, %2, %7;\n\tsubc.cc.u32 %3, %3, %8;\n\tsubc.u32 %4, %4, %9;"
+            : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4])
+            : "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]));
+    } else if constexpr (W == 6) {
+        asm("sub.cc.u32 %0, %0, %6;\n\tsubc.cc.u32 %1, %1, %7;\n\tsubc.cc.u32 %2, %2, %8;\n\tsubc.cc.u32 %3, %3, %9;\n\tsubc.cc.u32 %4, %4, %10;\n\tsubc.u32 %5, %5, %11;"
+            : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5])
+            : "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]));
     } else {
-        if (q < L) x.w[q] = vl << r;
-        if (q + 1 < L) x.w[q + 1] = __funnelshift_l(vl, vh, r);
-        if (q + 2 < L) x.w[q + 2] = vh >> (32 - r);
+        static_assert(W <= 6, "mw chain width");
     }
-    return x;
+}
+template <int W>
+__device__ __forceinline__ void mw_add(uint32_t (&a)[W], const uint32_t* b) {
+    if constexpr (W == 1) {
+        a[0] += b[0];
+    } else if constexpr (W == 2) {
+        asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;"
+            : "+r"(a[0]), "+r"(a[1])
+            : "r"(b[0]), "r"(b[1]));
+    } else if constexpr (W == 3) {
+        asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+            : "+r"(a[0]), "+r"(a[1]), "+r"(a[2])
+            : "r"(b[0]), "r"(b[1]), "r"(b[2]));
+    } else if constexpr (W == 4) {
+        asm("add.cc.u32 %0, %0, %4;\n\taddc.cc.u32 %1, %1, %5;\n\taddc.cc.u32 %2, %2, %6;\n\taddc.u32 %3, %3, %7;"
+            : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3])
+            : "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]));
+    } else if constexpr (W == 5) {
+        asm("add.cc.u32 %0, %0, %5;\n\taddc.cc.u32 %1, %1, %6;\n\taddc.cc.u32 %2, %2, %7;\n\taddc.cc.u32 %3, %3, %8;\n\taddc.u32 %4, %4, %9;"
+            : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4])
+            : "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]));
+    } else if constexpr (W == 6) {
+        asm("add.cc.u32 %0, %0, %6;\n\taddc.cc.u32 %1, %1, %7;\n\taddc.cc.u32 %2, %2, %8;\n\taddc.cc.u32 %3, %3, %9;\n\taddc.cc.u32 %4, %4, %10;\n\taddc.u32 %5, %5, %11;"
+            : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5])
+            : "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]));
+    } else {
+        static_assert(W <= 6, "mw chain width");
+    }
 }
 
-// 2^sc * RN(X) for a signed L-limb integer X (reading R10: round, then scale)
-template <int L>
-__device__ __forceinline__ double limbs_to_double_scaled(Limbs<L> X, int sc) {
-    const bool neg = (int32_t)X.w[L - 1] < 0;
-    Limbs<L> mag = lzero<L>();
-    lsub<L>(mag, X);                                       // -X
+// 2^sc * RN(X) for a signed WX-word integer X (reading R10: round to nearest
+// even, then scale), in integer arithmetic; only a subnormal or overflowing
+// result takes the FP64 ldexp path.
+template <int WX>
+__device__ __forceinline__ double x_to_double_scaled(const uint32_t (&X)[WX], int sc) {
+    constexpr int U = (WX + 1) / 2;                        // 64-bit words
+    const uint32_t s = (uint32_t)((int32_t)X[WX - 1] >> 31);
+    uint32_t mag[WX], sv[WX];
     #pragma unroll
-    for (int i = 0; i < L; i++) mag.w[i] = neg ? mag.w[i] : X.w[i];
-    // 64-bit words, least significant first
-    uint64_t w[L / 2];
+    for (int i = 0; i < WX; i++) { mag[i] = X[i] ^ s; sv[i] = s; }
+    mw_sub<WX>(mag, sv);                                   // |X| = (X ^ s) - s
+    uint64_t u[U];
     #pragma unroll
-    for (int i = 0; i < L / 2; i++) w[i] = ((uint64_t)mag.w[2 * i + 1] << 32) | mag.w[2 * i];
-    double r;
-    int sh = 0;
-    // the highest non-zero 64-bit word
-    int lead = 0;
-    #pragma unroll
-    for (int i = 1; i < L / 2; i++) if (w[i]) lead = i;
-    if (lead == 0) {
-        r = __ull2double_rn(w[0]);                          // exact rounding of a 64-bit integer
+    for (int i = 0; i < U; i++)
+        u[i] = (uint64_t)mag[2 * i] | ((2 * i + 1 < WX ? (uint64_t)mag[2 * i + 1] : 0ull) << 32);
+    uint64_t top, below = 0;
+    int E0;                                                // |X| = (top + frac) 2^E0, bit 63 of top set
+    if constexpr (U == 1) {
+        if (u[0] == 0) return 0.0;
+        const int lz = __clzll((long long)u[0]);
+        top = u[0] << lz;
+        E0 = -lz;
     } else {
-        const uint64_t hi = w[lead], lo = w[lead - 1];
+        int lead = 0;
+        #pragma unroll
+        for (int i = 1; i < U; i++) if (u[i]) lead = i;
+        uint64_t hi = u[0], lo = 0;
+        #pragma unroll
+        for (int i = 1; i < U; i++) if (lead == i) { hi = u[i]; lo = u[i - 1]; }
+        if (hi == 0) return 0.0;
         const int lz = __clzll((long long)hi);
-        const uint64_t top = lz ? (hi << lz) | (lo >> (64 - lz)) : hi;   // the 64 leading bits
-        uint64_t below = lo << lz;                         // bits below the window in this word
+        top = lz ? (hi << lz) | (lo >> (64 - lz)) : hi;
+        below = lz ? lo << lz : lo;
+        if (lead == 0) below = 0;
         #pragma unroll
-        for (int i = 0; i < L / 2 - 2; i++) if (i < lead - 1) below |= w[i];
-        sh = 64 * lead - lz;
-        r = __ull2double_rn(top | (below ? 1ull : 0ull));   // sticky below the round bit
+        for (int i = 0; i + 2 < U; i++) if (i + 1 < lead) below |= u[i];
+        E0 = 64 * lead - lz;
     }
-    if (neg) r = -r;
-    const int s2 = sc + sh;
-    if (s2 >= -1022 && s2 <= 1023) {
-        const double p = r * __longlong_as_double((long long)(s2 + 1023) << 52);
-        if (fabs(p) >= 0x1p-1022 || r == 0.0) return p;     // exact
-    }
-    return ldexp(ldexp(r, sh), sc);                         // rare: extreme exponents (one rounding)
+    uint64_t mant = top >> 11;                             // 53 bits, leading one at bit 52
+    const uint64_t rbit = (top >> 10) & 1ull;
+    const uint64_t sticky = ((top & 0x3ffull) | below) ? 1ull : 0ull;
+    mant += rbit & (sticky | (mant & 1ull));               // round half to even (may reach 2^53)
+    const int ebias = 63 + E0 + sc + 1023;                 // biased exponent of mant * 2^(11 + E0 + sc)
+    const uint64_t sign = (uint64_t)(s & 0x80000000u) << 32;
+    if (ebias >= 1 && ebias <= 2046)
+        return __longlong_as_double((long long)(sign | (((uint64_t)(ebias - 1) << 52) + mant)));
+    // rare: subnormal or overflowing result -- RN(X) is mant * 2^(11 + E0) exactly
+    const double r = ldexp((double)mant, 11 + E0);
+    return ldexp(s ? -r : r, sc);
 }
 
-template <int P, int L>
-__device__ __forceinline__ Limbs<L> assemble_biased(const uint64_t (&b)[5]) {
-    Limbs<L> X = place<L, 0>((uint32_t)b[0], (uint32_t)(b[0] >> 32));
-    if constexpr (P > 1) ladd<L>(X, place<L, 1>((uint32_t)b[1], (uint32_t)(b[1] >> 32)));
-    if constexpr (P > 2) ladd<L>(X, place<L, 2>((uint32_t)b[2], (uint32_t)(b[2] >> 32)));
-    if constexpr (P > 3) ladd<L>(X, place<L, 3>((uint32_t)b[3], (uint32_t)(b[3] >> 32)));
-    if constexpr (P > 4) ladd<L>(X, place<L, 4>((uint32_t)b[4], (uint32_t)(b[4] >> 32)));
-    return X;
+// 4 x 4 byte transpose: out[e] byte i = byte e of in[i]
+__device__ __forceinline__ void transpose4x4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t (&o)[4]) {
+    const uint32_t ab_lo = prmt(a, b, 0x5140u), ab_hi = prmt(a, b, 0x7362u);
+    const uint32_t cd_lo = prmt(c, d, 0x5140u), cd_hi = prmt(c, d, 0x7362u);
+    o[0] = prmt(ab_lo, cd_lo, 0x5410u);
+    o[1] = prmt(ab_lo, cd_lo, 0x7632u);
+    o[2] = prmt(ab_hi, cd_hi, 0x5410u);
+    o[3] = prmt(ab_hi, cd_hi, 0x7632u);
 }
 
-// lines 8-10 from the reduced residues r_t = c''_t in [0, m_t):
-//   S_p = sum_t r_t W[p][t] exactly (W < 2^38, r < 2^8, N <= 20: every partial
-//   sum < 2^51); Q ~ S/M rounded (from the top two pieces, within +-1 of
-//   floor(S/M + 1/2)); X_p = S_p - Q M_p with |X_p| < 2^51, so X_p + 1.5*2^52 is
-//   exact and its bit pattern is X_p + 0x4338000000000000: the pieces are
-//   summed as integers (mod 2^128, or 2^192 for N >= 16), the bias removed,
-//   and X corrected by +-M into [-M/2, M/2) -- the exact Eq. (1) result.
+// lines 8-10 from the reduced residues c''_t in [0, m_t), packed 4 per word
+// (byte i of P[g] = c''_(4g+i), 0 beyond N), entirely in integer arithmetic
+// (FP64 in the GEMM epilogue would compete with the tensor pipe):
+//   line 8:  S = sum_t c''_t w_t exactly: per byte j of the weights
+//            s_j = sum_g dp4a(P[g], Wb[j][g]) < 2^21, S = sum_j s_j 2^(8j)
+//            accumulated into 32-bit words (64-bit column sums, carries);
+//   line 9:  Q = rint(S / M) from the top two words in FP32 (within +-1 of
+//            floor(S/M + 1/2)), X = S - Q M mod 2^(32 WX), then one exact +-M
+//            correction into [-M/2, M/2) -- the Eq. (1) result for every S;
+//   line 10: C = 2^-(e+f) RN(X).
 template <int NM>
-__device__ __forceinline__ double crt_from_residues(const uint32_t (&r)[NM], int ei, int fj) {
+__device__ __forceinline__ double crt_from_packed(const uint32_t (&P)[(NM + 3) / 4], int ei, int fj) {
     const Oz2Table& T = c_tab[NM];
-    constexpr int P = crt_pieces(NM);
-    constexpr int L = NM <= 15 ? 4 : 6;                          // |X| < M/2 < 2^118 (N <= 15)
-    constexpr double MAGIC = 6755399441055744.0;                 // 1.5 * 2^52
-    double S[P];
+    constexpr int G = (NM + 3) / 4, JB = crt_bytes(NM), WS = crt_swords(NM), WX = crt_words(NM);
+    uint32_t S[WS];
+    uint64_t carry = 0;
     #pragma unroll
-    for (int p = 0; p < P; p++) S[p] = 0.0;
-    #pragma unroll
-    for (int t = 0; t < NM; t++) {
-        const double rt = u32_to_double(r[t]);
+    for (int w = 0; w < WS; w++) {
+        uint64_t col = carry;
         #pragma unroll
-        for (int p = 0; p < P; p++) S[p] = fma(rt, T.W[p][t], S[p]);       // exact
+        for (int i = 0; i < 4; i++) {
+            const int j = 4 * w + i;
+            if (j < JB) {
+                uint32_t sj = 0;
+                #pragma unroll
+                for (int g = 0; g < G; g++) sj = dp4a_uu(P[g], T.Wb[j][g], sj);
+                col += (uint64_t)sj << (8 * i);
+            }
+        }
+        S[w] = (uint32_t)col;
+        carry = col >> 32;
     }
-    const double top = P >= 2 ? fma(S[P - 1], 0x1p38, S[P - 2]) : S[0];
-    const double Q = fma(top, T.invM, MAGIC) - MAGIC;                       // rint(S / M), approximately
-    uint64_t b[5] = {0, 0, 0, 0, 0};
+    const float top = WS >= 2 ? fmaf(__uint2float_rn(S[WS - 1]), 4294967296.0f, __uint2float_rn(S[WS - 2]))
+                              : __uint2float_rn(S[0]);
+    const uint32_t Q = (uint32_t)(__float_as_int(fmaf(top, T.qscale, 12582912.0f)) - 0x4B400000);
+    uint32_t X[WX], QM[WX];
+    {
+        uint64_t c = 0;
+        #pragma unroll
+        for (int w = 0; w < WX; w++) {
+            X[w] = S[w];
+            const uint64_t p = (uint64_t)Q * T.M32[w] + c;
+            QM[w] = (uint32_t)p;
+            c = p >> 32;
+        }
+    }
+    mw_sub<WX>(X, QM);                                     // X = S - Q M  (mod 2^(32 WX))
+    uint32_t D[WX];
     #pragma unroll
-    for (int p = 0; p < P; p++) b[p] = (uint64_t)__double_as_longlong(fma(-Q, T.Mp[p], S[p] + MAGIC));
-    Limbs<L> X = assemble_biased<P, L>(b);
-    lsub<L>(X, lconst<L>(T.bias));
-    // Eq. (1) range [-M/2, M/2): Q is within one of the exact quotient
-    Limbs<L> D = X;
-    lsub<L>(D, lconst<L>(T.Mhalf));                              // X - M/2
-    Limbs<L> E = X;
-    ladd<L>(E, lconst<L>(T.Mhalf));                              // X + M/2
-    if ((int32_t)D.w[L - 1] >= 0) lsub<L>(X, lconst<L>(T.Mw));
-    else if ((int32_t)E.w[L - 1] < 0) ladd<L>(X, lconst<L>(T.Mw));
+    for (int w = 0; w < WX; w++) D[w] = X[w];
+    mw_sub<WX>(D, T.Mh32);                                 // X - M/2
+    if ((int32_t)D[WX - 1] >= 0) {
+        mw_sub<WX>(X, T.M32);
+    } else {
+        #pragma unroll
+        for (int w = 0; w < WX; w++) D[w] = X[w];
+        mw_add<WX>(D, T.Mh32);                             // X + M/2
+        if ((int32_t)D[WX - 1] < 0) mw_add<WX>(X, T.M32);
+    }
     if (ei == OZ2_EXP_NONFINITE_DEV || fj == OZ2_EXP_NONFINITE_DEV) return __longlong_as_double(0x7ff8000000000000ll);
-    return limbs_to_double_scaled<L>(X, -(ei + fj));
+    return x_to_double_scaled<WX>(X, -(ei + fj));
 }
 
 template <int NM>
 __device__ __forceinline__ double crt_element(const int32_t (&cp)[NM], int ei, int fj) {
-    uint32_t r[NM];
+    constexpr int G = (NM + 3) / 4;
+    uint32_t P[G];
     #pragma unroll
-    for (int t = 0; t < NM; t++) r[t] = reduce_line7<NM>(cp[t], t);
-    return crt_from_residues<NM>(r, ei, fj);
+    for (int g = 0; g < G; g++) P[g] = 0;
+    #pragma unroll
+    for (int t = 0; t < NM; t++) P[t / 4] |= reduce_line7<NM>(cp[t], t) << (8 * (t % 4));
+    return crt_from_packed<NM>(P, ei, fj);
 }
 
 template <int NM>

@@ -4,20 +4,28 @@
 // oz2_dgemm -- lines 7-10 in the epilogue, so no int32 product leaves the chip.
 //
 // One persistent, warp-specialised kernel, CG = 1 (one CTA per 128 x 256 tile)
-// or CG = 2 (a CTA pair per 256 x 256 tile, tcgen05 cta_group::2: each CTA
-// stages its 128 rows of A and 128 of the 256 rows of B, the leader issues the
-// M = 256 MMAs that read both CTAs' shared memory):
+// or CG = 2 (a CTA pair, tcgen05 cta_group::2: each CTA stages its 128 rows of
+// A and half of every 256-row slab of B, the leader issues the M = 256 MMAs
+// that read both CTAs' shared memory).  NH = number of 256-column halves per
+// tile: NH = 2 (default with CG = 2) makes the pair tile 256 x 512 -- two
+// N = 256 MMAs per K step share each A stage, so the pair pulls 48 instead of
+// 64 bytes from L2 per 1024 MACs (the operand feed, not the tensor pipe, is
+// the measured limit: ~9.5 TB/s of TMA traffic at 71 % tensor activity);
+// its 512 int32 accumulator columns fill TMEM, so instead of a double buffer
+// each half has its own "empty" barrier and the next unit's first MMAs into a
+// half wait only for that half's drain:
 //   warp 0       TMA producer: 3-D tensor maps over the residue planes
 //                [N][rows][ld_res] (K-major, 128-byte swizzle), STAGES-deep
 //                mbarrier ring; with CG = 2 both CTAs' loads complete on the
 //                leader's barrier;
 //   warp 1       MMA issuer (leader CTA): tcgen05.mma.kind::i8, K = 32 per
-//                instruction, int32 accumulators in TMEM, double-buffered
-//                (2 x 256 of the 512 TMEM columns); tcgen05.commit frees smem
+//                instruction, int32 accumulators in TMEM (NH = 1: double-
+//                buffered 2 x 256 columns; NH = 2: 2 halves of 256 columns
+//                with per-half empty barriers); tcgen05.commit frees smem
 //                stages and hands accumulators to the epilogue (multicast to
 //                both CTAs with CG = 2);
 //   warp 2       TMEM allocator;
-//   warps 4..11  epilogue (2 warps per TMEM lane quadrant, 4 column chunks each):
+//   warps 4..11  epilogue (2 warps per TMEM lane quadrant, 4 * NH column chunks each):
 //                RAW:   tcgen05.ld -> int32 C'_t to global (split API);
 //                FUSED: tcgen05.ld -> c''_t = C'_t mod m_t (line 7) -> uint8
 //                scratch; at t = N-1 the tile's N residues are combined by the
@@ -37,7 +45,7 @@ namespace oz2 {
 namespace gemm {
 
 constexpr int BM = 128;             // rows of A per CTA (UMMA M per CTA)
-constexpr int BN = 256;             // UMMA N (tile columns)
+constexpr int BN = 256;             // UMMA N (columns of one accumulator half)
 constexpr int BK = 128;             // bytes = int8 elements per stage (one 128B swizzle row)
 constexpr int UK = 32;              // K per tcgen05.mma kind::i8
 constexpr int EPI_WARPS = 8;
@@ -45,31 +53,34 @@ constexpr int THREADS = 128 + 32 * EPI_WARPS;
 constexpr int EPI_WARP0 = 4;
 constexpr int GROUP_TM = 8;         // tile rows per raster group
 constexpr uint32_t TMEM_COLS = 512;
-constexpr int TILE_BYTES = BM * BN; // one uint8 residue tile (per CTA)
 
-template <int CG>
+template <int CG, int NH>
 struct Cfg {
-    static constexpr int B_ROWS = BN / CG;              // rows of B'^T staged per CTA
+    static constexpr int B_ROWS = BN / CG;              // rows of B'^T staged per CTA per half
     static constexpr int A_BYTES = BM * BK;
-    static constexpr int B_BYTES = B_ROWS * BK;
-    static constexpr int STAGES = CG == 2 ? 6 : 4;
+    static constexpr int B_HALF_BYTES = B_ROWS * BK;
+    static constexpr int B_BYTES = NH * B_HALF_BYTES;
+    static constexpr int STAGES = CG == 2 ? (NH == 2 ? 4 : 6) : 4;
     static constexpr int TILE_M = BM * CG;              // output rows per tile
+    static constexpr int TILE_N = BN * NH;              // output columns per tile
+    static constexpr int TILE_BYTES = BM * TILE_N;      // one uint8 residue tile (per CTA, per modulus)
+    static constexpr int CHUNKS = 4 * NH;               // 32-column chunks per epilogue warp
 };
 
-template <int CG>
+template <int CG, int NH>
 struct __align__(1024) Smem {
-    uint8_t a[Cfg<CG>::STAGES][Cfg<CG>::A_BYTES];
-    uint8_t b[Cfg<CG>::STAGES][Cfg<CG>::B_BYTES];
-    uint64_t full[Cfg<CG>::STAGES];
-    uint64_t empty[Cfg<CG>::STAGES];
+    uint8_t a[Cfg<CG, NH>::STAGES][Cfg<CG, NH>::A_BYTES];
+    uint8_t b[Cfg<CG, NH>::STAGES][Cfg<CG, NH>::B_BYTES];
+    uint64_t full[Cfg<CG, NH>::STAGES];
+    uint64_t empty[Cfg<CG, NH>::STAGES];
     uint64_t tfull[2];
-    uint64_t tempty[2];
+    uint64_t tempty[2];      // NH = 1: per accumulator buffer; NH = 2: per half
     uint32_t tmem_base;
 };
 
 struct Params {
     int m, n, k, N;
-    int num_tm, num_tn, num_kb;     // tiles of TILE_M x BN
+    int num_tm, num_tn, num_kb;     // tiles of TILE_M x TILE_N
     int group_tm;                   // tile rows per raster group
     int epi_nop;                    // experiment only: epilogue drains TMEM and does nothing else
     unsigned long long* dbg;        // experiment only: per-CTA wait-cycle counters (or NULL)
@@ -123,7 +134,7 @@ __device__ __forceinline__ void reduce32(const uint32_t (&v)[32], int t, uint32_
 
 // lines 8-10 for this thread's row and 8 columns [col0, col0 + 8) of a finished
 // tile (32-column chunk c, 8-column group hh) from its N residue bytes in scratch
-template <int NM>
+template <int NM, int TILE_BYTES>
 __device__ __forceinline__ void crt_slice(const Params& p, const uint8_t* tile_scr, int c, int hh, int r,
                                           int row, int col0, int ei) {
     uint32_t wt[NM][2];
@@ -136,21 +147,27 @@ __device__ __forceinline__ void crt_slice(const Params& p, const uint8_t* tile_s
     double* crow = p.C + (int64_t)row * p.ldc + col0;
     const int ncol = p.n - col0;
     const bool vec = ncol >= 8 && ((reinterpret_cast<uintptr_t>(crow) & 15) == 0);
+    constexpr int G = (NM + 3) / 4;
     #pragma unroll
     for (int q = 0; q < 2; q++) {                      // word q of each residue row: columns 4q..4q+3
+        uint32_t P[4][G];                              // P[e][g] byte i = c''_(4g+i) of column 4q+e
+        #pragma unroll
+        for (int g = 0; g < G; g++) {
+            uint32_t o[4];
+            transpose4x4(wt[4 * g][q], 4 * g + 1 < NM ? wt[4 * g + 1][q] : 0u,
+                         4 * g + 2 < NM ? wt[4 * g + 2][q] : 0u, 4 * g + 3 < NM ? wt[4 * g + 3][q] : 0u, o);
+            #pragma unroll
+            for (int e = 0; e < 4; e++) P[e][g] = o[e];
+        }
         #pragma unroll 1
         for (int pr = 0; pr < 2; pr++) {                // column pair (4q + 2pr, 4q + 2pr + 1)
             const int j = 4 * q + 2 * pr;
             double o[2];
             #pragma unroll
             for (int jj = 0; jj < 2; jj++) {
-                uint32_t res[NM];
-                const uint32_t sel = 0x4440u | (uint32_t)(2 * pr + jj);
-                #pragma unroll
-                for (int tt = 0; tt < NM; tt++) res[tt] = prmt(wt[tt][q], 0u, sel);
                 const int col = col0 + j + jj;
                 const int fj = col < p.n ? __ldg(p.f + col) : 0;
-                o[jj] = crt_from_residues<NM>(res, ei, fj);
+                o[jj] = crt_from_packed<NM>(P[2 * pr + jj], ei, fj);
             }
             if (vec) {
                 *reinterpret_cast<double2*>(crow + j) = make_double2(o[0], o[1]);
@@ -162,14 +179,15 @@ __device__ __forceinline__ void crt_slice(const Params& p, const uint8_t* tile_s
     }
 }
 
-template <int NM, int CG>
+template <int NM, int CG, int NH>
 __global__ void __launch_bounds__(THREADS, 1)
 modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const Params p) {
-    using C_ = Cfg<CG>;
+    using C_ = Cfg<CG, NH>;
     constexpr bool FUSED = NM > 0;
+    constexpr int TB = C_::TILE_BYTES;
     extern __shared__ uint8_t smem_raw[];
-    Smem<CG>& s = *reinterpret_cast<Smem<CG>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Smem<CG, NH>& s = *reinterpret_cast<Smem<CG, NH>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
     const bool leader = rank == 0;
@@ -181,7 +199,9 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         for (int i = 0; i < C_::STAGES; i++) { mbar_init(smem_u32(&s.full[i]), 1); mbar_init(smem_u32(&s.empty[i]), 1); }
-        for (int i = 0; i < 2; i++) { mbar_init(smem_u32(&s.tfull[i]), 1); mbar_init(smem_u32(&s.tempty[i]), CG * EPI_WARPS); }
+        // tempty: NH = 1 -> all 8 epilogue warps of both CTAs drain a buffer;
+        //         NH = 2 -> the 4 warps of one half (per CTA) drain that half
+        for (int i = 0; i < 2; i++) { mbar_init(smem_u32(&s.tfull[i]), 1); mbar_init(smem_u32(&s.tempty[i]), CG * EPI_WARPS / NH); }
         fence_barrier_init();
     }
     if (warp == 2) {
@@ -208,13 +228,15 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 int ptm, ptn;
                 tile_coords(p, pj, ptm, ptn);
                 tma_prefetch_3d(&tmA, pkb * BK, ptm * C_::TILE_M + (int)rank * BM, pt);
-                tma_prefetch_3d(&tmB, pkb * BK, ptn * BN + (int)rank * C_::B_ROWS, pt);
+                #pragma unroll
+                for (int h = 0; h < NH; h++)
+                    tma_prefetch_3d(&tmB, pkb * BK, ptn * C_::TILE_N + h * BN + (int)rank * C_::B_ROWS, pt);
                 if (++pkb == p.num_kb) { pkb = 0; if (++pt == p.N) { pt = 0; pj += ncl; } }
             };
             for (int i = 0; i < p.pf_dist; i++) prefetch_next();
             for_each_unit(p, cid, ncl, [&](int tm, int tn, int t) {
                 const int arow = tm * C_::TILE_M + (int)rank * BM;
-                const int brow = tn * BN + (int)rank * C_::B_ROWS;
+                const int brow = tn * C_::TILE_N + (int)rank * C_::B_ROWS;
                 for (int kb = 0; kb < p.num_kb; kb++) {
                     if (p.sync_ctr && kb_in_step == 0 && step > p.sync_lag) {
                         // stay within sync_lag steps of the slowest CTA: the grid then
@@ -232,10 +254,15 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     if (CG == 2) {
                         const uint32_t fl = mapa_shared(fb, 0);          // the leader's full barrier
                         tma_load_3d_cg2(smem_u32(s.a[stage]), &tmA, fl, kb * BK, arow, t);
-                        tma_load_3d_cg2(smem_u32(s.b[stage]), &tmB, fl, kb * BK, brow, t);
+                        #pragma unroll
+                        for (int h = 0; h < NH; h++)
+                            tma_load_3d_cg2(smem_u32(s.b[stage] + h * C_::B_HALF_BYTES), &tmB, fl, kb * BK,
+                                            brow + h * BN, t);
                     } else {
                         tma_load_3d(smem_u32(s.a[stage]), &tmA, fb, kb * BK, arow, t);
-                        tma_load_3d(smem_u32(s.b[stage]), &tmB, fb, kb * BK, brow, t);
+                        #pragma unroll
+                        for (int h = 0; h < NH; h++)
+                            tma_load_3d(smem_u32(s.b[stage] + h * C_::B_HALF_BYTES), &tmB, fb, kb * BK, brow + h * BN, t);
                     }
                     if (++stage == C_::STAGES) { stage = 0; ph ^= 1; }
                     if (p.pf_dist) prefetch_next();
@@ -254,23 +281,37 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (lane == 0 && leader) {
             const uint32_t idesc = idesc_i8(C_::TILE_M, BN);
             int stage = 0; uint32_t ph = 0;
-            int acc = 0; uint32_t aph = 0;
+            int acc = 0; uint32_t aph = 0;     // NH = 1: buffer and its phase; NH = 2: phase of the halves
             for_each_unit(p, cid, ncl, [&](int, int, int) {
-                { const long long t0 = p.dbg ? clock64() : 0;
-                  mbar_wait(smem_u32(&s.tempty[acc]), aph ^ 1);
-                  if (p.dbg) dbg_tempty += clock64() - t0; }
-                tc_fence_after();
+                if (NH == 1) {
+                    const long long t0 = p.dbg ? clock64() : 0;
+                    mbar_wait(smem_u32(&s.tempty[acc]), aph ^ 1);
+                    if (p.dbg) dbg_tempty += clock64() - t0;
+                    tc_fence_after();
+                }
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
                 for (int kb = 0; kb < p.num_kb; kb++) {
                     { const long long t0 = p.dbg ? clock64() : 0;
                       mbar_wait(smem_u32(&s.full[stage]), ph);
                       if (p.dbg) dbg_full += clock64() - t0; }
                     tc_fence_after();
-                    const uint32_t a0 = smem_u32(s.a[stage]), b0 = smem_u32(s.b[stage]);
+                    const uint32_t a0 = smem_u32(s.a[stage]);
                     #pragma unroll
-                    for (int kk = 0; kk < BK / UK; kk++) {
-                        if (CG == 2) mma_i8_cg2(d, sw128_desc(a0 + kk * UK), sw128_desc(b0 + kk * UK), idesc, (kb | kk) != 0);
-                        else mma_i8(d, sw128_desc(a0 + kk * UK), sw128_desc(b0 + kk * UK), idesc, (kb | kk) != 0);
+                    for (int h = 0; h < NH; h++) {
+                        if (NH == 2 && kb == 0) {
+                            // the first MMA into half h of this unit waits for that half's drain
+                            const long long t0 = p.dbg ? clock64() : 0;
+                            mbar_wait(smem_u32(&s.tempty[h]), aph ^ 1);
+                            if (p.dbg) dbg_tempty += clock64() - t0;
+                            tc_fence_after();
+                        }
+                        const uint32_t b0 = smem_u32(s.b[stage] + h * C_::B_HALF_BYTES);
+                        const uint32_t dh = d + (uint32_t)(h * BN);
+                        #pragma unroll
+                        for (int kk = 0; kk < BK / UK; kk++) {
+                            if (CG == 2) mma_i8_cg2(dh, sw128_desc(a0 + kk * UK), sw128_desc(b0 + kk * UK), idesc, (kb | kk) != 0);
+                            else mma_i8(dh, sw128_desc(a0 + kk * UK), sw128_desc(b0 + kk * UK), idesc, (kb | kk) != 0);
+                        }
                     }
                     // the stage is reusable (in both CTAs) when these MMAs finish
                     if (CG == 2) mma_commit_cg2(smem_u32(&s.empty[stage]), 0x3);
@@ -279,14 +320,17 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 }
                 if (CG == 2) mma_commit_cg2(smem_u32(&s.tfull[acc]), 0x3);   // accumulators ready
                 else mma_commit(smem_u32(&s.tfull[acc]));
-                if (++acc == 2) { acc = 0; aph ^= 1; }
+                if (NH == 1) { if (++acc == 2) { acc = 0; aph ^= 1; } }
+                else aph ^= 1;
             });
         }
     } else if (warp >= EPI_WARP0) {
         // ===================== epilogue (every CTA) =====================
         const int q = warp & 3;                           // TMEM lane quadrant
-        const int half = (warp - EPI_WARP0) >> 2;         // column chunks [4*half, 4*half+4)
+        const int half = (warp - EPI_WARP0) >> 2;         // column chunks [CHUNKS*half, CHUNKS*half + CHUNKS)
         const int r = q * 32 + lane;                      // row within this CTA's 128 rows
+        constexpr int CH = C_::CHUNKS;
+        constexpr int SLICES = 4 * CH;                    // 8-column CRT slices per warp and tile
         uint32_t tempty_leader[2];
         #pragma unroll
         for (int i = 0; i < 2; i++)
@@ -294,14 +338,23 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         int acc = 0; uint32_t aph = 0;
         bool pend = false;                                // a finished tile awaits lines 8-10
         int ptm = 0, ptn = 0, pslot = 0, slot = 0;
+        auto release = [&]() {                            // this warp's TMEM columns may be overwritten
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t bar = tempty_leader[NH == 1 ? acc : half];
+                if (CG == 2) mbar_arrive_cluster(bar);
+                else mbar_arrive(bar);
+            }
+        };
         auto run_slice = [&](int sl) {
           if constexpr (FUSED) {
-            const int c = half * 4 + (sl >> 2), hh = sl & 3;
+            const int c = half * CH + (sl >> 2), hh = sl & 3;
             const int prow = ptm * C_::TILE_M + (int)rank * BM + r;
-            const int col0 = ptn * BN + c * 32 + hh * 8;
+            const int col0 = ptn * C_::TILE_N + c * 32 + hh * 8;
             if (prow < p.m && col0 < p.n) {
-                const uint8_t* pscr = p.scratch + (((size_t)blockIdx.x * 2 + pslot) * NM) * TILE_BYTES;
-                crt_slice<NM>(p, pscr, c, hh, r, prow, col0, __ldg(p.e + prow));
+                const uint8_t* pscr = p.scratch + (((size_t)blockIdx.x * 2 + pslot) * NM) * TB;
+                crt_slice<NM, TB>(p, pscr, c, hh, r, prow, col0, __ldg(p.e + prow));
             }
           }
         };
@@ -312,26 +365,21 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
             if (p.epi_nop) {
                 #pragma unroll 1
-                for (int cc = 0; cc < 4; cc++) {
+                for (int cc = 0; cc < CH; cc++) {
                     uint32_t v[32];
-                    tmem_ld_32x32b_x32(tbase + (uint32_t)((half * 4 + cc) * 32), v);
+                    tmem_ld_32x32b_x32(tbase + (uint32_t)((half * CH + cc) * 32), v);
                     tmem_ld_wait();
                     if (v[0] == 0x12345678u && v[31] == 0x9abcdef0u) p.cprod[0] = 1;   // keep the loads alive
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    if (CG == 2) mbar_arrive_cluster(tempty_leader[acc]);
-                    else mbar_arrive(tempty_leader[acc]);
-                }
+                release();
             } else if constexpr (!FUSED) {
                 #pragma unroll 1
-                for (int cc = 0; cc < 4; cc++) {
-                    const int c = half * 4 + cc;
+                for (int cc = 0; cc < CH; cc++) {
+                    const int c = half * CH + cc;
                     uint32_t v[32];
                     tmem_ld_32x32b_x32(tbase + (uint32_t)(c * 32), v);
                     tmem_ld_wait();
-                    const int col0 = tn * BN + c * 32;
+                    const int col0 = tn * C_::TILE_N + c * 32;
                     if (row < p.m) {
                         int32_t* dst = p.cprod + ((int64_t)t * p.m + row) * p.n + col0;
                         if (col0 + 32 <= p.n && (p.n & 3) == 0) {
@@ -345,46 +393,37 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         }
                     }
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    if (CG == 2) mbar_arrive_cluster(tempty_leader[acc]);
-                    else mbar_arrive(tempty_leader[acc]);
-                }
+                release();
             } else {
-                // line 7 for the 4 chunks -> uint8 residues in this tile's scratch slot
-                uint8_t* tile_scr = p.scratch + (((size_t)blockIdx.x * 2 + slot) * NM) * TILE_BYTES;
-                #pragma unroll
-                for (int cc = 0; cc < 4; cc++) {
-                    const int c = half * 4 + cc;
+                // line 7 for this warp's chunks -> uint8 residues in this tile's scratch slot
+                uint8_t* tile_scr = p.scratch + (((size_t)blockIdx.x * 2 + slot) * NM) * TB;
+                #pragma unroll 2
+                for (int cc = 0; cc < CH; cc++) {
+                    const int c = half * CH + cc;
                     uint32_t v[32], w[8];
                     tmem_ld_32x32b_x32(tbase + (uint32_t)(c * 32), v);
                     tmem_ld_wait();
                     reduce32<NM>(v, t, w);
-                    uint4* d4 = reinterpret_cast<uint4*>(tile_scr + (size_t)t * TILE_BYTES + ((size_t)(c * BM + r)) * 32);
+                    uint4* d4 = reinterpret_cast<uint4*>(tile_scr + (size_t)t * TB + ((size_t)(c * BM + r)) * 32);
                     d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
                     d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {                                   // TMEM buffer free
-                    if (CG == 2) mbar_arrive_cluster(tempty_leader[acc]);
-                    else mbar_arrive(tempty_leader[acc]);
-                }
-                // lines 8-10 of the previous tile, 16 slices of 8 columns spread
+                release();
+                // lines 8-10 of the previous tile, SLICES slices of 8 columns spread
                 // over this tile's N units (no burst that would hold TMEM back)
                 if (pend) {
-                    const int s0 = (t * 16) / NM, s1 = ((t + 1) * 16) / NM;
+                    const int s0 = (t * SLICES) / NM, s1 = ((t + 1) * SLICES) / NM;
                     for (int sl = s0; sl < s1; sl++) run_slice(sl);
                 }
                 if (t == NM - 1) {
                     pend = true; ptm = tm; ptn = tn; pslot = slot; slot ^= 1;
                 }
             }
-            if (++acc == 2) { acc = 0; aph ^= 1; }
+            if (NH == 1) { if (++acc == 2) { acc = 0; aph ^= 1; } }
+            else aph ^= 1;
         });
         if constexpr (FUSED) {
-            if (pend) for (int sl = 0; sl < 16; sl++) run_slice(sl);    // the last tile
+            if (pend) for (int sl = 0; sl < SLICES; sl++) run_slice(sl);    // the last tile
         }
     }
 
@@ -402,13 +441,13 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     }
 }
 
-template <int NM, int CG>
+template <int NM, int CG, int NH>
 static int launch_nm(const CUtensorMap* tmA, const CUtensorMap* tmB, const Params& p, int grid, cudaStream_t st) {
-    const size_t smem = sizeof(Smem<CG>) + 1024;
+    const size_t smem = sizeof(Smem<CG, NH>) + 1024;
     static bool attr_done[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
-    auto kern = modmul_kernel<NM, CG>;
+    auto kern = modmul_kernel<NM, CG, NH>;
     if (dev < 64 && !attr_done[dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
@@ -429,6 +468,17 @@ static int launch_nm(const CUtensorMap* tmA, const CUtensorMap* tmB, const Param
     return (int)cudaLaunchKernelEx(&cfg, kern, *tmA, *tmB, p);
 }
 
+// the three supported shapes: (CG, NH) = (2, 2) default, (2, 1), (1, 1)
+template <int NM>
+static int launch_shape(int shape, const CUtensorMap* tmA, const CUtensorMap* tmB, const Params& p, int grid,
+                        cudaStream_t st) {
+    switch (shape) {
+        case 22: return launch_nm<NM, 2, 2>(tmA, tmB, p, grid, st);
+        case 21: return launch_nm<NM, 2, 1>(tmA, tmB, p, grid, st);
+        default: return launch_nm<NM, 1, 1>(tmA, tmB, p, grid, st);
+    }
+}
+
 }  // namespace gemm
 
 static int env_int(const char* name, int dflt) {
@@ -436,16 +486,18 @@ static int env_int(const char* name, int dflt) {
     return v && *v ? atoi(v) : dflt;
 }
 
-// tuning knobs for experiments (env): OZ2_CG (1 | 2), OZ2_GROUP_TM, OZ2_TILE_MAJOR
+// tuning knobs for experiments (env): OZ2_CG (1 | 2), OZ2_NH (1 | 2, CG = 2 only), OZ2_GROUP_TM, ...
 int gemm_cta_group() { return env_int("OZ2_CG", 2) == 1 ? 1 : 2; }
+int gemm_halves() { return gemm_cta_group() == 2 && env_int("OZ2_NH", 2) == 2 ? 2 : 1; }
+static int gemm_shape() { return gemm_cta_group() * 10 + gemm_halves(); }
 
-static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_sms, int cg, int* grid_out) {
+static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_sms, int cg, int nh, int* grid_out) {
     using namespace gemm;
     Params p{};
     p.m = (int)m; p.n = (int)n; p.k = (int)k; p.N = N;
-    const int tile_m = BM * cg;
+    const int tile_m = BM * cg, tile_n = BN * nh;
     p.num_tm = (int)((m + tile_m - 1) / tile_m);
-    p.num_tn = (int)((n + BN - 1) / BN);
+    p.num_tn = (int)((n + tile_n - 1) / tile_n);
     p.num_kb = (int)((k + BK - 1) / BK);
     p.group_tm = std::max(1, env_int("OZ2_GROUP_TM", GROUP_TM));
     p.epi_nop = env_int("OZ2_EPI_NOP", 0);
@@ -453,7 +505,7 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
     const int tiles = p.num_tm * p.num_tn;
     const int nclusters = num_sms / cg;
     const int ncl = tiles < nclusters ? tiles : nclusters;
-    p.sync_kb = env_int("OZ2_SYNC_KB", 32);
+    p.sync_kb = env_int("OZ2_SYNC_KB", 32 / nh);
     p.sync_lag = env_int("OZ2_SYNC_LAG", 0);
     {
         // busiest CTA: its tiles x N moduli x num_kb k-blocks, in sync_kb steps
@@ -466,27 +518,26 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
 
 size_t fused_scratch_bytes(int64_t m, int64_t n, int N, int num_sms) {
     int grid;
-    make_params(m, n, 1, N, num_sms, gemm_cta_group(), &grid);
-    return (size_t)grid * 2 * N * gemm::TILE_BYTES;
+    const int cg = gemm_cta_group(), nh = gemm_halves();
+    make_params(m, n, 1, N, num_sms, cg, nh, &grid);
+    return (size_t)grid * 2 * N * gemm::BM * gemm::BN * nh;
 }
 
 int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                   int N, int32_t* cprod, uint32_t* sync_ctr, int num_sms, cudaStream_t st) {
-    const int cg = gemm_cta_group();
     int grid;
-    gemm::Params p = make_params(m, n, k, N, num_sms, cg, &grid);
+    gemm::Params p = make_params(m, n, k, N, num_sms, gemm_cta_group(), gemm_halves(), &grid);
     p.cprod = cprod;
     p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
     if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
-    return cg == 2 ? gemm::launch_nm<0, 2>(tmA, tmB, p, grid, st) : gemm::launch_nm<0, 1>(tmA, tmB, p, grid, st);
+    return gemm::launch_shape<0>(gemm_shape(), tmA, tmB, p, grid, st);
 }
 
 int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                         int N, uint8_t* scratch, const int32_t* e, const int32_t* f, double* C, int64_t ldc,
                         uint32_t* sync_ctr, int num_sms, cudaStream_t st) {
-    const int cg = gemm_cta_group();
     int grid;
-    gemm::Params p = make_params(m, n, k, N, num_sms, cg, &grid);
+    gemm::Params p = make_params(m, n, k, N, num_sms, gemm_cta_group(), gemm_halves(), &grid);
     p.scratch = scratch; p.e = e; p.f = f; p.C = C; p.ldc = ldc;
     p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
     if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
@@ -511,9 +562,9 @@ int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t 
                     tot / grid, sf / grid, se / grid, st_ / (grid / 2.0), sfu / (grid / 2.0));
         }
     } dbgp{want_dbg, dbg, grid, st};
+    const int shape = gemm_shape();
     switch (N) {
-#define OZ2_CASE(NN) case NN: return cg == 2 ? gemm::launch_nm<NN, 2>(tmA, tmB, p, grid, st) \
-                                             : gemm::launch_nm<NN, 1>(tmA, tmB, p, grid, st);
+#define OZ2_CASE(NN) case NN: return gemm::launch_shape<NN>(shape, tmA, tmB, p, grid, st);
         OZ2_CASE(2) OZ2_CASE(3) OZ2_CASE(4) OZ2_CASE(5) OZ2_CASE(6) OZ2_CASE(7) OZ2_CASE(8)
         OZ2_CASE(9) OZ2_CASE(10) OZ2_CASE(11) OZ2_CASE(12) OZ2_CASE(13) OZ2_CASE(14) OZ2_CASE(15)
         OZ2_CASE(16) OZ2_CASE(17) OZ2_CASE(18) OZ2_CASE(19) OZ2_CASE(20)

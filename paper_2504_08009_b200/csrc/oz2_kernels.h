@@ -6,11 +6,16 @@
 
 namespace oz2 {
 
-// number of 38-bit pieces of M = prod of the first N moduli (ceil(bitlen(M) / 38));
-// tables.cpp computes the same value and api.cu checks they agree
-__host__ __device__ constexpr int crt_pieces(int N) {
-    return N <= 4 ? 1 : (N <= 9 ? 2 : (N <= 14 ? 3 : (N <= 19 ? 4 : 5)));
+// bit length of M = prod of the first N moduli (N = 2..20; tables.cpp computes M
+// itself and api.cu checks that its limb and word counts agree with these)
+__host__ __device__ constexpr int m_bits(int N) {
+    constexpr int b[21] = {0, 8, 16, 24, 32, 40, 48, 56, 64, 72, 80, 87, 95, 103, 110, 118, 126, 133, 141, 148, 156};
+    return b[N];
 }
+// bytes of M; 32-bit words of S < 2^13 M; 32-bit words of X in [-3M/2, 3M/2)
+__host__ __device__ constexpr int crt_bytes(int N) { return (m_bits(N) + 7) / 8; }
+__host__ __device__ constexpr int crt_swords(int N) { return (m_bits(N) + 13 + 31) / 32; }
+__host__ __device__ constexpr int crt_words(int N) { return (m_bits(N) + 2 + 31) / 32; }
 
 int host_T(int N);   // floor(L/2) for N moduli (host copy of the table)
 

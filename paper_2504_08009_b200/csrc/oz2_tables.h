@@ -6,12 +6,15 @@
 #include <stdint.h>
 
 #define OZ2_MAX_MODULI 20
-#define OZ2_PIECE_BITS 38   // CRT weights and M are split into 38-bit FP64 pieces
-#define OZ2_MAX_PIECES 5
+#define OZ2_MAX_BYTES 20    // bytes of M (and of every w_t < M): M < 2^156 for N <= 20
+#define OZ2_MAX_GROUPS 5    // groups of 4 moduli (one dp4a per group and byte)
+#define OZ2_MAX_WORDS 5     // 32-bit words of X in [-3M/2, 3M/2), two's complement
 
 struct Oz2Table {
     int32_t N;           // number of moduli
-    int32_t P;           // number of 38-bit pieces of M (1..5)
+    int32_t JB;          // bytes of M (1..20)
+    int32_t WS;          // 32-bit words of S = sum_t c''_t w_t < 2^13 M (1..6)
+    int32_t WX;          // 32-bit words that hold X in [-3M/2, 3M/2) (1..5)
     int32_t L;           // floor(log2(M/2 - 1))        (Eq. 16 with q dropped)
     int32_t T;           // floor(L/2): FAST bound ||2^e a||_2 <= 2^T   (reading R4)
     int32_t m[OZ2_MAX_MODULI];        // moduli, Eq. (18) + reading R1
@@ -25,13 +28,14 @@ struct Oz2Table {
     uint32_t G63[OZ2_MAX_MODULI];     // (-2^63) mod m_t: undoes the 2^63 bias of 64-bit residue inputs
     uint32_t G95[OZ2_MAX_MODULI];     // (-2^95) mod m_t: same for 96-bit inputs
     uint64_t hmagic[OZ2_MAX_MODULI];  // h_t * magic_t: floor((y + h)/m) = (y * magic + hmagic) >> 32
-    double W[OZ2_MAX_PIECES][OZ2_MAX_MODULI];  // w_t = M y_t / m_t = sum_p W[p][t] 2^(38p), W < 2^38
-    double Mp[OZ2_MAX_PIECES];        // M = sum_p Mp[p] 2^(38p)
-    double invM;                      // 2^(38(P-2)) / M  (P >= 2),  1/M  (P == 1)
-    uint64_t bias[3];                 // (0x4338000000000000 * sum_p 2^(38p)) mod 2^192 (piece-extraction bias)
-    double inv_m[OZ2_MAX_MODULI];     // 1.0 / m_t
-    uint64_t Mw[3];                   // M, 192-bit little endian
-    uint64_t Mhalf[3];                // M / 2
+    // w_t = M y_t / m_t (Alg. 1 line 8) as bytes, packed for dp4a: byte i of
+    // Wb[j][g] is byte j of w_(4g+i) (0 beyond N), so that
+    // sum_t c''_t byte_j(w_t) = sum_g dp4a(c''_(4g..4g+3), Wb[j][g])
+    uint32_t Wb[OZ2_MAX_BYTES][OZ2_MAX_GROUPS];
+    uint32_t w32[OZ2_MAX_MODULI][OZ2_MAX_WORDS];  // w_t as 32-bit words (host export / tests)
+    uint32_t M32[OZ2_MAX_WORDS];      // M, 32-bit words, little endian
+    uint32_t Mh32[OZ2_MAX_WORDS];     // M / 2, same
+    float qscale;                     // 2^(32 (WS - 2)) / M (WS >= 2), 1 / M (WS = 1)
     int32_t y[OZ2_MAX_MODULI];        // least positive inverse of M_t mod m_t (host only)
 };
 

@@ -98,42 +98,22 @@ int oz2_build_tables(Oz2Table tabs[OZ2_MAX_MODULI + 1]) {
         T.N = N;
         Nat M = product(N);
         int Mbits = M.bits();
-        T.P = (Mbits + OZ2_PIECE_BITS - 1) / OZ2_PIECE_BITS;
+        T.JB = (Mbits + 7) / 8;
+        T.WS = (Mbits + 13 + 31) / 32;                // S < 20 * 255 * M < 2^13 M
+        T.WX = (Mbits + 2 + 31) / 32;                 // 3M/2 < 2^(Mbits + 1) fits 32 WX - 1 bits
         Nat half = shr1(M);                            // M is even (m_1 = 256)
         T.L = sub_small(half, 1).bits() - 1;
         T.T = T.L / 2;
-        for (int p = 0; p < OZ2_MAX_PIECES; p++) T.Mp[p] = (double)bits_at(M, OZ2_PIECE_BITS * p, OZ2_PIECE_BITS);
-        {
-            // bias = sum_p 0x4338000000000000 * 2^(38p) mod 2^192, as three 64-bit limbs
-            uint64_t b[3] = {0, 0, 0};
-            for (int p = 0; p < T.P; p++) {
-                const int sh = OZ2_PIECE_BITS * p;
-                const unsigned __int128 v = (unsigned __int128)0x4338000000000000ull;
-                uint64_t add[3] = {0, 0, 0};
-                // v << sh into 192 bits
-                for (int bit = 0; bit < 64; bit++)
-                    if ((uint64_t)(v >> bit) & 1ull) {
-                        const int pos = bit + sh;
-                        if (pos < 192) add[pos / 64] |= 1ull << (pos % 64);
-                    }
-                unsigned __int128 c = 0;
-                for (int w = 0; w < 3; w++) {
-                    c += (unsigned __int128)b[w] + add[w];
-                    b[w] = (uint64_t)c;
-                    c >>= 64;
-                }
-            }
-            for (int w = 0; w < 3; w++) T.bias[w] = b[w];
+        for (int w = 0; w < OZ2_MAX_WORDS; w++) {
+            T.M32[w] = (uint32_t)bits_at(M, 32 * w, 32);
+            T.Mh32[w] = (uint32_t)bits_at(half, 32 * w, 32);
         }
-        for (int w = 0; w < 3; w++) { T.Mw[w] = bits_at(M, 64 * w, 64); T.Mhalf[w] = bits_at(half, 64 * w, 64); }
-        double Md = to_double(M);
-        T.invM = T.P >= 2 ? ldexp(1.0, OZ2_PIECE_BITS * (T.P - 2)) / Md : 1.0 / Md;
+        T.qscale = (float)((T.WS >= 2 ? ldexp(1.0, 32 * (T.WS - 2)) : 1.0) / to_double(M));
         for (int t = 0; t < N; t++) {
             int64_t m = kModuli[t];
             T.m[t] = (int32_t)m;
             T.magic[t] = (uint32_t)(((1ull << 32) + (uint64_t)m - 1) / (uint64_t)m);
             T.h[t] = (int32_t)((m - 1) / 2);
-            T.inv_m[t] = 1.0 / (double)m;
             for (int w = 0; w < 3; w++) {
                 uint32_t packed = 0;
                 for (int b = 0; b < 4; b++) packed |= (uint32_t)pow2_mod(8 * (4 * w + b), m) << (8 * b);
@@ -155,8 +135,10 @@ int oz2_build_tables(Oz2Table tabs[OZ2_MAX_MODULI + 1]) {
             if (y <= 0) return 2;
             T.y[t] = (int32_t)y;
             Nat w = mul_small(Mt, (uint32_t)y);
-            for (int p = 0; p < OZ2_MAX_PIECES; p++) T.W[p][t] = (double)bits_at(w, OZ2_PIECE_BITS * p, OZ2_PIECE_BITS);
-            if (w.bits() > OZ2_PIECE_BITS * T.P) return 3;
+            if (w.bits() > Mbits) return 3;
+            for (int j = 0; j < OZ2_MAX_BYTES; j++)
+                T.Wb[j][t / 4] |= (uint32_t)bits_at(w, 8 * j, 8) << (8 * (t % 4));
+            for (int x = 0; x < OZ2_MAX_WORDS; x++) T.w32[t][x] = (uint32_t)bits_at(w, 32 * x, 32);
         }
     }
     return 0;

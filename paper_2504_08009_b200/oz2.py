@@ -21,7 +21,6 @@ MODE_FAST = 0
 MODE_EQ17 = 1
 EXP_NONFINITE = -(2**31)
 MAX_K = 2**17
-PIECE_BITS = 38
 
 # every symbol include/oz2.h declares (checked by tests/test_abi.py)
 SYMBOLS = [
@@ -102,15 +101,16 @@ def _mode_id(mode) -> int:
 def tables(N: int) -> dict:
     m = np.zeros(N, np.int32)
     y = np.zeros(N, np.int32)
-    W = np.zeros(5 * N, np.float64)
-    Mp = np.zeros(5, np.float64)
-    P, L, T = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    w = np.zeros(5 * N, np.uint32)
+    Mw = np.zeros(5, np.uint32)
+    nb, L, T = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
     c = lambda a: a.ctypes.data_as(ctypes.c_void_p)
-    _check(lib().oz2_tables(N, c(m), c(y), c(W), c(Mp), ctypes.byref(P), ctypes.byref(L),
+    _check(lib().oz2_tables(N, c(m), c(y), c(w), c(Mw), ctypes.byref(nb), ctypes.byref(L),
                             ctypes.byref(T)), "oz2_tables")
+    words = lambda ws: sum(int(v) << (32 * i) for i, v in enumerate(ws))
     return {"moduli": [int(v) for v in m], "y": [int(v) for v in y],
-            "W": W.reshape(5, N)[:P.value].copy(), "Mp": Mp[:P.value].copy(),
-            "P": P.value, "L": L.value, "T": T.value}
+            "w": [words(w[5 * t:5 * t + 5]) for t in range(N)], "M": words(Mw),
+            "nbytes": nb.value, "L": L.value, "T": T.value}
 
 
 def eq17_k(N: int, q: int) -> int:
