@@ -15,14 +15,14 @@
 namespace oz2 {
 
 // line 7: c'' = c' - floor(c'/m_t) m_t in [0, m_t), for any int32 c', in
-// integer arithmetic: u = c' mod 2^32 = hi 2^16 + lo, y = hi (2^16 mod m_t) + lo
-// (+ (-2^32) mod m_t when c' < 0) == c' (mod m_t), y < 2^24, then the magic
-// multiply gives floor(y / m_t) exactly.
+// integer arithmetic: c' = hi 2^16 + lo (hi signed, lo in [0, 2^16)),
+// y = hi k16s + lo + off7 == c' (mod m_t) with |k16s| <= m_t/2, so
+// 0 <= y < 2^23 + 2^17, and the magic multiply gives floor(y / m_t) exactly
+// (exact for y < 2^24).  Six integer instructions.
 template <int NM>
 __device__ __forceinline__ uint32_t reduce_line7(int32_t c, int t) {
     const Oz2Table& T = c_tab[NM];
-    const uint32_t u = (uint32_t)c;
-    const uint32_t y = (u >> 16) * T.k16[t] + (u & 0xffffu) + ((uint32_t)(c >> 31) & T.g32[t]);
+    const uint32_t y = (uint32_t)((c >> 16) * T.k16s[t]) + ((uint32_t)c & 0xffffu) + T.off7[t];
     const uint32_t q = __umulhi(y, T.magic[t]);
     return y - q * (uint32_t)T.m[t];
 }

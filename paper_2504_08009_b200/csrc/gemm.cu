@@ -124,11 +124,11 @@ template <int NM>
 __device__ __forceinline__ void reduce32(const uint32_t (&v)[32], int t, uint32_t (&w)[8]) {
     #pragma unroll
     for (int q = 0; q < 8; q++) {
-        uint32_t r0 = reduce_line7<NM>((int32_t)v[4 * q + 0], t);
-        uint32_t r1 = reduce_line7<NM>((int32_t)v[4 * q + 1], t);
-        uint32_t r2 = reduce_line7<NM>((int32_t)v[4 * q + 2], t);
-        uint32_t r3 = reduce_line7<NM>((int32_t)v[4 * q + 3], t);
-        w[q] = r0 | (r1 << 8) | (r2 << 16) | (r3 << 24);
+        const uint32_t r0 = reduce_line7<NM>((int32_t)v[4 * q + 0], t);
+        const uint32_t r1 = reduce_line7<NM>((int32_t)v[4 * q + 1], t);
+        const uint32_t r2 = reduce_line7<NM>((int32_t)v[4 * q + 2], t);
+        const uint32_t r3 = reduce_line7<NM>((int32_t)v[4 * q + 3], t);
+        w[q] = r3 * 16777216u + (r2 * 65536u + (r1 * 256u + r0));     // bytes < 256: three IMADs
     }
 }
 
@@ -395,16 +395,25 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 }
                 release();
             } else {
-                // line 7 for this warp's chunks -> uint8 residues in this tile's scratch slot
-                uint8_t* tile_scr = p.scratch + (((size_t)blockIdx.x * 2 + slot) * NM) * TB;
-                #pragma unroll 2
-                for (int cc = 0; cc < CH; cc++) {
+                // line 7 for this warp's chunks -> uint8 residues in this tile's scratch slot;
+                // TMEM loads double-buffered: chunk cc + 1 is in flight while cc is reduced
+                uint8_t* tile_scr = p.scratch + (((size_t)blockIdx.x * 2 + slot) * NM) * TB + (size_t)t * TB;
+                uint32_t va[32], vb[32];
+                tmem_ld_32x32b_x32(tbase + (uint32_t)(half * CH * 32), va);
+                #pragma unroll
+                for (int cc = 0; cc < CH; cc += 2) {
                     const int c = half * CH + cc;
-                    uint32_t v[32], w[8];
-                    tmem_ld_32x32b_x32(tbase + (uint32_t)(c * 32), v);
-                    tmem_ld_wait();
-                    reduce32<NM>(v, t, w);
-                    uint4* d4 = reinterpret_cast<uint4*>(tile_scr + (size_t)t * TB + ((size_t)(c * BM + r)) * 32);
+                    uint32_t w[8];
+                    tmem_ld_wait_regs(va);
+                    tmem_ld_32x32b_x32(tbase + (uint32_t)((c + 1) * 32), vb);
+                    reduce32<NM>(va, t, w);
+                    uint4* d4 = reinterpret_cast<uint4*>(tile_scr + ((size_t)(c * BM + r)) * 32);
+                    d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                    d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+                    tmem_ld_wait_regs(vb);
+                    if (cc + 2 < CH) tmem_ld_32x32b_x32(tbase + (uint32_t)((c + 2) * 32), va);
+                    reduce32<NM>(vb, t, w);
+                    d4 = reinterpret_cast<uint4*>(tile_scr + ((size_t)((c + 1) * BM + r)) * 32);
                     d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
                     d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
                 }

@@ -22,6 +22,8 @@ struct Oz2Table {
     int32_t h[OZ2_MAX_MODULI];        // (m - 1) / 2 (odd m): symmetric offset
     uint32_t cw[3][OZ2_MAX_MODULI];   // byte b of cw[w][t] = 2^(8(4w+b)) mod m_t
     uint32_t k16[OZ2_MAX_MODULI];     // 2^16 mod m_t
+    int32_t k16s[OZ2_MAX_MODULI];     // 2^16 mod m_t, symmetric representative (|k16s| <= m_t / 2)
+    uint32_t off7[OZ2_MAX_MODULI];    // m_t * ceil(2^22 / m_t): keeps the line-7 value non-negative
     uint32_t g32[OZ2_MAX_MODULI];     // (-2^32) mod m_t in [0, m_t)
     int32_t g64[OZ2_MAX_MODULI];      // (-2^64) mod m_t in [0, m_t)
     int32_t g96[OZ2_MAX_MODULI];      // (-2^96) mod m_t in [0, m_t)

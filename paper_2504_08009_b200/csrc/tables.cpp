@@ -120,6 +120,8 @@ int oz2_build_tables(Oz2Table tabs[OZ2_MAX_MODULI + 1]) {
                 T.cw[w][t] = packed;
             }
             T.k16[t] = (uint32_t)pow2_mod(16, m);
+            T.k16s[t] = 2 * (int64_t)T.k16[t] > m ? (int32_t)T.k16[t] - (int32_t)m : (int32_t)T.k16[t];
+            T.off7[t] = (uint32_t)(m * (((1 << 22) + m - 1) / m));
             T.g32[t] = (uint32_t)((m - pow2_mod(32, m)) % m);
             T.g64[t] = (int32_t)((m - pow2_mod(64, m)) % m);
             T.g96[t] = (int32_t)((m - pow2_mod(96, m)) % m);
