@@ -87,8 +87,13 @@ int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* 
                  int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                  int num_moduli);
 /* End-to-end variant with HOST buffers: copies A and B to the device, runs
- * oz2_dgemm_ex, copies C back and synchronises the handle's stream.  For full
- * copy bandwidth the host buffers should be page-locked. */
+ * Algorithm 1 and copies C back, then synchronises.  Pipelined over up to 8
+ * row blocks of A / C (rows multiple of 256, >= 4096 rows each): B is copied
+ * and converted first, each row block is converted and multiplied as soon as
+ * it lands, and its C block is copied back on a second copy stream while the
+ * next block computes.  The result is bit-identical to oz2_dgemm_ex.  Copies
+ * overlap only if the host buffers are page-locked.  Workspace (ctx-owned or
+ * oz2_set_workspace): oz2_workspace_bytes(m, n, k, N) + 8 (mk + kn + mn) + 1 KiB. */
 int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A,
                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                    int num_moduli);

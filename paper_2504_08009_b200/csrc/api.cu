@@ -6,6 +6,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 #include <new>
 #include <vector>
@@ -83,6 +84,9 @@ struct oz2_context {
     size_t ws_own_bytes;
     int profiling;
     std::vector<cudaEvent_t> events;   // OZ2_NUM_STAGES + 1 per profiled call
+    // oz2_dgemm_host pipeline: copy streams and events (created on first use)
+    cudaStream_t s_h2d, s_d2h;
+    std::vector<cudaEvent_t> pipe_ev;
 };
 
 namespace {
@@ -256,6 +260,9 @@ int oz2_destroy(oz2_handle_t h) {
     if (!h) return OZ2_ERR_INVALID_ARG;
     DevGuard g(h->device);
     drop_events(h);
+    for (cudaEvent_t ev : h->pipe_ev) cudaEventDestroy(ev);
+    if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
+    if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
     if (h->ws_own) cudaFree(h->ws_own);
     delete h;
     return OZ2_OK;
@@ -488,39 +495,92 @@ int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
     if (rc) return rc;
     if (lda < (k > 0 ? k : 1) || ldb < (n > 0 ? n : 1) || ldc < (n > 0 ? n : 1)) return OZ2_ERR_INVALID_ARG;
     if (m == 0 || n == 0) return OZ2_OK;
+    if (!C || (k > 0 && (!A || !B))) return OZ2_ERR_INVALID_ARG;
+    int kstar = 0;
+    if (k > 0 && (rc = kstar_for(h, N, k, &kstar))) return rc;
     DevGuard g(h->device);
-    // device staging buffers live after the dgemm workspace
-    Layout L = layout_for(m, n, k, N, h->num_sms);
-    size_t bytesA = sizeof(double) * (size_t)m * (size_t)(k > 0 ? k : 1);
-    size_t bytesB = sizeof(double) * (size_t)(k > 0 ? k : 1) * (size_t)n;
-    size_t bytesC = sizeof(double) * (size_t)m * (size_t)n;
-    size_t offA = (size_t)round_up((int64_t)L.total, 256);
-    size_t offB = (size_t)round_up((int64_t)(offA + bytesA), 256);
-    size_t offC = (size_t)round_up((int64_t)(offB + bytesB), 256);
-    size_t total = offC + bytesC;
+    if (k == 0) {
+        for (int64_t i = 0; i < m; i++) memset(C + i * ldc, 0, sizeof(double) * (size_t)n);
+        return OZ2_OK;
+    }
+    // Pipeline over R row blocks of A and C (rows a multiple of 256): B goes
+    // first on the H2D stream and is converted once; row block i is converted and
+    // multiplied as soon as its copy lands, and its C block leaves on the D2H
+    // stream while block i + 1 computes.  Results are bit-identical to one call
+    // (e_i depends on row i only).
+    const int64_t R = std::max<int64_t>(1, std::min<int64_t>(8, m / 4096));
+    const int64_t mb = round_up((m + R - 1) / R, 256);
+    const int64_t nblk = (m + mb - 1) / mb;
+    Layout L = layout_for(mb, n, k, N, h->num_sms);          // A planes and e for one row block
+    const size_t bytesA = sizeof(double) * (size_t)m * (size_t)k;
+    const size_t bytesB = sizeof(double) * (size_t)k * (size_t)n;
+    const size_t bytesC = sizeof(double) * (size_t)m * (size_t)n;
+    const size_t offA = (size_t)round_up((int64_t)L.total, 256);
+    const size_t offB = (size_t)round_up((int64_t)(offA + bytesA), 256);
+    const size_t offC = (size_t)round_up((int64_t)(offB + bytesB), 256);
     uint8_t* ws;
-    if ((rc = get_workspace(h, total, &ws))) return rc;
+    if ((rc = get_workspace(h, offC + bytesC, &ws))) return rc;
     double* dA = (double*)(ws + offA);
     double* dB = (double*)(ws + offB);
     double* dC = (double*)(ws + offC);
-    if (k > 0) {
-        if (cudaMemcpy2DAsync(dA, sizeof(double) * k, A, sizeof(double) * lda, sizeof(double) * k, m,
-                              cudaMemcpyHostToDevice, h->stream) != cudaSuccess) return OZ2_ERR_CUDA;
-        if (cudaMemcpy2DAsync(dB, sizeof(double) * n, B, sizeof(double) * ldb, sizeof(double) * n, k,
-                              cudaMemcpyHostToDevice, h->stream) != cudaSuccess) return OZ2_ERR_CUDA;
+    if (!h->s_h2d && cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking) != cudaSuccess) return OZ2_ERR_CUDA;
+    if (!h->s_d2h && cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking) != cudaSuccess) return OZ2_ERR_CUDA;
+    const size_t nev = (size_t)(2 * nblk + 2);
+    while (h->pipe_ev.size() < nev) {
+        cudaEvent_t ev;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return OZ2_ERR_CUDA;
+        h->pipe_ev.push_back(ev);
     }
-    // the dgemm workspace is the prefix [0, L.total): run with it as a user workspace
-    void* save_ptr = h->ws_user;
-    size_t save_bytes = h->ws_user_bytes;
-    h->ws_user = ws;
-    h->ws_user_bytes = L.total;
-    rc = oz2_dgemm_ex(h, m, n, k, dA, k > 0 ? k : 1, dB, n, dC, n, N);
-    h->ws_user = save_ptr;
-    h->ws_user_bytes = save_bytes;
-    if (rc) return rc;
-    if (cudaMemcpy2DAsync(C, sizeof(double) * ldc, dC, sizeof(double) * n, sizeof(double) * n, m,
-                          cudaMemcpyDeviceToHost, h->stream) != cudaSuccess) return OZ2_ERR_CUDA;
-    return cudaStreamSynchronize(h->stream) == cudaSuccess ? OZ2_OK : OZ2_ERR_CUDA;
+    cudaEvent_t evB = h->pipe_ev[0], evStart = h->pipe_ev[1];
+    cudaEvent_t* evA = &h->pipe_ev[2];
+    cudaEvent_t* evC = &h->pipe_ev[2 + nblk];
+    // the copy streams start after work already queued on the handle's stream
+    if (cudaEventRecord(evStart, h->stream) != cudaSuccess) return OZ2_ERR_CUDA;
+    cudaStreamWaitEvent(h->s_h2d, evStart, 0);
+    cudaStreamWaitEvent(h->s_d2h, evStart, 0);
+    if (cudaMemcpy2DAsync(dB, sizeof(double) * n, B, sizeof(double) * ldb, sizeof(double) * n, k,
+                          cudaMemcpyHostToDevice, h->s_h2d) != cudaSuccess) return OZ2_ERR_CUDA;
+    cudaEventRecord(evB, h->s_h2d);
+    for (int64_t b = 0; b < nblk; b++) {
+        const int64_t r0 = b * mb, rows = std::min(mb, m - r0);
+        if (cudaMemcpy2DAsync(dA + r0 * k, sizeof(double) * k, A + r0 * lda, sizeof(double) * lda,
+                              sizeof(double) * k, rows, cudaMemcpyHostToDevice, h->s_h2d) != cudaSuccess)
+            return OZ2_ERR_CUDA;
+        cudaEventRecord(evA[b], h->s_h2d);
+    }
+    int8_t* Ares = (int8_t*)(ws + L.off_Ares);
+    int8_t* Bres = (int8_t*)(ws + L.off_Bres);
+    int32_t* e = (int32_t*)(ws + L.off_e);
+    int32_t* f = (int32_t*)(ws + L.off_f);
+    cudaStreamWaitEvent(h->stream, evB, 0);
+    mark(h);
+    mark(h);                                                  // rows of A are timed inside the GEMM stage here
+    oz2::launch_cols_exponents(dB, k, n, n, N, h->mode, kstar, f, ws + L.off_stats, h->stream);
+    mark(h);
+    oz2::launch_cols_residues(dB, k, n, n, f, N, Bres, L.ldr, h->stream);
+    mark(h);
+    CUtensorMap tB;
+    if ((rc = make_plane_map(&tB, Bres, n, k, L.ldr, N, 256 / oz2::gemm_cta_group()))) return rc;
+    for (int64_t b = 0; b < nblk; b++) {
+        const int64_t r0 = b * mb, rows = std::min(mb, m - r0);
+        cudaStreamWaitEvent(h->stream, evA[b], 0);
+        oz2::launch_rows(dA + r0 * k, rows, k, k, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
+        CUtensorMap tA;
+        if ((rc = make_plane_map(&tA, Ares, rows, k, L.ldr, N, 128))) return rc;
+        if (oz2::launch_modmul_fused(&tA, &tB, rows, n, k, N, ws + L.off_scratch, e, f, dC + r0 * n, n,
+                                     (uint32_t*)(ws + L.off_sync), h->num_sms, h->stream))
+            return OZ2_ERR_CUDA;
+        cudaEventRecord(evC[b], h->stream);
+        cudaStreamWaitEvent(h->s_d2h, evC[b], 0);
+        if (cudaMemcpy2DAsync(C + r0 * ldc, sizeof(double) * ldc, dC + r0 * n, sizeof(double) * n,
+                              sizeof(double) * n, rows, cudaMemcpyDeviceToHost, h->s_d2h) != cudaSuccess)
+            return OZ2_ERR_CUDA;
+    }
+    mark(h);
+    mark(h);
+    if ((rc = cuda_status())) return rc;
+    return cudaStreamSynchronize(h->s_d2h) == cudaSuccess && cudaStreamSynchronize(h->stream) == cudaSuccess
+               ? OZ2_OK : OZ2_ERR_CUDA;
 }
 
 }  // extern "C"

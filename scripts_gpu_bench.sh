@@ -1,0 +1,8 @@
+#!/bin/bash
+# tests + one full bench line (e2e included)
+mkdir -p gpurun_out
+python -c "from paper_2504_08009_b200 import build; build.build()" > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -x ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
+tail -5 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err

@@ -175,6 +175,20 @@ def test_host_entry_point(oz2, oracle):
     assert_bitwise(C, oracle.dgemm(A, B, 14), "oz2_dgemm_host")
 
 
+def test_host_entry_point_pipelined(oz2, oracle):
+    """m = 9000: two row blocks (4608 + 4392 rows) on the copy/compute pipeline."""
+    A = phi_matrix_np(9000, 700, 1.0, seed=21)
+    B = phi_matrix_np(700, 600, 1.0, seed=22)
+    Ah = torch.from_numpy(A).pin_memory().numpy()
+    Bh = torch.from_numpy(B).pin_memory().numpy()
+    Ch = torch.empty((9000, 600), dtype=torch.float64).pin_memory().numpy()
+    oz2.dgemm_host(Ah, Bh, 14, out=Ch)
+    Cd = oz2.dgemm(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), 14).cpu().numpy()
+    assert_bitwise(Ch, Cd, "pipelined host path vs device path")
+    rows = np.array([0, 4607, 4608, 8999])                    # both sides of the block boundary
+    assert_bitwise(Ch[rows], oracle.dgemm(A[rows], B, 14), "pipelined host path vs oracle")
+
+
 def test_strided_operands(oz2, oracle):
     A = phi_matrix_np(70, 300, 1.0, seed=11)
     B = phi_matrix_np(300, 90, 1.0, seed=12)
