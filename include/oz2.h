@@ -150,7 +150,7 @@ int oz2_eq17_k(int num_moduli, int64_t q);
  * milliseconds of each stage since the last read into ms[0..OZ2_NUM_STAGES-1]
  * (order: OZ2_STAGE_*), the number of calls into *calls, and resets. */
 #define OZ2_NUM_STAGES 5
-#define OZ2_STAGE_ROWS 0    /* rows of A: exponents + residues (lines 1, 2, 4)      */
+#define OZ2_STAGE_ROWS 0    /* rows of A (lines 1, 2, 4) [+ B if OZ2_CONV_OVERLAP=1]   */
 #define OZ2_STAGE_COLSTATS 1/* columns of B: exponents (line 1)                      */
 #define OZ2_STAGE_COLRES 2  /* columns of B: residues (lines 3, 5)                   */
 #define OZ2_STAGE_GEMM 3    /* N modular products on tcgen05 (line 6) [+ fused 7-10] */

@@ -87,6 +87,9 @@ struct oz2_context {
     // oz2_dgemm_host pipeline: copy streams and events (created on first use)
     cudaStream_t s_h2d, s_d2h;
     std::vector<cudaEvent_t> pipe_ev;
+    // B's conversion runs on s_aux concurrently with A's (fork / join events)
+    cudaStream_t s_aux;
+    cudaEvent_t ev_fork, ev_join;
 };
 
 namespace {
@@ -197,6 +200,18 @@ struct DevGuard {
 
 oz2_handle_t g_default[64] = {nullptr};
 
+int env_flag(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+int ensure_aux(oz2_handle_t h) {
+    if (!h->s_aux && cudaStreamCreateWithFlags(&h->s_aux, cudaStreamNonBlocking) != cudaSuccess) return OZ2_ERR_CUDA;
+    if (!h->ev_fork && cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess) return OZ2_ERR_CUDA;
+    if (!h->ev_join && cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) return OZ2_ERR_CUDA;
+    return OZ2_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -263,6 +278,9 @@ int oz2_destroy(oz2_handle_t h) {
     for (cudaEvent_t ev : h->pipe_ev) cudaEventDestroy(ev);
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
+    if (h->s_aux) cudaStreamDestroy(h->s_aux);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->ws_own) cudaFree(h->ws_own);
     delete h;
     return OZ2_OK;
@@ -457,13 +475,31 @@ int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* 
     if ((rc = make_plane_map(&tA, Ares, m, k, L.ldr, N, 128))) return rc;
     if ((rc = make_plane_map(&tB, Bres, n, k, L.ldr, N, 256 / oz2::gemm_cta_group()))) return rc;
     mark(h);
-    // Part 1 + 2-a (Alg. 1 lines 1-5)
-    oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
-    mark(h);
-    oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, h->stream);
-    mark(h);
-    oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, h->stream);
-    mark(h);
+    // Part 1 + 2-a (Alg. 1 lines 1-5).  A (rows) and B (columns) are independent
+    // passes; OZ2_CONV_OVERLAP=1 runs B's on a second stream concurrently with
+    // A's (stage ROWS then times both, the column stages read 0).  Default off:
+    // measured no gain, both passes are instruction-issue bound.
+    const bool overlap = env_flag("OZ2_CONV_OVERLAP", 0);
+    if (overlap) {
+        if ((rc = ensure_aux(h))) return rc;
+        cudaEventRecord(h->ev_fork, h->stream);
+        cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0);
+        oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, h->s_aux);
+        oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, h->s_aux);
+        cudaEventRecord(h->ev_join, h->s_aux);
+        oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
+        cudaStreamWaitEvent(h->stream, h->ev_join, 0);
+        mark(h);
+        mark(h);
+        mark(h);
+    } else {
+        oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
+        mark(h);
+        oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, h->stream);
+        mark(h);
+        oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, h->stream);
+        mark(h);
+    }
     // Part 2-b (line 6) with Parts 2-c, 3, 4 (lines 7-10) fused into the epilogue
     if (oz2::launch_modmul_fused(&tA, &tB, m, n, k, N, scratch, e, f, C, ldc, (uint32_t*)(ws + L.off_sync),
                                  h->num_sms, h->stream))

@@ -24,7 +24,7 @@ __device__ __forceinline__ uint32_t reduce_line7(int32_t c, int t) {
     const Oz2Table& T = c_tab[NM];
     const uint32_t y = (uint32_t)((c >> 16) * T.k16s[t]) + ((uint32_t)c & 0xffffu) + T.off7[t];
     const uint32_t q = __umulhi(y, T.magic[t]);
-    return y - q * (uint32_t)T.m[t];
+    return q * T.negm[t] + y;                                   // y - q m_t (mod 2^32)
 }
 
 // ---------------------------------------------------------------------------

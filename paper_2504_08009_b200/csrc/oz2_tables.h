@@ -20,6 +20,7 @@ struct Oz2Table {
     int32_t m[OZ2_MAX_MODULI];        // moduli, Eq. (18) + reading R1
     uint32_t magic[OZ2_MAX_MODULI];   // ceil(2^32 / m): floor(y/m) = umulhi(y, magic) for y < 2^24
     int32_t h[OZ2_MAX_MODULI];        // (m - 1) / 2 (odd m): symmetric offset
+    uint32_t negm[OZ2_MAX_MODULI];    // 2^32 - m: y - q m as one multiply-add
     uint32_t cw[3][OZ2_MAX_MODULI];   // byte b of cw[w][t] = 2^(8(4w+b)) mod m_t
     uint32_t k16[OZ2_MAX_MODULI];     // 2^16 mod m_t
     int32_t k16s[OZ2_MAX_MODULI];     // 2^16 mod m_t, symmetric representative (|k16s| <= m_t / 2)

@@ -17,10 +17,11 @@
 #include "oz2_device.cuh"
 #include "oz2_kernels.h"
 
+#include <stdlib.h>
+
 namespace oz2 {
 
 constexpr int KC = 256;            // FAST chunk length (reading R4)
-constexpr int ROW_THREADS = 512;   // fewer rows in flight: each row stays in L2 between its two passes
 constexpr int MAX_CHUNKS = 512;    // k < 2^17
 
 __device__ __forceinline__ uint64_t ceil_shift(uint64_t S, int sh) {
@@ -63,7 +64,7 @@ __device__ __forceinline__ uint32_t residue_odd(int t, const uint32_t (&w)[3]) {
     y = dp4a_uu(w[1], T.cw[1][t], y);
     if (WORDS == 3) y = dp4a_uu(w[2], T.cw[2][t], y);
     const uint32_t q = (uint32_t)(((uint64_t)y * T.magic[t] + T.hmagic[t]) >> 32);
-    return y - q * (uint32_t)T.m[t];
+    return q * T.negm[t] + y;                                   // y - q m_t (mod 2^32)
 }
 
 // U = trunc(2^e a) + 2^63 (WORDS = 2) or + 2^95 (WORDS = 3) as words; zeros
@@ -285,8 +286,8 @@ __device__ void row_residues(const double* __restrict__ X, int64_t k, int e, int
 // Row kernels (A: m x k, row-major, lda); one CTA per row
 // ---------------------------------------------------------------------------
 // what: 1 = exponents, 2 = residues (given e), 3 = both
-template <int NM, int WORDS, int MODE>
-__global__ void __launch_bounds__(ROW_THREADS)
+template <int NM, int WORDS, int MODE, int THREADS>
+__global__ void __launch_bounds__(THREADS)
 rows_kernel(const double* __restrict__ A, int64_t m, int64_t k, int64_t lda, int what, int kstar,
             int32_t* __restrict__ e_io, int8_t* __restrict__ res, int64_t ldr) {
     __shared__ RowSmem sm;
@@ -457,10 +458,16 @@ __global__ void trunc_cols_kernel(const double* __restrict__ B, int64_t k, int64
 template <int NM>
 static void launch_rows_nm(const double* A, int64_t m, int64_t k, int64_t lda, int what, int mode,
                            int kstar, int32_t* e, int8_t* res, int64_t ldr, cudaStream_t st) {
-    dim3 grid((unsigned)m), block(ROW_THREADS);
     constexpr int W = NM <= 16 ? 2 : 3;
-    if (mode == 0) rows_kernel<NM, W, 0><<<grid, block, 0, st>>>(A, m, k, lda, what, kstar, e, res, ldr);
-    else rows_kernel<NM, W, 1><<<grid, block, 0, st>>>(A, m, k, lda, what, kstar, e, res, ldr);
+    static const int threads = [] { const char* v = getenv("OZ2_ROW_THREADS"); return v && atoi(v) == 512 ? 512 : 256; }();
+    dim3 grid((unsigned)m), block((unsigned)threads);
+    if (threads == 512) {
+        if (mode == 0) rows_kernel<NM, W, 0, 512><<<grid, block, 0, st>>>(A, m, k, lda, what, kstar, e, res, ldr);
+        else rows_kernel<NM, W, 1, 512><<<grid, block, 0, st>>>(A, m, k, lda, what, kstar, e, res, ldr);
+    } else {
+        if (mode == 0) rows_kernel<NM, W, 0, 256><<<grid, block, 0, st>>>(A, m, k, lda, what, kstar, e, res, ldr);
+        else rows_kernel<NM, W, 1, 256><<<grid, block, 0, st>>>(A, m, k, lda, what, kstar, e, res, ldr);
+    }
 }
 
 template <int NM>

@@ -114,6 +114,7 @@ int oz2_build_tables(Oz2Table tabs[OZ2_MAX_MODULI + 1]) {
             T.m[t] = (int32_t)m;
             T.magic[t] = (uint32_t)(((1ull << 32) + (uint64_t)m - 1) / (uint64_t)m);
             T.h[t] = (int32_t)((m - 1) / 2);
+            T.negm[t] = (uint32_t)(0x100000000ull - (uint64_t)m);
             for (int w = 0; w < 3; w++) {
                 uint32_t packed = 0;
                 for (int b = 0; b < 4; b++) packed |= (uint32_t)pow2_mod(8 * (4 * w + b), m) << (8 * b);

@@ -30,6 +30,8 @@ SYMBOLS = [
     "oz2_modmul", "oz2_crt", "oz2_tables", "oz2_eq17_k", "oz2_strerror", "oz2_version",
     "oz2_set_profiling", "oz2_stage_times",
 ]
+# stage 0 times A's conversion (and B's too with OZ2_CONV_OVERLAP=1; the two column
+# stages then read 0); the host pipeline (oz2_dgemm_host) times rows of A inside "gemm"
 STAGES = ["rows_A", "colstats_B", "colres_B", "gemm", "crt"]
 
 
