@@ -24,7 +24,10 @@
  *    (256, 255, 253, 251, 247, 239, 233, 229, 227, 223, 217, 211, 199, 197,
  *    193, 191, 241, 181, 179, 173): Eq. (18) for N <= 16,
  *    then reading R1.
- *  - k must be < 2^17 so that every int32 product is exact.
+ *  - k must be < OZ2_MAX_K = 2^20.  The int32 products are exact for k < 2^17
+ *    (PAPER.md:457-458); for larger k the GEMM splits K into blocks of at most
+ *    1023 * 128 = 130944 ("block matrix multiplication") and adds
+ *    their residues mod m_t.  oz2_modmul (raw int32 products) keeps k < 2^17.
  *  - Rows of A / columns of B holding Inf or NaN give exponent
  *    OZ2_EXP_NONFINITE and NaN in the corresponding row / column of C
  *    (reading R13; the paper assumes finite data).
@@ -45,7 +48,8 @@ extern "C" {
 #define OZ2_OK 0
 #define OZ2_ERR_INVALID_ARG 1   /* negative size, ld too small, NULL, bad mode */
 #define OZ2_ERR_NUM_MODULI 2    /* N outside [2, 20] */
-#define OZ2_ERR_K_TOO_LARGE 3   /* k >= 2^17 */
+#define OZ2_ERR_K_TOO_LARGE 3   /* k >= OZ2_MAX_K (oz2_modmul: k >= 2^17) */
+#define OZ2_MAX_K (1 << 20)
 #define OZ2_ERR_BUDGET 4        /* EQ17 mode: Eq. (17) gives k_A < 1 */
 #define OZ2_ERR_CUDA 5          /* a CUDA runtime / driver call failed */
 #define OZ2_ERR_NO_DEVICE 6     /* no sm_100 device */

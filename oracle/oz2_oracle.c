@@ -43,6 +43,7 @@
 
 /* R4/R5: chunk length of the FAST (Cauchy-Schwarz) rule */
 #define OZ2O_KC 256
+#define OZ2O_MAX_N 20
 
 /* ------------------------------------------------------------------------- */
 /* 256-bit two's-complement integers                                           */
@@ -437,7 +438,7 @@ int oz2o_modmul(int64_t m, int64_t n, int64_t k, const int8_t* Ar, const int8_t*
  *   line 8:  S = sum_t c''_t w_t                         (exact)
  *   line 9:  X = S mod M                                 (Eq. 1, symmetric)
  *   line 10: c = 2^(-e-f) RN(X)                          (reading R10)        */
-static double crt_one(const consts_t* c, const int32_t* cp, int64_t stride,
+static double crt_one(const consts_t* c, const int64_t* cp, int64_t stride,
                       int32_t e, int32_t f, wide_t* Xo) {
     wide_t S = w_from_i64(0);
     for (int t = 0; t < c->N; t++) {
@@ -461,7 +462,9 @@ int oz2o_crt(int64_t m, int64_t n, int N, const int32_t* Cp, const int32_t* e,
     for (int64_t i = 0; i < m; i++)
         for (int64_t j = 0; j < n; j++) {
             wide_t X;
-            C[i * ldc + j] = crt_one(&c, Cp + i * n + j, m * n, e[i], f[j], &X);
+            int64_t cp[OZ2O_MAX_N];
+            for (int t = 0; t < N; t++) cp[t] = Cp[(int64_t)t * m * n + i * n + j];
+            C[i * ldc + j] = crt_one(&c, cp, 1, e[i], f[j], &X);
             if (X_limbs) for (int l = 0; l < WL; l++) X_limbs[(i * n + j) * WL + l] = X.l[l];
         }
     return OZ2O_OK;
@@ -477,7 +480,9 @@ int oz2o_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
                int32_t* e_out, int32_t* f_out) {
     consts_t c; int rc = make_consts(N, &c); if (rc) return rc;
     if (m < 0 || n < 0 || k < 0) return OZ2O_ERR_ARG;
-    if (k >= (1 << 17)) return OZ2O_ERR_K_TOO_LARGE;
+    /* q >= 2^17: "apply block matrix multiplication".  The sum of the
+     * block products is the same integer C'_t, so it is accumulated here in int64
+     * (|C'_t| <= k 2^14 < 2^63) and reduced once (reading R12).                  */
     int32_t* e = (int32_t*)malloc(sizeof(int32_t) * (m ? m : 1));
     int32_t* f = (int32_t*)malloc(sizeof(int32_t) * (n ? n : 1));
     if (mode == OZ2O_MODE_FAST) {
@@ -500,12 +505,12 @@ int oz2o_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
     int bad = 0;
     #pragma omp parallel for schedule(dynamic, 1) reduction(|:bad)
     for (int64_t i = 0; i < m; i++) {
-        int32_t* cp = (int32_t*)malloc(sizeof(int32_t) * N);
+        int64_t* cp = (int64_t*)malloc(sizeof(int64_t) * N);
         for (int64_t j = 0; j < n; j++) {
             for (int t = 0; t < N; t++) {
                 const int8_t* a = Ar + ((int64_t)t * m + i) * k;
                 const int8_t* b = Br + ((int64_t)t * n + j) * k;
-                int32_t acc = 0;                       /* exact: k < 2^17 */
+                int64_t acc = 0;                       /* exact */
                 for (int64_t l = 0; l < k; l++) acc += (int32_t)a[l] * (int32_t)b[l];
                 cp[t] = acc;
             }

@@ -135,7 +135,7 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms) {
 int check_common(int64_t m, int64_t n, int64_t k, int N) {
     if (m < 0 || n < 0 || k < 0) return OZ2_ERR_INVALID_ARG;
     if (N < 2 || N > OZ2_MAX_MODULI) return OZ2_ERR_NUM_MODULI;
-    if (k >= (int64_t)1 << 17) return OZ2_ERR_K_TOO_LARGE;
+    if (k >= OZ2_MAX_K) return OZ2_ERR_K_TOO_LARGE;
     if (m > INT32_MAX || n > INT32_MAX) return OZ2_ERR_INVALID_ARG;
     return OZ2_OK;
 }
@@ -223,7 +223,7 @@ const char* oz2_strerror(int code) {
         case OZ2_OK: return "ok";
         case OZ2_ERR_INVALID_ARG: return "invalid argument";
         case OZ2_ERR_NUM_MODULI: return "num_moduli must be in [2, 20]";
-        case OZ2_ERR_K_TOO_LARGE: return "k must be < 2^17 (int32 exactness, PAPER.md:457-459)";
+        case OZ2_ERR_K_TOO_LARGE: return "k too large: < 2^20, and < 2^17 for oz2_modmul's int32 products (PAPER.md:457-459)";
         case OZ2_ERR_BUDGET: return "EQ17 mode: Eq. (17) budget k_A < 1 for this (N, k)";
         case OZ2_ERR_CUDA: return "CUDA error";
         case OZ2_ERR_NO_DEVICE: return "no sm_100 CUDA device";
@@ -419,6 +419,7 @@ int oz2_modmul(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const int8_t* Ar
     int rc = check_common(m, n, k, N);
     if (rc) return rc;
     if (ld_res < k || ld_res % 16) return OZ2_ERR_INVALID_ARG;
+    if (k >= (int64_t)1 << 17) return OZ2_ERR_K_TOO_LARGE;     // int32 C'_t exact only below 2^17
     if (m == 0 || n == 0) return OZ2_OK;
     DevGuard g(h->device);
     if (k == 0) {

@@ -81,10 +81,12 @@ struct __align__(1024) Smem {
 struct Params {
     int m, n, k, N;
     int num_tm, num_tn, num_kb;     // tiles of TILE_M x TILE_N
+    int kb_chunk, nchunk;           // K blocking: <= 1023 k-blocks per exact int32 product
     int group_tm;                   // tile rows per raster group
     int epi_nop;                    // experiment only: epilogue drains TMEM and does nothing else
     unsigned long long* dbg;        // experiment only: per-CTA wait-cycle counters (or NULL)
     int pf_dist;                    // k-blocks of L2 prefetch ahead of the TMA loads
+    int exp_skip_b1;                // experiment only (wrong results): skip the second B half's load
     int32_t* cprod;                 // RAW: [N][m][n]
     uint8_t* scratch;               // FUSED: [grid][2 slots][N][BM*BN] uint8 residues
     double* C;                      // FUSED
@@ -117,6 +119,30 @@ __device__ __forceinline__ void for_each_unit(const Params& p, int cid, int ncl,
         tile_coords(p, j, tm, tn);
         for (int t = 0; t < p.N; t++) fn(tm, tn, t);
     }
+}
+
+// the same sequence split into K chunks (tm, tn, t, ch, [kb0, kb1)): each chunk
+// is one int32 accumulation in TMEM; the epilogue adds the chunks' residues mod m_t
+template <typename F>
+__device__ __forceinline__ void for_each_subunit(const Params& p, int cid, int ncl, F&& fn) {
+    for_each_unit(p, cid, ncl, [&](int tm, int tn, int t) {
+        for (int ch = 0; ch < p.nchunk; ch++) {
+            const int kb0 = ch * p.kb_chunk;
+            fn(tm, tn, t, ch, kb0, min(p.num_kb, kb0 + p.kb_chunk));
+        }
+    });
+}
+
+// (a + b) mod m per byte, a, b in [0, m)
+__device__ __forceinline__ uint32_t add_mod_bytes(uint32_t a, uint32_t b, uint32_t m) {
+    uint32_t r = 0;
+    #pragma unroll
+    for (int i = 0; i < 4; i++) {
+        uint32_t v = ((a >> (8 * i)) & 0xffu) + ((b >> (8 * i)) & 0xffu);
+        v = v >= m ? v - m : v;
+        r |= v << (8 * i);
+    }
+    return r;
 }
 
 // 32 reduced residues (bytes) of one modulus -> 8 words
@@ -250,12 +276,12 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                       mbar_wait(smem_u32(&s.empty[stage]), ph ^ 1);
                       if (p.dbg) dbg_empty += clock64() - t0; }
                     const uint32_t fb = smem_u32(&s.full[stage]);
-                    if (leader) mbar_expect_tx(fb, CG * (C_::A_BYTES + C_::B_BYTES));
+                    const int nh_load = (NH == 2 && p.exp_skip_b1) ? 1 : NH;
+                    if (leader) mbar_expect_tx(fb, CG * (C_::A_BYTES + nh_load * C_::B_HALF_BYTES));
                     if (CG == 2) {
                         const uint32_t fl = mapa_shared(fb, 0);          // the leader's full barrier
                         tma_load_3d_cg2(smem_u32(s.a[stage]), &tmA, fl, kb * BK, arow, t);
-                        #pragma unroll
-                        for (int h = 0; h < NH; h++)
+                        for (int h = 0; h < nh_load; h++)
                             tma_load_3d_cg2(smem_u32(s.b[stage] + h * C_::B_HALF_BYTES), &tmB, fl, kb * BK,
                                             brow + h * BN, t);
                     } else {
@@ -282,7 +308,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const uint32_t idesc = idesc_i8(C_::TILE_M, BN);
             int stage = 0; uint32_t ph = 0;
             int acc = 0; uint32_t aph = 0;     // NH = 1: buffer and its phase; NH = 2: phase of the halves
-            for_each_unit(p, cid, ncl, [&](int, int, int) {
+            for_each_subunit(p, cid, ncl, [&](int, int, int, int, int kb0, int kb1) {
                 if (NH == 1) {
                     const long long t0 = p.dbg ? clock64() : 0;
                     mbar_wait(smem_u32(&s.tempty[acc]), aph ^ 1);
@@ -290,7 +316,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     tc_fence_after();
                 }
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
-                for (int kb = 0; kb < p.num_kb; kb++) {
+                for (int kb = kb0; kb < kb1; kb++) {
                     { const long long t0 = p.dbg ? clock64() : 0;
                       mbar_wait(smem_u32(&s.full[stage]), ph);
                       if (p.dbg) dbg_full += clock64() - t0; }
@@ -298,7 +324,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     const uint32_t a0 = smem_u32(s.a[stage]);
                     #pragma unroll
                     for (int h = 0; h < NH; h++) {
-                        if (NH == 2 && kb == 0) {
+                        if (NH == 2 && kb == kb0) {
                             // the first MMA into half h of this unit waits for that half's drain
                             const long long t0 = p.dbg ? clock64() : 0;
                             mbar_wait(smem_u32(&s.tempty[h]), aph ^ 1);
@@ -309,8 +335,9 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         const uint32_t dh = d + (uint32_t)(h * BN);
                         #pragma unroll
                         for (int kk = 0; kk < BK / UK; kk++) {
-                            if (CG == 2) mma_i8_cg2(dh, sw128_desc(a0 + kk * UK), sw128_desc(b0 + kk * UK), idesc, (kb | kk) != 0);
-                            else mma_i8(dh, sw128_desc(a0 + kk * UK), sw128_desc(b0 + kk * UK), idesc, (kb | kk) != 0);
+                            const uint32_t accum = (kb != kb0 || kk != 0) ? 1u : 0u;
+                            if (CG == 2) mma_i8_cg2(dh, sw128_desc(a0 + kk * UK), sw128_desc(b0 + kk * UK), idesc, accum);
+                            else mma_i8(dh, sw128_desc(a0 + kk * UK), sw128_desc(b0 + kk * UK), idesc, accum);
                         }
                     }
                     // the stage is reusable (in both CTAs) when these MMAs finish
@@ -347,6 +374,22 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 else mbar_arrive(bar);
             }
         };
+        // residues of K chunk ch: stored (ch = 0) or added mod m_t to the earlier chunks'
+        auto store_residues = [&](uint4* d4, const uint32_t (&w)[8], int ch, int t) {
+            if (ch == 0) {
+                d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            } else {
+                if constexpr (FUSED) {
+                    const uint32_t mt = (uint32_t)c_tab[NM].m[t];
+                    const uint4 o0 = d4[0], o1 = d4[1];
+                    d4[0] = make_uint4(add_mod_bytes(o0.x, w[0], mt), add_mod_bytes(o0.y, w[1], mt),
+                                       add_mod_bytes(o0.z, w[2], mt), add_mod_bytes(o0.w, w[3], mt));
+                    d4[1] = make_uint4(add_mod_bytes(o1.x, w[4], mt), add_mod_bytes(o1.y, w[5], mt),
+                                       add_mod_bytes(o1.z, w[6], mt), add_mod_bytes(o1.w, w[7], mt));
+                }
+            }
+        };
         auto run_slice = [&](int sl) {
           if constexpr (FUSED) {
             const int c = half * CH + (sl >> 2), hh = sl & 3;
@@ -358,7 +401,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             }
           }
         };
-        for_each_unit(p, cid, ncl, [&](int tm, int tn, int t) {
+        for_each_subunit(p, cid, ncl, [&](int tm, int tn, int t, int ch, int, int) {
             mbar_wait(smem_u32(&s.tfull[acc]), aph);
             tc_fence_after();
             const int row = tm * C_::TILE_M + (int)rank * BM + r;
@@ -407,25 +450,23 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     tmem_ld_wait_regs(va);
                     tmem_ld_32x32b_x32(tbase + (uint32_t)((c + 1) * 32), vb);
                     reduce32<NM>(va, t, w);
-                    uint4* d4 = reinterpret_cast<uint4*>(tile_scr + ((size_t)(c * BM + r)) * 32);
-                    d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
-                    d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+                    store_residues(reinterpret_cast<uint4*>(tile_scr + ((size_t)(c * BM + r)) * 32), w, ch, t);
                     tmem_ld_wait_regs(vb);
                     if (cc + 2 < CH) tmem_ld_32x32b_x32(tbase + (uint32_t)((c + 2) * 32), va);
                     reduce32<NM>(vb, t, w);
-                    d4 = reinterpret_cast<uint4*>(tile_scr + ((size_t)((c + 1) * BM + r)) * 32);
-                    d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
-                    d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+                    store_residues(reinterpret_cast<uint4*>(tile_scr + ((size_t)((c + 1) * BM + r)) * 32), w, ch, t);
                 }
                 release();
-                // lines 8-10 of the previous tile, SLICES slices of 8 columns spread
-                // over this tile's N units (no burst that would hold TMEM back)
-                if (pend) {
-                    const int s0 = (t * SLICES) / NM, s1 = ((t + 1) * SLICES) / NM;
-                    for (int sl = s0; sl < s1; sl++) run_slice(sl);
-                }
-                if (t == NM - 1) {
-                    pend = true; ptm = tm; ptn = tn; pslot = slot; slot ^= 1;
+                if (ch == p.nchunk - 1) {                         // the last K chunk of (tile, t)
+                    // lines 8-10 of the previous tile, SLICES slices of 8 columns spread
+                    // over this tile's N units (no burst that would hold TMEM back)
+                    if (pend) {
+                        const int s0 = (t * SLICES) / NM, s1 = ((t + 1) * SLICES) / NM;
+                        for (int sl = s0; sl < s1; sl++) run_slice(sl);
+                    }
+                    if (t == NM - 1) {
+                        pend = true; ptm = tm; ptn = tn; pslot = slot; slot ^= 1;
+                    }
                 }
             }
             if (NH == 1) { if (++acc == 2) { acc = 0; aph ^= 1; } }
@@ -508,9 +549,13 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
     p.num_tm = (int)((m + tile_m - 1) / tile_m);
     p.num_tn = (int)((n + tile_n - 1) / tile_n);
     p.num_kb = (int)((k + BK - 1) / BK);
+    // K blocking: |C'_t| <= kb_chunk * 128 * 2^14 < 2^31 for kb_chunk <= 1023 (OZ2_KB_CHUNK: tests)
+    p.kb_chunk = std::min(1023, std::max(1, env_int("OZ2_KB_CHUNK", 1023)));
+    p.nchunk = std::max(1, (p.num_kb + p.kb_chunk - 1) / p.kb_chunk);
     p.group_tm = std::max(1, env_int("OZ2_GROUP_TM", GROUP_TM));
     p.epi_nop = env_int("OZ2_EPI_NOP", 0);
     p.pf_dist = env_int("OZ2_PF_DIST", 0);       // measured: L2 prefetch slows the GEMM (TMA contention)
+    p.exp_skip_b1 = env_int("OZ2_EXP_SKIP_B1", 0);
     const int tiles = p.num_tm * p.num_tn;
     const int nclusters = num_sms / cg;
     const int ncl = tiles < nclusters ? tiles : nclusters;
@@ -537,6 +582,8 @@ int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int
     int grid;
     gemm::Params p = make_params(m, n, k, N, num_sms, gemm_cta_group(), gemm_halves(), &grid);
     p.cprod = cprod;
+    p.kb_chunk = std::max(1, p.num_kb);               // RAW int32 products: one accumulation (k < 2^17)
+    p.nchunk = 1;
     p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
     if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
     return gemm::launch_shape<0>(gemm_shape(), tmA, tmB, p, grid, st);

@@ -22,7 +22,7 @@
 namespace oz2 {
 
 constexpr int KC = 256;            // FAST chunk length (reading R4)
-constexpr int MAX_CHUNKS = 512;    // k < 2^17
+constexpr int MAX_CHUNKS = 4096;   // k < 2^20 (OZ2 max k; chunk statistics live in shared memory)
 
 __device__ __forceinline__ uint64_t ceil_shift(uint64_t S, int sh) {
     if (S == 0) return 0;
@@ -156,12 +156,16 @@ __device__ __forceinline__ double u_sq(double x, double s1, double s2) {
     return x != 0.0 ? u * u : 0.0;
 }
 
+// per-row chunk statistics in dynamic shared memory: Sc[nch], Ec[nch], then bad, e
 struct RowSmem {
-    int Ec[MAX_CHUNKS];
-    unsigned long long Sc[MAX_CHUNKS];
-    int bad;
-    int e;
+    unsigned long long* Sc;
+    int* Ec;
+    int* misc;                        // [0] = bad, [1] = e
 };
+__host__ __device__ inline size_t row_smem_bytes(int64_t k) {
+    const int64_t nch = (k + KC - 1) / KC;
+    return (size_t)(nch > 0 ? nch : 1) * (sizeof(unsigned long long) + sizeof(int)) + 2 * sizeof(int);
+}
 
 // combine chunk statistics (warp 0): e = T + 15 - E - h, or EQ17 / zero / non-finite
 template <int MODE>
@@ -195,7 +199,7 @@ __device__ int row_exponent(const double* __restrict__ X, int64_t k, int Tb, int
     const int nch = (int)((k + KC - 1) / KC);
     const bool vec = ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
     const uint64_t pol = l2_evict_last();
-    if (threadIdx.x == 0) sm.bad = 0;
+    if (threadIdx.x == 0) sm.misc[0] = 0;
     __syncthreads();
     for (int c = warp; c < nch; c += nwarps) {
         double v[KC / 32];
@@ -223,7 +227,7 @@ __device__ int row_exponent(const double* __restrict__ X, int64_t k, int Tb, int
         int Ec = INT32_MIN;
         double S = 0.0;
         if (mb >= INF_BITS) {
-            if (lane == 0) sm.bad = 1;
+            if (lane == 0) sm.misc[0] = 1;
         } else if (mb != 0) {
             Ec = ilogb_bits(mb);
             if (MODE == 0) {
@@ -238,11 +242,11 @@ __device__ int row_exponent(const double* __restrict__ X, int64_t k, int Tb, int
     }
     __syncthreads();
     if (warp == 0) {
-        const int e = combine_chunks<MODE>(sm.Ec, sm.Sc, nch, sm.bad, Tb, kstar);
-        if (lane == 0) sm.e = e;
+        const int e = combine_chunks<MODE>(sm.Ec, sm.Sc, nch, sm.misc[0], Tb, kstar);
+        if (lane == 0) sm.misc[1] = e;
     }
     __syncthreads();
-    return sm.e;
+    return sm.misc[1];
 }
 
 // residues of one row for all N moduli: planes out[t][l], 8 elements per thread
@@ -290,7 +294,12 @@ template <int NM, int WORDS, int MODE, int THREADS>
 __global__ void __launch_bounds__(THREADS)
 rows_kernel(const double* __restrict__ A, int64_t m, int64_t k, int64_t lda, int what, int kstar,
             int32_t* __restrict__ e_io, int8_t* __restrict__ res, int64_t ldr) {
-    __shared__ RowSmem sm;
+    extern __shared__ __align__(16) unsigned char row_smem[];
+    const int64_t nch = (k + KC - 1) / KC;
+    RowSmem sm;
+    sm.Sc = reinterpret_cast<unsigned long long*>(row_smem);
+    sm.Ec = reinterpret_cast<int*>(row_smem + sizeof(unsigned long long) * (nch > 0 ? nch : 1));
+    sm.misc = sm.Ec + (nch > 0 ? nch : 1);
     const int64_t i = blockIdx.x;
     if (i >= m) return;
     const double* X = A + i * lda;
@@ -461,13 +470,11 @@ static void launch_rows_nm(const double* A, int64_t m, int64_t k, int64_t lda, i
     constexpr int W = NM <= 16 ? 2 : 3;
     static const int threads = [] { const char* v = getenv("OZ2_ROW_THREADS"); return v && atoi(v) == 512 ? 512 : 256; }();
     dim3 grid((unsigned)m), block((unsigned)threads);
-    if (threads == 512) {
-        if (mode == 0) rows_kernel<NM, W, 0, 512><<<grid, block, 0, st>>>(A, m, k, lda, what, kstar, e, res, ldr);
-        else rows_kernel<NM, W, 1, 512><<<grid, block, 0, st>>>(A, m, k, lda, what, kstar, e, res, ldr);
-    } else {
-        if (mode == 0) rows_kernel<NM, W, 0, 256><<<grid, block, 0, st>>>(A, m, k, lda, what, kstar, e, res, ldr);
-        else rows_kernel<NM, W, 1, 256><<<grid, block, 0, st>>>(A, m, k, lda, what, kstar, e, res, ldr);
-    }
+    const size_t smem = row_smem_bytes(k);
+    auto kern = threads == 512 ? (mode == 0 ? rows_kernel<NM, W, 0, 512> : rows_kernel<NM, W, 1, 512>)
+                               : (mode == 0 ? rows_kernel<NM, W, 0, 256> : rows_kernel<NM, W, 1, 256>);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, block, smem, st>>>(A, m, k, lda, what, kstar, e, res, ldr);
 }
 
 template <int NM>

@@ -20,7 +20,7 @@ OK = 0
 MODE_FAST = 0
 MODE_EQ17 = 1
 EXP_NONFINITE = -(2**31)
-MAX_K = 2**17
+MAX_K = 2**20          # oz2_modmul (raw int32 products): 2**17
 
 # every symbol include/oz2.h declares (checked by tests/test_abi.py)
 SYMBOLS = [

@@ -157,7 +157,7 @@ def test_errors_fail_loudly(oz2):
         oz2.dgemm(A, A, 21)
     with pytest.raises(oz2.Oz2Error):
         oz2.dgemm(A, A, 1)
-    big = torch.ones((1, 2**17), dtype=torch.float64, device=DEV)
+    big = torch.ones((1, 2**20), dtype=torch.float64, device=DEV)
     with pytest.raises(oz2.Oz2Error):
         oz2.dgemm(big, big.T.contiguous(), 14)
     with pytest.raises(oz2.Oz2Error):        # EQ17 budget < 1 (N = 2, k = 20000)
@@ -187,6 +187,26 @@ def test_host_entry_point_pipelined(oz2, oracle):
     assert_bitwise(Ch, Cd, "pipelined host path vs device path")
     rows = np.array([0, 4607, 4608, 8999])                    # both sides of the block boundary
     assert_bitwise(Ch[rows], oracle.dgemm(A[rows], B, 14), "pipelined host path vs oracle")
+
+
+def test_k_blocking_forced(oz2, oracle, monkeypatch):
+    """K blocking exercised at small k: OZ2_KB_CHUNK=2 splits the
+    8 k-blocks of k = 1000 into 4 int32 accumulations whose residues are added."""
+    monkeypatch.setenv("OZ2_KB_CHUNK", "2")
+    A = phi_matrix_np(300, 1000, 1.0, seed=41)
+    B = phi_matrix_np(1000, 530, 1.0, seed=42)
+    for N in (3, 14, 20):
+        C = oz2.dgemm(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), N).cpu().numpy()
+        assert_bitwise(C, oracle.dgemm(A, B, N), f"k-blocked N={N}")
+
+
+def test_k_beyond_int32_range(oz2, oracle):
+    """k = 2^17 + 3000 > 2^17: two K blocks of <= 1023 k-blocks (ragged tail)."""
+    k = 2**17 + 3000
+    A = phi_matrix_np(96, k, 0.5, seed=43)
+    B = phi_matrix_np(k, 200, 0.5, seed=44)
+    C = oz2.dgemm(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), 14).cpu().numpy()
+    assert_bitwise(C, oracle.dgemm(A, B, 14), "k = 2^17 + 3000")
 
 
 def test_strided_operands(oz2, oracle):

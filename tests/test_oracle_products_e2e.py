@@ -76,6 +76,31 @@ def test_reconstruction_equals_integer_product(oracle, N, mode, phi):
     assert np.array_equal(C, C2)
 
 
+@pytest.mark.parametrize("N,phi", [(14, 1.0), (16, 0.5)])
+def test_large_k_block_product(oracle, N, phi):
+    """q >= 2^17 (reading R12): the block-accumulated products still
+    reconstruct X = A'B' exactly -- checked against Python integers computed from
+    A', B' alone (no modular arithmetic)."""
+    m, n, k = 3, 2, 2**17 + 37
+    A = phi_matrix_np(m, k, phi, seed=31)
+    B = phi_matrix_np(k, n, phi, seed=32)
+    C, e, f = oracle.dgemm(A, B, N, return_exponents=True)
+    Ap = oracle.trunc_rows(A, e)
+    BpT = oracle.trunc_cols(B, f)
+    M = math.prod(oracle.constants(N)["moduli"])
+    for i in range(m):
+        a = [int(v) for v in Ap[i]]
+        for j in range(n):
+            b = [int(v) for v in BpT[j]]
+            x = sum(p * q for p, q in zip(a, b))
+            assert 2 * sum(abs(p * q) for p, q in zip(a, b)) < M       # condition (13)
+            assert C[i, j] == math.ldexp(float(x), -int(e[i] + f[j]))
+    # integer inputs within budget give AB exactly at this k too
+    Ai = integer_matrix_np(2, k, 3, seed=33)
+    Bi = integer_matrix_np(k, 2, 3, seed=34)
+    assert np.array_equal(oracle.dgemm(Ai, Bi, N), (Ai.astype(np.int64) @ Bi.astype(np.int64)).astype(np.float64))
+
+
 @pytest.mark.parametrize("N", [8, 14, 20])
 def test_integer_inputs_exact(oracle, N):
     # SPEC.md:393,397: integer matrices within budget give AB exactly
