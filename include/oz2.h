@@ -77,7 +77,7 @@ int oz2_set_mode(oz2_handle_t h, int mode);
  * library-managed, grown on demand with cudaMalloc).  Must stay valid and
  * unused by others while calls on this handle are in flight. */
 int oz2_set_workspace(oz2_handle_t h, void* ptr, size_t bytes);
-/* Workspace bytes oz2_dgemm_ex needs for (m, n, k, N). */
+/* Workspace bytes oz2_dgemm_ex / oz2_dgemm_op / one batch item need for (m, n, k, N). */
 size_t oz2_workspace_bytes(int64_t m, int64_t n, int64_t k, int num_moduli);
 
 /* ---- main entry points ---------------------------------------------------- */
@@ -90,6 +90,28 @@ int oz2_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
 int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A,
                  int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                  int num_moduli);
+/* The DGEMM surface ("GEMM ... depending on the
+ * structure"; semantics of BLAS DGEMM, reading R19), row-major:
+ *   C := alpha op(A) op(B) + beta C,  op(A) m x k, op(B) k x n, C m x n,
+ *   transA = OZ2_OP_N: A stored m x k (lda >= k); OZ2_OP_T: A stored k x m (lda >= m);
+ *   transB = OZ2_OP_N: B stored k x n (ldb >= n); OZ2_OP_T: B stored n x k (ldb >= k).
+ * The product is Algorithm 1's C (exponents of the rows of op(A) and columns of
+ * op(B)); then each entry is RN(alpha c + RN(beta c_old)) (one fma; exactly c
+ * for alpha = 1, beta = 0).  beta == 0: C is not read.  alpha == 0 or k == 0:
+ * no product, C := beta C.  (Column-major BLAS calls map by swapping A and B.) */
+#define OZ2_OP_N 0
+#define OZ2_OP_T 1
+int oz2_dgemm_op(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, int64_t k,
+                 double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                 double beta, double* C, int64_t ldc, int num_moduli);
+/* batch independent products: A + b*strideA, B + b*strideB, C + b*strideC
+ * (elements), b = 0..batch-1, in stream order on one workspace. */
+int oz2_dgemm_strided_batched(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n,
+                              int64_t k, double alpha, const double* A, int64_t lda,
+                              int64_t strideA, const double* B, int64_t ldb, int64_t strideB,
+                              double beta, double* C, int64_t ldc, int64_t strideC,
+                              int64_t batch, int num_moduli);
+
 /* End-to-end variant with HOST buffers: copies A and B to the device, runs
  * Algorithm 1 and copies C back, then synchronises.  Pipelined over up to 8
  * row blocks of A / C (rows multiple of 256, >= 4096 rows each): B is copied

@@ -78,6 +78,8 @@ def lib():
         L.oz2o_wide_from_double.argtypes = [ctypes.c_double, P]
         L.oz2o_wide_from_double.restype = None
         L.oz2o_set_threads.argtypes = [i32]
+        L.oz2o_axpby.argtypes = [i64, ctypes.c_double, P, ctypes.c_double, P, P]
+        L.oz2o_axpby.restype = None
         L.oz2o_set_threads.restype = None
         L.oz2o_get_threads.restype = i32
         _lib = L
@@ -238,6 +240,22 @@ def dgemm(A, B, N: int, mode: int = MODE_FAST, return_exponents: bool = False):
     f = np.zeros(max(n, 1), np.int32)
     _check(lib().oz2o_dgemm(m, n, k, _p(A), k, _p(B), n, _p(C), n, N, mode, _p(e), _p(f)))
     return (C, e[:m], f[:n]) if return_exponents else C
+
+
+def gemm(A, B, N: int, alpha: float = 1.0, beta: float = 0.0, C=None, transA: bool = False,
+         transB: bool = False, mode: int = MODE_FAST) -> np.ndarray:
+    """alpha op(A) op(B) + beta C around dgemm (reading R19): the transposes are
+    plain numpy views, the update is oz2o_axpby."""
+    Aop = np.ascontiguousarray(np.asarray(A, np.float64).T if transA else A, dtype=np.float64)
+    Bop = np.ascontiguousarray(np.asarray(B, np.float64).T if transB else B, dtype=np.float64)
+    m, n = Aop.shape[0], Bop.shape[1]
+    Cold = np.zeros((m, n)) if C is None else np.ascontiguousarray(C, dtype=np.float64)
+    if alpha == 0.0 or Aop.shape[1] == 0:
+        return np.zeros((m, n)) if beta == 0.0 else beta * Cold
+    ab = dgemm(Aop, Bop, N, mode)
+    out = np.empty((m, n))
+    lib().oz2o_axpby(m * n, float(alpha), _p(ab), float(beta), _p(Cold), _p(out))
+    return out
 
 
 def int_product(Ap, BpT) -> list:

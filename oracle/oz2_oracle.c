@@ -621,6 +621,15 @@ void oz2o_exact_entries(int64_t k, const double* A, int64_t lda, const double* B
     }
 }
 
+/* The DGEMM surface around Algorithm 1 (reading R19, BLAS DGEMM semantics):
+ * out = RN(alpha c + RN(beta c_old)) with one fused multiply-add; beta == 0
+ * means c_old is not read (alpha c, one rounding).                             */
+void oz2o_axpby(int64_t n, double alpha, const double* c, double beta, const double* c_old,
+                double* out) {
+    for (int64_t i = 0; i < n; i++)
+        out[i] = beta == 0.0 ? alpha * c[i] : fma(alpha, c[i], beta * c_old[i]);
+}
+
 /* wide integer -> RN double, exposed so the conversion can be pinned against
  * an independent correctly-rounded conversion (Python's int -> float).         */
 double oz2o_wide_to_double(const uint64_t* limbs4) {

@@ -116,7 +116,7 @@ struct Layout {
     size_t off_Ares, off_Bres, off_e, off_f, off_stats, off_scratch, off_sync, total;
 };
 
-Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms) {
+Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms, int64_t stats_cols = -1) {
     Layout L;
     L.ldr = round_up(k > 0 ? k : 1, 16);
     size_t off = 0;
@@ -125,7 +125,7 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms) {
     L.off_Bres = take((size_t)N * (size_t)n * (size_t)L.ldr);
     L.off_e = take(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));
     L.off_f = take(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
-    L.off_stats = take(oz2::cols_stats_bytes(k, n));
+    L.off_stats = take(oz2::cols_stats_bytes(k, stats_cols >= 0 ? stats_cols : n));
     L.off_scratch = take(oz2::fused_scratch_bytes(m, n, N, num_sms));
     L.off_sync = take(256);
     L.total = off;
@@ -343,7 +343,7 @@ size_t oz2_workspace_bytes(int64_t m, int64_t n, int64_t k, int N) {
         cudaGetLastError();
         sms = 160;                                   // conservative (> 148) without a device
     }
-    return layout_for(m, n, k, N, sms).total;
+    return layout_for(m, n, k, N, sms, std::max(m, n)).total;
 }
 
 // ---------------------------------------------------------------------------
@@ -449,22 +449,39 @@ int oz2_crt(oz2_handle_t h, int64_t m, int64_t n, const int32_t* Cprod, const in
 // ---------------------------------------------------------------------------
 // main entry points
 // ---------------------------------------------------------------------------
-int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
-                 const double* B, int64_t ldb, double* C, int64_t ldc, int N) {
-    if (!h) return OZ2_ERR_INVALID_ARG;
+}  // extern "C"
+
+namespace {
+
+// Argument checks of the DGEMM surface (row-major): op(A) m x k, op(B) k x n.
+int check_op_args(int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                  int64_t ldb, const double* C, int64_t ldc, int N) {
     int rc = check_common(m, n, k, N);
     if (rc) return rc;
-    if (lda < (k > 0 ? k : 1) || ldb < (n > 0 ? n : 1) || ldc < (n > 0 ? n : 1)) return OZ2_ERR_INVALID_ARG;
+    if ((ta != OZ2_OP_N && ta != OZ2_OP_T) || (tb != OZ2_OP_N && tb != OZ2_OP_T)) return OZ2_ERR_INVALID_ARG;
+    const int64_t need_a = ta == OZ2_OP_N ? k : m, need_b = tb == OZ2_OP_N ? n : k;
+    if (lda < (need_a > 0 ? need_a : 1) || ldb < (need_b > 0 ? need_b : 1) || ldc < (n > 0 ? n : 1))
+        return OZ2_ERR_INVALID_ARG;
+    if (m > 0 && n > 0 && (!C || (k > 0 && (!A || !B)))) return OZ2_ERR_INVALID_ARG;
+    return OZ2_OK;
+}
+
+// C = alpha op(A) op(B) + beta C by Algorithm 1 (arguments already checked).
+// op(A) = A^T means the stored A is k x m: its "rows of op(A)" are the columns
+// of the stored matrix, so the column kernels produce e and the K-major planes;
+// likewise op(B) = B^T (stored n x k) goes through the row kernel.
+int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+               int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int N) {
     if (m == 0 || n == 0) return OZ2_OK;
-    if (!C || (k > 0 && (!A || !B))) return OZ2_ERR_INVALID_ARG;
-    int kstar = 0;
-    if (k > 0 && (rc = kstar_for(h, N, k, &kstar))) return rc;
+    int rc, kstar = 0;
+    if (k > 0 && alpha != 0.0 && (rc = kstar_for(h, N, k, &kstar))) return rc;
     DevGuard g(h->device);
-    if (k == 0) {
-        cudaError_t e = cudaMemset2DAsync(C, sizeof(double) * ldc, 0, sizeof(double) * n, m, h->stream);
-        return e == cudaSuccess ? OZ2_OK : OZ2_ERR_CUDA;
+    if (k == 0 || alpha == 0.0) {                     // no product: C = beta C (0 if beta == 0)
+        if (beta == 1.0) return OZ2_OK;
+        oz2::launch_scale_c(C, m, n, ldc, beta, h->stream);
+        return cuda_status();
     }
-    Layout L = layout_for(m, n, k, N, h->num_sms);
+    Layout L = layout_for(m, n, k, N, h->num_sms, ta == OZ2_OP_T ? std::max(m, n) : n);
     uint8_t* ws;
     if ((rc = get_workspace(h, L.total, &ws))) return rc;
     int8_t* Ares = (int8_t*)(ws + L.off_Ares);
@@ -475,39 +492,91 @@ int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* 
     CUtensorMap tA, tB;
     if ((rc = make_plane_map(&tA, Ares, m, k, L.ldr, N, 128))) return rc;
     if ((rc = make_plane_map(&tB, Bres, n, k, L.ldr, N, 256 / oz2::gemm_cta_group()))) return rc;
+    // Part 1 + 2-a (Alg. 1 lines 1-5) for op(A) and op(B)
+    auto convert_A = [&](cudaStream_t st) {
+        if (ta == OZ2_OP_N) {
+            oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, st);
+        } else {
+            oz2::launch_cols_exponents(A, k, m, lda, N, h->mode, kstar, e, ws + L.off_stats, st);
+            oz2::launch_cols_residues(A, k, m, lda, e, N, Ares, L.ldr, st);
+        }
+    };
+    auto convert_B_stats = [&](cudaStream_t st) {
+        if (tb == OZ2_OP_N) oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, st);
+    };
+    auto convert_B_res = [&](cudaStream_t st) {
+        if (tb == OZ2_OP_N) oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, st);
+        else oz2::launch_rows(B, n, k, ldb, N, 3, h->mode, kstar, f, Bres, L.ldr, st);
+    };
     mark(h);
-    // Part 1 + 2-a (Alg. 1 lines 1-5).  A (rows) and B (columns) are independent
-    // passes; OZ2_CONV_OVERLAP=1 runs B's on a second stream concurrently with
-    // A's (stage ROWS then times both, the column stages read 0).  Default off:
-    // measured no gain, both passes are instruction-issue bound.
-    const bool overlap = env_flag("OZ2_CONV_OVERLAP", 0);
+    // A and B are independent passes; OZ2_CONV_OVERLAP=1 runs B's on a second
+    // stream concurrently with A's (stage ROWS then times both, the column stages
+    // read 0).  Default off: measured no gain, both passes are issue-bound.  (Not
+    // with op(A) = A^T, whose column statistics share B's scratch.)
+    const bool overlap = env_flag("OZ2_CONV_OVERLAP", 0) && ta == OZ2_OP_N;
     if (overlap) {
         if ((rc = ensure_aux(h))) return rc;
         cudaEventRecord(h->ev_fork, h->stream);
         cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0);
-        oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, h->s_aux);
-        oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, h->s_aux);
+        convert_B_stats(h->s_aux);
+        convert_B_res(h->s_aux);
         cudaEventRecord(h->ev_join, h->s_aux);
-        oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
+        convert_A(h->stream);
         cudaStreamWaitEvent(h->stream, h->ev_join, 0);
         mark(h);
         mark(h);
         mark(h);
     } else {
-        oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
+        convert_A(h->stream);
         mark(h);
-        oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, h->stream);
+        convert_B_stats(h->stream);
         mark(h);
-        oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, h->stream);
+        convert_B_res(h->stream);
         mark(h);
     }
     // Part 2-b (line 6) with Parts 2-c, 3, 4 (lines 7-10) fused into the epilogue
     if (oz2::launch_modmul_fused(&tA, &tB, m, n, k, N, scratch, e, f, C, ldc, (uint32_t*)(ws + L.off_sync),
-                                 h->num_sms, h->stream))
+                                 h->num_sms, h->stream, alpha, beta))
         return OZ2_ERR_CUDA;
     mark(h);
     mark(h);                                          // (no separate CRT stage)
     return cuda_status();
+}
+
+}  // namespace
+
+extern "C" {
+
+int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                 const double* B, int64_t ldb, double* C, int64_t ldc, int N) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_op_args(OZ2_OP_N, OZ2_OP_N, m, n, k, A, lda, B, ldb, C, ldc, N);
+    if (rc) return rc;
+    return dgemm_core(h, OZ2_OP_N, OZ2_OP_N, m, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldc, N);
+}
+
+int oz2_dgemm_op(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, int64_t k, double alpha,
+                 const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+                 int64_t ldc, int N) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_op_args(transA, transB, m, n, k, A, lda, B, ldb, C, ldc, N);
+    if (rc) return rc;
+    return dgemm_core(h, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, N);
+}
+
+int oz2_dgemm_strided_batched(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, int64_t k,
+                              double alpha, const double* A, int64_t lda, int64_t strideA, const double* B,
+                              int64_t ldb, int64_t strideB, double beta, double* C, int64_t ldc,
+                              int64_t strideC, int64_t batch, int N) {
+    if (!h || batch < 0 || strideA < 0 || strideB < 0 || strideC < 0) return OZ2_ERR_INVALID_ARG;
+    int rc = check_op_args(transA, transB, m, n, k, A, lda, B, ldb, C, ldc, N);
+    if (rc) return rc;
+    for (int64_t b = 0; b < batch; b++) {            // one workspace, reused in stream order
+        rc = dgemm_core(h, transA, transB, m, n, k, alpha, A ? A + b * strideA : A, lda,
+                        B ? B + b * strideB : B, ldb, beta, C + b * strideC, ldc, N);
+        if (rc) return rc;
+    }
+    return OZ2_OK;
 }
 
 int oz2_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B, int64_t ldb,

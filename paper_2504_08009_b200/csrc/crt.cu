@@ -224,6 +224,20 @@ __device__ __forceinline__ double crt_element(const int32_t (&cp)[NM], int ei, i
     return crt_from_packed<NM>(P, ei, fj);
 }
 
+// C = beta C, or C = 0 when beta == 0 (C not read: BLAS semantics)
+__global__ void scale_c_kernel(double* __restrict__ C, int64_t m, int64_t n, int64_t ldc, double beta) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= m * n) return;
+    double* c = C + (idx / n) * ldc + idx % n;
+    *c = beta == 0.0 ? 0.0 : beta * *c;
+}
+
+void launch_scale_c(double* C, int64_t m, int64_t n, int64_t ldc, double beta, cudaStream_t st) {
+    const int64_t tot = m * n;
+    if (tot <= 0) return;
+    scale_c_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(C, m, n, ldc, beta);
+}
+
 template <int NM>
 __global__ void __launch_bounds__(256)
 crt_kernel(const int32_t* __restrict__ cprod, int64_t m, int64_t n, const int32_t* __restrict__ e,

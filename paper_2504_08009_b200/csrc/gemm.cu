@@ -91,6 +91,8 @@ struct Params {
     uint8_t* scratch;               // FUSED: [grid][2 slots][N][BM*BN] uint8 residues
     double* C;                      // FUSED
     int64_t ldc;
+    int axpby;                      // FUSED: 0 -> C = AB; 1 -> C = alpha AB (+ beta C if beta != 0)
+    double alpha, beta;
     const int32_t* e;
     const int32_t* f;
     uint32_t* sync_ctr;             // global progress counter (zeroed before launch), or NULL
@@ -194,6 +196,14 @@ __device__ __forceinline__ void crt_slice(const Params& p, const uint8_t* tile_s
                 const int col = col0 + j + jj;
                 const int fj = col < p.n ? __ldg(p.f + col) : 0;
                 o[jj] = crt_from_packed<NM>(P[2 * pr + jj], ei, fj);
+            }
+            if (p.axpby) {
+                // BLAS semantics (reading R19): RN(alpha c + RN(beta c_old)); C not read if beta == 0
+                #pragma unroll
+                for (int jj = 0; jj < 2; jj++) {
+                    if (j + jj < ncol)
+                        o[jj] = p.beta == 0.0 ? p.alpha * o[jj] : fma(p.alpha, o[jj], p.beta * crow[j + jj]);
+                }
             }
             if (vec) {
                 *reinterpret_cast<double2*>(crow + j) = make_double2(o[0], o[1]);
@@ -591,10 +601,12 @@ int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int
 
 int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                         int N, uint8_t* scratch, const int32_t* e, const int32_t* f, double* C, int64_t ldc,
-                        uint32_t* sync_ctr, int num_sms, cudaStream_t st) {
+                        uint32_t* sync_ctr, int num_sms, cudaStream_t st, double alpha, double beta) {
     int grid;
     gemm::Params p = make_params(m, n, k, N, num_sms, gemm_cta_group(), gemm_halves(), &grid);
     p.scratch = scratch; p.e = e; p.f = f; p.C = C; p.ldc = ldc;
+    p.axpby = (alpha != 1.0 || beta != 0.0) ? 1 : 0;
+    p.alpha = alpha; p.beta = beta;
     p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
     if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
     static unsigned long long* dbg = nullptr;

@@ -39,9 +39,13 @@ int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int
                   int N, int32_t* cprod, uint32_t* sync_ctr, int num_sms, cudaStream_t st);
 // + Alg. 1 lines 7-10 fused into the epilogue (uint8 residue scratch, exact CRT)
 size_t fused_scratch_bytes(int64_t m, int64_t n, int N, int num_sms);
+// (alpha, beta) != (1, 0): C = alpha AB + beta C in the epilogue (BLAS semantics)
 int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                         int N, uint8_t* scratch, const int32_t* e, const int32_t* f, double* C, int64_t ldc,
-                        uint32_t* sync_ctr, int num_sms, cudaStream_t st);
+                        uint32_t* sync_ctr, int num_sms, cudaStream_t st, double alpha = 1.0,
+                        double beta = 0.0);
+// C = beta C (beta != 0) or 0: the alpha = 0 / k = 0 cases of the DGEMM surface
+void launch_scale_c(double* C, int64_t m, int64_t n, int64_t ldc, double beta, cudaStream_t st);
 
 // crt.cu -- Alg. 1 lines 7-10
 void launch_crt(const int32_t* cprod, int64_t m, int64_t n, const int32_t* e, const int32_t* f,

@@ -28,8 +28,9 @@ SYMBOLS = [
     "oz2_workspace_bytes", "oz2_dgemm", "oz2_dgemm_ex", "oz2_dgemm_host", "oz2_scale_rows",
     "oz2_scale_cols", "oz2_trunc_rows", "oz2_trunc_cols", "oz2_residues_rows", "oz2_residues_cols",
     "oz2_modmul", "oz2_crt", "oz2_tables", "oz2_eq17_k", "oz2_strerror", "oz2_version",
-    "oz2_set_profiling", "oz2_stage_times",
+    "oz2_set_profiling", "oz2_stage_times", "oz2_dgemm_op", "oz2_dgemm_strided_batched",
 ]
+OP_N, OP_T = 0, 1
 # stage 0 times A's conversion (and B's too with OZ2_CONV_OVERLAP=1; the two column
 # stages then read 0); the host pipeline (oz2_dgemm_host) times rows of A inside "gemm"
 STAGES = ["rows_A", "colstats_B", "colres_B", "gemm", "crt"]
@@ -67,6 +68,10 @@ def lib() -> ctypes.CDLL:
                 L.oz2_dgemm.argtypes = [i64, i64, i64, P, i64, P, i64, P, i64, i32]
                 L.oz2_dgemm_ex.argtypes = [P, i64, i64, i64, P, i64, P, i64, P, i64, i32]
                 L.oz2_dgemm_host.argtypes = [P, i64, i64, i64, P, i64, P, i64, P, i64, i32]
+                d = ctypes.c_double
+                L.oz2_dgemm_op.argtypes = [P, i32, i32, i64, i64, i64, d, P, i64, P, i64, d, P, i64, i32]
+                L.oz2_dgemm_strided_batched.argtypes = [P, i32, i32, i64, i64, i64, d, P, i64, i64, P, i64, i64,
+                                                        d, P, i64, i64, i64, i32]
                 L.oz2_scale_rows.argtypes = [P, i64, i64, P, i64, i32, P]
                 L.oz2_scale_cols.argtypes = [P, i64, i64, P, i64, i32, P]
                 L.oz2_trunc_rows.argtypes = [P, i64, i64, P, i64, P, P]
@@ -228,6 +233,55 @@ def dgemm(A, B, num_moduli: int = 14, mode="fast", out=None):
     h.prepare(mode, workspace_bytes(m, n, k, num_moduli))
     _check(lib().oz2_dgemm_ex(h.ptr, m, n, k, _vp(A), _ld(A), _vp(B), _ld(B), _vp(C), _ld(C),
                               num_moduli), "oz2_dgemm_ex")
+    return C
+
+
+def gemm(A, B, num_moduli: int = 14, alpha: float = 1.0, beta: float = 0.0, C=None,
+         transA: bool = False, transB: bool = False, mode="fast"):
+    """C := alpha op(A) op(B) + beta C (float64, CUDA, row-major; BLAS DGEMM semantics)
+    through oz2_dgemm_op.  A, B are the STORED matrices: op(A) = A.T if transA."""
+    import torch
+
+    A = _rowmajor(A, torch.float64)
+    B = _rowmajor(B, torch.float64)
+    m, k = (A.shape[1], A.shape[0]) if transA else A.shape
+    kb, n = (B.shape[1], B.shape[0]) if transB else B.shape
+    if k != kb:
+        raise ValueError(f"inner dimensions differ: op(A) {m}x{k}, op(B) {kb}x{n}")
+    if C is None:
+        C = torch.zeros((m, n), dtype=torch.float64, device=A.device)
+    assert C.is_cuda and C.dtype == torch.float64 and C.shape == (m, n) and C.stride(1) == 1
+    h = handle(A.device.index)
+    h.prepare(mode, workspace_bytes(m, n, k, num_moduli))
+    _check(lib().oz2_dgemm_op(h.ptr, OP_T if transA else OP_N, OP_T if transB else OP_N, m, n, k,
+                              float(alpha), _vp(A), _ld(A), _vp(B), _ld(B), float(beta), _vp(C), _ld(C),
+                              num_moduli), "oz2_dgemm_op")
+    return C
+
+
+def gemm_strided_batched(A, B, num_moduli: int = 14, alpha: float = 1.0, beta: float = 0.0, C=None,
+                         transA: bool = False, transB: bool = False, mode="fast"):
+    """Batched gemm over the leading dimension of contiguous 3-D tensors (one
+    oz2_dgemm_strided_batched call)."""
+    import torch
+
+    assert A.dim() == 3 and B.dim() == 3 and A.shape[0] == B.shape[0]
+    A = A.contiguous()
+    B = B.contiguous()
+    batch = A.shape[0]
+    m, k = (A.shape[2], A.shape[1]) if transA else A.shape[1:]
+    kb, n = (B.shape[2], B.shape[1]) if transB else B.shape[1:]
+    if k != kb:
+        raise ValueError("inner dimensions differ")
+    if C is None:
+        C = torch.zeros((batch, m, n), dtype=torch.float64, device=A.device)
+    assert C.is_contiguous() and C.shape == (batch, m, n)
+    h = handle(A.device.index)
+    h.prepare(mode, workspace_bytes(m, n, k, num_moduli))
+    _check(lib().oz2_dgemm_strided_batched(
+        h.ptr, OP_T if transA else OP_N, OP_T if transB else OP_N, m, n, k, float(alpha),
+        _vp(A), max(1, A.shape[2]), A.shape[1] * A.shape[2], _vp(B), max(1, B.shape[2]), B.shape[1] * B.shape[2],
+        float(beta), _vp(C), max(1, n), m * n, batch, num_moduli), "oz2_dgemm_strided_batched")
     return C
 
 

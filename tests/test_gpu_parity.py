@@ -235,3 +235,48 @@ def test_c2_sampled(oz2, oracle, n, N):
     full_rows = rows[:2]
     Ar = A[torch.from_numpy(full_rows).to(DEV)].cpu().numpy()
     assert_bitwise(C[full_rows], oracle.dgemm(Ar, B.cpu().numpy(), N), f"c2 full rows N={N}")
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+def test_gemm_surface_transposes_alpha_beta(oz2, oracle, ta, tb):
+    """oz2_dgemm_op (reading R19): op(A), op(B) and C := alpha AB + beta C, bitwise."""
+    m, n, k = 300, 270, 520
+    Aop = phi_matrix_np(m, k, 1.0, seed=61)
+    Bop = phi_matrix_np(k, n, 1.0, seed=62)
+    A = Aop.T.copy() if ta else Aop
+    B = Bop.T.copy() if tb else Bop
+    Cold = phi_matrix_np(m, n, 1.0, seed=63)
+    for alpha, beta in [(1.0, 0.0), (-1.5, 0.0), (0.75, -2.0)]:
+        Cd = torch.from_numpy(Cold.copy()).to(DEV)
+        oz2.gemm(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), 14, alpha, beta, Cd,
+                 transA=ta, transB=tb)
+        ref = oracle.gemm(A, B, 14, alpha, beta, Cold, transA=ta, transB=tb)
+        assert_bitwise(Cd.cpu().numpy(), ref, f"gemm ta={ta} tb={tb} alpha={alpha} beta={beta}")
+
+
+def test_gemm_surface_degenerate(oz2, oracle):
+    A = torch.from_numpy(phi_matrix_np(40, 50, 1.0, seed=64)).to(DEV)
+    B = torch.from_numpy(phi_matrix_np(50, 30, 1.0, seed=65)).to(DEV)
+    C0 = phi_matrix_np(40, 30, 1.0, seed=66)
+    # beta = 0: C is not read (NaN must not propagate)
+    Cn = torch.full((40, 30), float("nan"), dtype=torch.float64, device=DEV)
+    oz2.gemm(A, B, 14, 2.0, 0.0, Cn)
+    assert_bitwise(Cn.cpu().numpy(), 2.0 * oracle.dgemm(A.cpu().numpy(), B.cpu().numpy(), 14), "beta=0")
+    # alpha = 0: C := beta C, no product
+    Cd = torch.from_numpy(C0.copy()).to(DEV)
+    oz2.gemm(A, B, 14, 0.0, -3.0, Cd)
+    assert_bitwise(Cd.cpu().numpy(), -3.0 * C0, "alpha=0")
+    # k = 0
+    Cd = torch.from_numpy(C0.copy()).to(DEV)
+    oz2.gemm(A[:, :0], B[:0, :], 14, 1.0, 0.5, Cd)
+    assert_bitwise(Cd.cpu().numpy(), 0.5 * C0, "k=0")
+
+
+def test_gemm_strided_batched(oz2, oracle):
+    rng_seeds = [(71, 72), (73, 74), (75, 76)]
+    A = np.stack([phi_matrix_np(90, 130, 1.0, seed=a) for a, _ in rng_seeds])
+    B = np.stack([phi_matrix_np(110, 130, 1.0, seed=b) for _, b in rng_seeds])    # stored n x k (transB)
+    C = oz2.gemm_strided_batched(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), 13,
+                                 transB=True).cpu().numpy()
+    for i in range(3):
+        assert_bitwise(C[i], oracle.gemm(A[i], B[i], 13, transB=True), f"batch item {i}")

@@ -214,3 +214,28 @@ def test_nonfinite_propagation_and_degenerate(oracle):
         oracle.dgemm(np.ones((1, 5)), np.ones((5, 1)), 21)
     with pytest.raises(oracle.OracleError):
         oracle.dgemm(np.ones((1, 5)), np.ones((5, 1)), 1)
+
+
+def test_gemm_surface_axpby_against_fractions(oracle):
+    """Reading R19 (BLAS DGEMM semantics around Algorithm 1): each entry is
+    RN(alpha c + RN(beta c_old)); pinned against exact rational arithmetic
+    (float(Fraction) rounds to nearest) and the transposes against dgemm."""
+    A = phi_matrix_np(6, 40, 1.0, seed=51)
+    B = phi_matrix_np(40, 5, 1.0, seed=52)
+    Cold = phi_matrix_np(6, 5, 2.0, seed=53)
+    c = oracle.dgemm(A, B, 14)
+    for alpha, beta in [(1.0, 0.0), (-0.7, 0.0), (1.3, 2.1), (3.0, -1.0), (1e-300, 1e300)]:
+        got = oracle.gemm(A, B, 14, alpha, beta, Cold)
+        for i in range(6):
+            for j in range(5):
+                if beta == 0.0:
+                    ref = alpha * c[i, j]
+                else:
+                    ref = float(Fraction(alpha) * Fraction(float(c[i, j])) + Fraction(beta * Cold[i, j]))
+                assert got[i, j] == ref, (alpha, beta, i, j)
+    # beta == 0: C_old is not read (NaN ignored); alpha == 0: no product
+    nan = np.full((6, 5), np.nan)
+    assert np.array_equal(oracle.gemm(A, B, 14, 2.0, 0.0, nan), 2.0 * c)
+    assert np.array_equal(oracle.gemm(A, B, 14, 0.0, 3.0, Cold), 3.0 * Cold)
+    # op(A) = A^T of the stored k x m matrix, op(B) = B^T of the stored n x k matrix
+    assert np.array_equal(oracle.gemm(A.T.copy(), B.T.copy(), 14, transA=True, transB=True), c)
