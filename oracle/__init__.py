@@ -23,6 +23,7 @@ _LIB = os.path.join(_HERE, "liboz2_oracle.so")
 
 MODE_FAST = 0
 MODE_EQ17 = 1
+MODE_ACCU = 2
 EXP_NONFINITE = -(2**31)
 KC = 256
 
@@ -78,6 +79,7 @@ def lib():
         L.oz2o_wide_from_double.argtypes = [ctypes.c_double, P]
         L.oz2o_wide_from_double.restype = None
         L.oz2o_set_threads.argtypes = [i32]
+        L.oz2o_scale_accu.argtypes = [i64, i64, i64, P, i64, P, i64, i32, P, P, P, P]
         L.oz2o_axpby.argtypes = [i64, ctypes.c_double, P, ctypes.c_double, P, P]
         L.oz2o_axpby.restype = None
         L.oz2o_set_threads.restype = None
@@ -174,6 +176,20 @@ def scale_cols(B, N: int, mode: int = MODE_FAST, q: int | None = None) -> np.nda
     else:
         _check(lib().oz2o_scale_eq17(n, k, _p(B), 1, n, N, k if q is None else q, _p(f)))
     return f
+
+
+def scale_accu(A, B, N: int):
+    """OS II-accu exponents (reading R18): (e, f, rowmax P, colmax P)."""
+    A = _as_f64(A)
+    B = _as_f64(B)
+    m, k = A.shape
+    n = B.shape[1]
+    e = np.zeros(m, np.int32)
+    f = np.zeros(n, np.int32)
+    pr = np.zeros(m, np.uint32)
+    pc = np.zeros(n, np.uint32)
+    _check(lib().oz2o_scale_accu(m, n, k, _p(A), max(k, 1), _p(B), max(n, 1), N, _p(e), _p(f), _p(pr), _p(pc)))
+    return e, f, pr, pc
 
 
 def trunc_rows(A, e) -> np.ndarray:

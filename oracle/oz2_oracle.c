@@ -40,6 +40,7 @@
 
 #define OZ2O_MODE_FAST 0
 #define OZ2O_MODE_EQ17 1
+#define OZ2O_MODE_ACCU 2
 
 /* R4/R5: chunk length of the FAST (Cauchy-Schwarz) rule */
 #define OZ2O_KC 256
@@ -377,6 +378,91 @@ int oz2o_scale_eq17(int64_t rows, int64_t len, const double* X, int64_t s_row,
     return OZ2O_OK;
 }
 
+/* Mode ACCU (OS II-accu: "employing cublasGemmEx with CUDA_R_8I
+ * for the line 1 to satisfy the condition (13)"; "low-precision
+ * computation", 637-640).  Reading R18, step by step:
+ *   1. E_i = ilogb(max_l |a_il|), F_j = ilogb(max_l |b_lj|)  (rows/cols of zeros: none);
+ *   2. 7-bit upper approximations  ahat_il = ceil(|a_il| 2^(6 - E_i)) in [0, 128],
+ *      bhat_lj = ceil(|b_lj| 2^(6 - F_j)), so |a_il| <= ahat_il 2^(E_i - 6);
+ *   3. P = Ahat Bhat, the INT8 GEMM of the line-1 bound (unsigned, exact in int32
+ *      for k < 2^17):  (|A||B|)_ij <= P_ij 2^(E_i + F_j - 12);
+ *   4. with lambda(x) = ceil(log2 x):  g_i = min(G, floor((L + 12 - lambda(max_j P_ij)) / 2)),
+ *      h_j = min(G, floor((L + 12 - lambda(max_i P_ij)) / 2))  (G where the maximum
+ *      is 0);  e_i = g_i - E_i,  f_j = h_j - F_j.  G = 61 (N <= 16) or 93 (N > 16)
+ *      keeps |a'| < 2^(g + 1) within 62 / 94 bits, the integer width of FAST's
+ *      largest |a'| (2^T, T = 62 at N = 16, 77 at N = 20) rounded to whole words.
+ * Then (|A'||B'|)_ij <= 2^(g_i + h_j - 12) P_ij <= 2^L < M/2 (condition (13)).
+ * A zero row / column gets 0; one holding Inf / NaN the sentinel (R13).         */
+static int ilogb_max(int64_t len, const double* X, int64_t s_col, int* bad) {
+    int E = INT_MIN;
+    *bad = 0;
+    for (int64_t l = 0; l < len; l++) {
+        double x = X[l * s_col];
+        if (!isfinite(x)) { *bad = 1; return INT_MIN; }
+        if (x != 0.0) { int ex = ilogb(x); if (ex > E) E = ex; }
+    }
+    return E;
+}
+static uint8_t hat7(double x, int E) {                   /* ceil(|x| 2^(6 - E)) */
+    if (x == 0.0 || E == INT_MIN) return 0;
+    /* exact whenever the result is >= 1 (values < 1 become 1); 2^(6-E) itself
+     * overflows for E < -1017, hence two steps there                           */
+    double v = 6 - E > 1000 ? ceil(ldexp(ldexp(fabs(x), 1000), 6 - E - 1000)) : ceil(ldexp(fabs(x), 6 - E));
+    return (uint8_t)(v < 1.0 ? 1.0 : v);
+}
+static int lambda_ceil_log2(uint64_t x) {                /* ceil(log2 x), x >= 1 */
+    int l = 0;
+    while (l < 64 && (1ull << l) < x) l++;
+    return l;
+}
+static int floor_half(int v) { return v >= 0 ? v / 2 : -((-v + 1) / 2); }
+
+int oz2o_scale_accu(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                    int64_t ldb, int N, int32_t* e, int32_t* f, uint32_t* P_rowmax, uint32_t* P_colmax) {
+    consts_t c; int rc = make_consts(N, &c); if (rc) return rc;
+    if (k >= (1 << 17)) return OZ2O_ERR_K_TOO_LARGE;     /* the bound GEMM is exact in int32 */
+    int* E = (int*)malloc(sizeof(int) * (m ? m : 1));
+    int* F = (int*)malloc(sizeof(int) * (n ? n : 1));
+    int* badA = (int*)malloc(sizeof(int) * (m ? m : 1));
+    int* badB = (int*)malloc(sizeof(int) * (n ? n : 1));
+    uint8_t* Ah = (uint8_t*)malloc((size_t)(m * k > 0 ? m * k : 1));
+    uint8_t* Bh = (uint8_t*)malloc((size_t)(n * k > 0 ? n * k : 1));   /* Bhat^T: n x k */
+    uint32_t* rmax = (uint32_t*)calloc((size_t)(m ? m : 1), sizeof(uint32_t));
+    uint32_t* cmax = (uint32_t*)calloc((size_t)(n ? n : 1), sizeof(uint32_t));
+    for (int64_t i = 0; i < m; i++) {                    /* steps 1-2, rows of A */
+        E[i] = ilogb_max(k, A + i * lda, 1, &badA[i]);
+        for (int64_t l = 0; l < k; l++) Ah[i * k + l] = badA[i] ? 0 : hat7(A[i * lda + l], E[i]);
+    }
+    for (int64_t j = 0; j < n; j++) {                    /* steps 1-2, columns of B */
+        F[j] = ilogb_max(k, B + j, ldb, &badB[j]);
+        for (int64_t l = 0; l < k; l++) Bh[j * k + l] = badB[j] ? 0 : hat7(B[l * ldb + j], F[j]);
+    }
+    #pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t i = 0; i < m; i++)                      /* step 3 */
+        for (int64_t j = 0; j < n; j++) {
+            uint64_t p = 0;
+            for (int64_t l = 0; l < k; l++) p += (uint64_t)Ah[i * k + l] * Bh[j * k + l];
+            if (p > rmax[i]) rmax[i] = (uint32_t)p;
+            #pragma omp critical
+            { if (p > cmax[j]) cmax[j] = (uint32_t)p; }
+        }
+    const int G = N <= 16 ? 61 : 93;
+    for (int64_t i = 0; i < m; i++) {                    /* step 4 */
+        int g = rmax[i] ? floor_half(c.L + 12 - lambda_ceil_log2(rmax[i])) : G;
+        if (g > G) g = G;
+        e[i] = badA[i] ? OZ2O_EXP_NONFINITE : (E[i] == INT_MIN ? 0 : g - E[i]);
+        if (P_rowmax) P_rowmax[i] = rmax[i];
+    }
+    for (int64_t j = 0; j < n; j++) {
+        int h = cmax[j] ? floor_half(c.L + 12 - lambda_ceil_log2(cmax[j])) : G;
+        if (h > G) h = G;
+        f[j] = badB[j] ? OZ2O_EXP_NONFINITE : (F[j] == INT_MIN ? 0 : h - F[j]);
+        if (P_colmax) P_colmax[j] = cmax[j];
+    }
+    free(E); free(F); free(badA); free(badB); free(Ah); free(Bh); free(rmax); free(cmax);
+    return OZ2O_OK;
+}
+
 /* Alg. 1 lines 2-3: x' = trunc(2^e x), an FP64 integer.
  * Out is rows x len, row-major.  Non-finite rows give 0 (R13).                */
 void oz2o_trunc_scale(int64_t rows, int64_t len, const double* X, int64_t s_row,
@@ -488,6 +574,9 @@ int oz2o_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
     if (mode == OZ2O_MODE_FAST) {
         oz2o_scale_fast(m, k, A, lda, 1, N, e);
         oz2o_scale_fast(n, k, B, 1, ldb, N, f);
+    } else if (mode == OZ2O_MODE_ACCU) {
+        rc = oz2o_scale_accu(m, n, k, A, lda, B, ldb, N, e, f, NULL, NULL);
+        if (rc) { free(e); free(f); return rc; }
     } else {
         rc = oz2o_scale_eq17(m, k, A, lda, 1, N, k, e);
         if (!rc) rc = oz2o_scale_eq17(n, k, B, 1, ldb, N, k, f);

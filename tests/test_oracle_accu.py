@@ -1,0 +1,93 @@
+"""Pins of the OS II-accu scaling rule (reading R18 in
+DESIGN.md): a hand-derived worked example, the bound it rests on checked with
+exact integers, condition (13) on every entry, and the paper's claim that accu
+is more accurate than fast at large phi.  The bound GEMM P is recomputed here
+with a numpy int64 matmul (a library primitive) from 7-bit values built with
+Python's exact float arithmetic -- independent of the C oracle's loops."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2504_08009_b200.inputs import phi_matrix_np
+
+
+def _hat7(x, E):
+    # ceil(|x| 2^(6 - E)) with exact rational arithmetic (math.ldexp is exact here
+    # except below 1, where the result is clamped to 1 for x != 0)
+    if x == 0.0:
+        return 0
+    from fractions import Fraction
+    v = Fraction(abs(x)) * Fraction(2) ** (6 - E)
+    return max(1, math.ceil(v))
+
+
+def _ilogb(x):
+    return math.frexp(x)[1] - 1
+
+
+def test_worked_example_n2(oracle):
+    # A = [[1, 0.5]], B = [[0.25], [-3]], N = 2 (M = 65280, L = 14, T = 7):
+    # E = 0, ahat = [64, 32]; F = ilogb 3 = 1, bhat = [8, 96]; P = 512 + 3072 = 3584,
+    # lambda = 12, g = h = min(61, floor((14 + 12 - 12) / 2)) = 7 -> e = 7, f = 6;
+    # A' = [128, 64] (128 mod 256 is the Eq. (1) tie -> -128), B' = [16, -192],
+    # sum |a'||b'| = 2048 + 12288 = 14336 < M/2 = 32640, X = -10240, C = -10240 / 2^13.
+    A = np.array([[1.0, 0.5]])
+    B = np.array([[0.25], [-3.0]])
+    e, f, pr, pc = oracle.scale_accu(A, B, 2)
+    assert list(pr) == [3584] and list(pc) == [3584]
+    assert list(e) == [7] and list(f) == [6]
+    assert oracle.dgemm(A, B, 2, oracle.MODE_ACCU)[0, 0] == -1.25
+
+
+@pytest.mark.parametrize("N,phi", [(8, 1.0), (14, 4.0), (16, 2.0), (20, 4.0)])
+def test_bound_and_condition_13(oracle, N, phi):
+    m, n, k = 7, 6, 90
+    A = phi_matrix_np(m, k, phi, seed=81)
+    B = phi_matrix_np(k, n, phi, seed=82)
+    A[2, :] = 0.0                                          # a zero row
+    B[5, :] *= 1e-300                                      # tiny entries (subnormal range)
+    e, f, pr, pc = oracle.scale_accu(A, B, N)
+    E = [max(_ilogb(v) for v in row if v != 0) if np.any(row) else None for row in A]
+    F = [max(_ilogb(v) for v in col if v != 0) for col in B.T]
+    Ah = np.array([[_hat7(v, E[i]) if E[i] is not None else 0 for v in A[i]] for i in range(m)], np.int64)
+    Bh = np.array([[_hat7(v, F[j]) for v in B[:, j]] for j in range(n)], np.int64)
+    P = Ah @ Bh.T                                          # the line-1 INT8 GEMM
+    assert list(pr) == list(P.max(axis=1)) and list(pc) == list(P.max(axis=0))
+    c = oracle.constants(N)
+    L, T, M = c["L"], c["T"], math.prod(c["moduli"])
+    assert e[2] == 0
+    Ap = oracle.trunc_rows(A, e)
+    BpT = oracle.trunc_cols(B, f)
+    for i in range(m):
+        for j in range(n):
+            s = sum(abs(int(a)) * abs(int(b)) for a, b in zip(Ap[i], BpT[j]))
+            assert 2 * s < M                                # condition (13)
+    G = 61 if N <= 16 else 93                              # integer width cap of reading R18
+    assert all(abs(int(v)) < 2**(G + 1) for v in Ap.ravel()) and all(abs(int(v)) < 2**(G + 1) for v in BpT.ravel())
+    # the rule itself: g + h + lambda(P_ij) <= L + 12 for every entry
+    for i in range(m):
+        if E[i] is None:
+            continue
+        for j in range(n):
+            if P[i, j]:
+                lam = math.ceil(math.log2(int(P[i, j]))) if P[i, j] > 1 else 0
+                assert (e[i] + E[i]) + (f[j] + F[j]) + lam <= L + 12
+
+
+def test_accu_more_accurate_than_fast_at_large_phi(oracle):
+    """less overestimation of |A'||B'| -> more accurate, and it
+    can deal with larger phi."""
+    m, n, k = 24, 24, 512
+    A = phi_matrix_np(m, k, 4.0, seed=83)
+    B = phi_matrix_np(k, n, 4.0, seed=84)
+    ii, jj = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+    ab, absab = oracle.exact_entries(A, B, ii.ravel(), jj.ravel())
+    ab = ab.reshape(m, n)
+    absab = absab.reshape(m, n)
+    for N in (14, 16, 18):
+        ef = np.abs(oracle.dgemm(A, B, N, oracle.MODE_FAST) - ab) / absab
+        ea = np.abs(oracle.dgemm(A, B, N, oracle.MODE_ACCU) - ab) / absab
+        assert np.max(ea) <= np.max(ef) and np.median(ea) < np.median(ef), (N, np.max(ea), np.max(ef))
+        if N in (14, 18):
+            assert np.max(ea) < np.max(ef), (N, np.max(ea), np.max(ef))          # strictly better at phi = 4
