@@ -57,6 +57,8 @@ extern "C" {
 
 #define OZ2_MODE_FAST 0   /* OS II-fast: Cauchy-Schwarz bound, reading R4 */
 #define OZ2_MODE_EQ17 1   /* Eqs. (15)-(17): k_A = k_B = floor(log2((M/2-1)/q)/2) */
+#define OZ2_MODE_ACCU 2   /* OS II-accu: an INT8 GEMM of 7-bit upper approximations of |A|, |B|
+                             bounds |A'||B'|, reading R18; k < 2^17 */
 
 #define OZ2_EXP_NONFINITE INT32_MIN
 
@@ -71,7 +73,9 @@ int oz2_create(oz2_handle_t* h, int device);
 int oz2_destroy(oz2_handle_t h);
 /* Subsequent calls launch on `stream` (a cudaStream_t; NULL = legacy). */
 int oz2_set_stream(oz2_handle_t h, void* stream);
-/* OZ2_MODE_FAST (default) or OZ2_MODE_EQ17: the rule for Alg. 1 line 1. */
+/* OZ2_MODE_FAST (default), OZ2_MODE_EQ17 or OZ2_MODE_ACCU: the rule for Alg. 1
+ * line 1.  ACCU couples the operands (e depends on B, f on A): the split-API
+ * oz2_scale_rows / oz2_scale_cols reject it (use oz2_scale_accu). */
 int oz2_set_mode(oz2_handle_t h, int mode);
 /* Use caller-owned device memory [ptr, ptr+bytes) as workspace (NULL, 0 =
  * library-managed, grown on demand with cudaMalloc).  Must stay valid and
@@ -132,6 +136,10 @@ int oz2_scale_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_
 /* Alg. 1 line 1 for the columns of B (k x n): f[j], E = diag(2^f[j]).  f: int32[n]. */
 int oz2_scale_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb,
                    int num_moduli, int32_t* f);
+/* Alg. 1 line 1 by the OS II-accu rule (reading R18) for the product A B
+ * (A m x k, B k x n, row-major; k < 2^17): e[m], f[n].  Any handle mode. */
+int oz2_scale_accu(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                   const double* B, int64_t ldb, int num_moduli, int32_t* e, int32_t* f);
 /* Alg. 1 line 2: Ap = trunc(D A), m x k row-major FP64 integers (ld = k). */
 int oz2_trunc_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda,
                    const int32_t* e, double* Ap);

@@ -71,6 +71,10 @@ int host_T(int N) {
     std::call_once(g_tabs_once, build_tables_once);
     return g_tabs[N].T;
 }
+int host_L(int N) {
+    std::call_once(g_tabs_once, build_tables_once);
+    return g_tabs[N].L;
+}
 }  // namespace oz2
 
 struct oz2_context {
@@ -113,7 +117,9 @@ inline int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
 
 struct Layout {
     int64_t ldr;
-    size_t off_Ares, off_Bres, off_e, off_f, off_stats, off_scratch, off_sync, total;
+    size_t off_Ares, off_Bres, off_e, off_f, off_stats, off_scratch, off_sync;
+    size_t off_E, off_F, off_pr, off_pc;     // accu line 1: max exponents, row / column maxima of P
+    size_t total;
 };
 
 Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms, int64_t stats_cols = -1) {
@@ -128,6 +134,10 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms, int64_t s
     L.off_stats = take(oz2::cols_stats_bytes(k, stats_cols >= 0 ? stats_cols : n));
     L.off_scratch = take(oz2::fused_scratch_bytes(m, n, N, num_sms));
     L.off_sync = take(256);
+    L.off_E = take(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));
+    L.off_F = take(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    L.off_pr = take(sizeof(uint32_t) * (size_t)(m > 0 ? m : 1));
+    L.off_pc = take(sizeof(uint32_t) * (size_t)(n > 0 ? n : 1));
     L.total = off;
     return L;
 }
@@ -199,6 +209,11 @@ struct DevGuard {
 };
 
 oz2_handle_t g_default[64] = {nullptr};
+
+int check_op_args(int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                  int64_t ldb, const double* C, int64_t ldc, int N);
+int accu_line1(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+               const double* B, int64_t ldb, int N, uint8_t* ws, const Layout& L, int32_t* e, int32_t* f);
 
 int env_flag(const char* name, int dflt) {
     const char* v = getenv(name);
@@ -293,7 +308,7 @@ int oz2_set_stream(oz2_handle_t h, void* stream) {
 }
 
 int oz2_set_mode(oz2_handle_t h, int mode) {
-    if (!h || (mode != OZ2_MODE_FAST && mode != OZ2_MODE_EQ17)) return OZ2_ERR_INVALID_ARG;
+    if (!h || (mode != OZ2_MODE_FAST && mode != OZ2_MODE_EQ17 && mode != OZ2_MODE_ACCU)) return OZ2_ERR_INVALID_ARG;
     h->mode = mode;
     return OZ2_OK;
 }
@@ -350,7 +365,7 @@ size_t oz2_workspace_bytes(int64_t m, int64_t n, int64_t k, int N) {
 // split API
 // ---------------------------------------------------------------------------
 int oz2_scale_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda, int N, int32_t* e) {
-    if (!h) return OZ2_ERR_INVALID_ARG;
+    if (!h || h->mode == OZ2_MODE_ACCU) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(m, 1, k, N);
     if (rc) return rc;
     if (lda < (k > 0 ? k : 1) || (m > 0 && (!A || !e))) return OZ2_ERR_INVALID_ARG;
@@ -362,7 +377,7 @@ int oz2_scale_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_
 }
 
 int oz2_scale_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb, int N, int32_t* f) {
-    if (!h) return OZ2_ERR_INVALID_ARG;
+    if (!h || h->mode == OZ2_MODE_ACCU) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(1, n, k, N);
     if (rc) return rc;
     if (ldb < (n > 0 ? n : 1) || (n > 0 && (!B || !f))) return OZ2_ERR_INVALID_ARG;
@@ -373,6 +388,25 @@ int oz2_scale_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_
     if ((rc = get_workspace(h, oz2::cols_stats_bytes(k, n), &ws))) return rc;
     oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws, h->stream);
     return cuda_status();
+}
+
+int oz2_scale_accu(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                   const double* B, int64_t ldb, int N, int32_t* e, int32_t* f) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(m, n, k, N);
+    if (rc) return rc;
+    if (lda < (k > 0 ? k : 1) || ldb < (n > 0 ? n : 1)) return OZ2_ERR_INVALID_ARG;
+    if ((m > 0 && !e) || (n > 0 && !f) || ((m > 0 || n > 0) && k > 0 && (!A || !B))) return OZ2_ERR_INVALID_ARG;
+    DevGuard g(h->device);
+    if (k == 0 || m == 0 || n == 0) {                 // no products: zero rows / columns get 0
+        if (m > 0) cudaMemsetAsync(e, 0, sizeof(int32_t) * (size_t)m, h->stream);
+        if (n > 0) cudaMemsetAsync(f, 0, sizeof(int32_t) * (size_t)n, h->stream);
+        return cuda_status();
+    }
+    Layout L = layout_for(m, n, k, 1, h->num_sms);
+    uint8_t* ws;
+    if ((rc = get_workspace(h, L.total, &ws))) return rc;
+    return accu_line1(h, OZ2_OP_N, OZ2_OP_N, m, n, k, A, lda, B, ldb, N, ws, L, e, f);
 }
 
 int oz2_trunc_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda, const int32_t* e,
@@ -466,6 +500,41 @@ int check_op_args(int ta, int tb, int64_t m, int64_t n, int64_t k, const double*
     return OZ2_OK;
 }
 
+// Alg. 1 line 1 by the OS II-accu rule (reading R18): e[m], f[n] from op(A),
+// op(B).  Uses plane 0 of the residue buffers for the 7-bit approximations
+// (overwritten by the residues afterwards).  k < 2^17 (exact int32 bound GEMM).
+int accu_line1(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+               const double* B, int64_t ldb, int N, uint8_t* ws, const Layout& L, int32_t* e, int32_t* f) {
+    if (k >= (int64_t)1 << 17) return OZ2_ERR_K_TOO_LARGE;
+    uint8_t* Ah = ws + L.off_Ares;
+    uint8_t* Bh = ws + L.off_Bres;
+    int32_t* E = (int32_t*)(ws + L.off_E);
+    int32_t* F = (int32_t*)(ws + L.off_F);
+    uint32_t* pr = (uint32_t*)(ws + L.off_pr);
+    uint32_t* pc = (uint32_t*)(ws + L.off_pc);
+    if (ta == OZ2_OP_N) {
+        oz2::launch_rows_hat7(A, m, k, lda, E, Ah, L.ldr, h->stream);
+    } else {
+        oz2::launch_cols_exponents(A, k, m, lda, N, OZ2_MODE_ACCU, 0, E, ws + L.off_stats, h->stream);
+        oz2::launch_cols_hat7(A, k, m, lda, E, Ah, L.ldr, h->stream);
+    }
+    if (tb == OZ2_OP_N) {
+        oz2::launch_cols_exponents(B, k, n, ldb, N, OZ2_MODE_ACCU, 0, F, ws + L.off_stats, h->stream);
+        oz2::launch_cols_hat7(B, k, n, ldb, F, Bh, L.ldr, h->stream);
+    } else {
+        oz2::launch_rows_hat7(B, n, k, ldb, F, Bh, L.ldr, h->stream);
+    }
+    CUtensorMap tA, tB;
+    int rc;
+    if ((rc = make_plane_map(&tA, (const int8_t*)Ah, m, k, L.ldr, 1, 128))) return rc;
+    if ((rc = make_plane_map(&tB, (const int8_t*)Bh, n, k, L.ldr, 1, 256 / oz2::gemm_cta_group()))) return rc;
+    if (oz2::launch_bound_gemm(&tA, &tB, m, n, k, pr, pc, (uint32_t*)(ws + L.off_sync), h->num_sms, h->stream))
+        return OZ2_ERR_CUDA;
+    oz2::launch_accu_finalize(E, pr, m, N, e, h->stream);
+    oz2::launch_accu_finalize(F, pc, n, N, f, h->stream);
+    return cuda_status();
+}
+
 // C = alpha op(A) op(B) + beta C by Algorithm 1 (arguments already checked).
 // op(A) = A^T means the stored A is k x m: its "rows of op(A)" are the columns
 // of the stored matrix, so the column kernels produce e and the K-major planes;
@@ -492,28 +561,33 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     CUtensorMap tA, tB;
     if ((rc = make_plane_map(&tA, Ares, m, k, L.ldr, N, 128))) return rc;
     if ((rc = make_plane_map(&tB, Bres, n, k, L.ldr, N, 256 / oz2::gemm_cta_group()))) return rc;
-    // Part 1 + 2-a (Alg. 1 lines 1-5) for op(A) and op(B)
+    // Part 1 + 2-a (Alg. 1 lines 1-5) for op(A) and op(B).  With the accu rule
+    // the exponents come first from both operands (accu_line1, timed in stage
+    // ROWS), and the conversions below only form the residues.
+    const bool accu = h->mode == OZ2_MODE_ACCU;
+    const int what = accu ? 2 : 3;
     auto convert_A = [&](cudaStream_t st) {
         if (ta == OZ2_OP_N) {
-            oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, st);
+            oz2::launch_rows(A, m, k, lda, N, what, h->mode, kstar, e, Ares, L.ldr, st);
         } else {
-            oz2::launch_cols_exponents(A, k, m, lda, N, h->mode, kstar, e, ws + L.off_stats, st);
+            if (!accu) oz2::launch_cols_exponents(A, k, m, lda, N, h->mode, kstar, e, ws + L.off_stats, st);
             oz2::launch_cols_residues(A, k, m, lda, e, N, Ares, L.ldr, st);
         }
     };
     auto convert_B_stats = [&](cudaStream_t st) {
-        if (tb == OZ2_OP_N) oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, st);
+        if (tb == OZ2_OP_N && !accu) oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, st);
     };
     auto convert_B_res = [&](cudaStream_t st) {
         if (tb == OZ2_OP_N) oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, st);
-        else oz2::launch_rows(B, n, k, ldb, N, 3, h->mode, kstar, f, Bres, L.ldr, st);
+        else oz2::launch_rows(B, n, k, ldb, N, what, h->mode, kstar, f, Bres, L.ldr, st);
     };
     mark(h);
+    if (accu && (rc = accu_line1(h, ta, tb, m, n, k, A, lda, B, ldb, N, ws, L, e, f))) return rc;
     // A and B are independent passes; OZ2_CONV_OVERLAP=1 runs B's on a second
     // stream concurrently with A's (stage ROWS then times both, the column stages
     // read 0).  Default off: measured no gain, both passes are issue-bound.  (Not
     // with op(A) = A^T, whose column statistics share B's scratch.)
-    const bool overlap = env_flag("OZ2_CONV_OVERLAP", 0) && ta == OZ2_OP_N;
+    const bool overlap = env_flag("OZ2_CONV_OVERLAP", 0) && ta == OZ2_OP_N && !accu;
     if (overlap) {
         if ((rc = ensure_aux(h))) return rc;
         cudaEventRecord(h->ev_fork, h->stream);
@@ -608,6 +682,34 @@ int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
     if (k == 0) {
         for (int64_t i = 0; i < m; i++) memset(C + i * ldc, 0, sizeof(double) * (size_t)n);
         return OZ2_OK;
+    }
+    if (h->mode == OZ2_MODE_ACCU) {
+        // f depends on every row of A under the accu rule: no row-block pipeline
+        Layout L = layout_for(m, n, k, N, h->num_sms, std::max(m, n));
+        const size_t offA = (size_t)round_up((int64_t)L.total, 256);
+        const size_t offB = (size_t)round_up((int64_t)(offA + sizeof(double) * (size_t)m * k), 256);
+        const size_t offC = (size_t)round_up((int64_t)(offB + sizeof(double) * (size_t)k * n), 256);
+        uint8_t* ws;
+        if ((rc = get_workspace(h, offC + sizeof(double) * (size_t)m * n, &ws))) return rc;
+        double* dA = (double*)(ws + offA);
+        double* dB = (double*)(ws + offB);
+        double* dC = (double*)(ws + offC);
+        if (cudaMemcpy2DAsync(dA, sizeof(double) * k, A, sizeof(double) * lda, sizeof(double) * k, m,
+                              cudaMemcpyHostToDevice, h->stream) != cudaSuccess ||
+            cudaMemcpy2DAsync(dB, sizeof(double) * n, B, sizeof(double) * ldb, sizeof(double) * n, k,
+                              cudaMemcpyHostToDevice, h->stream) != cudaSuccess)
+            return OZ2_ERR_CUDA;
+        void* save_ptr = h->ws_user;
+        size_t save_bytes = h->ws_user_bytes;
+        h->ws_user = ws;
+        h->ws_user_bytes = L.total;
+        rc = dgemm_core(h, OZ2_OP_N, OZ2_OP_N, m, n, k, 1.0, dA, k, dB, n, 0.0, dC, n, N);
+        h->ws_user = save_ptr;
+        h->ws_user_bytes = save_bytes;
+        if (rc) return rc;
+        if (cudaMemcpy2DAsync(C, sizeof(double) * ldc, dC, sizeof(double) * n, sizeof(double) * n, m,
+                              cudaMemcpyDeviceToHost, h->stream) != cudaSuccess) return OZ2_ERR_CUDA;
+        return cudaStreamSynchronize(h->stream) == cudaSuccess ? OZ2_OK : OZ2_ERR_CUDA;
     }
     // Pipeline over R row blocks of A and C (rows a multiple of 256): B goes
     // first on the H2D stream and is converted once; row block i is converted and

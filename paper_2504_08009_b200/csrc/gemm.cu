@@ -92,6 +92,8 @@ struct Params {
     double* C;                      // FUSED
     int64_t ldc;
     int axpby;                      // FUSED: 0 -> C = AB; 1 -> C = alpha AB (+ beta C if beta != 0)
+    uint32_t* rowmax;               // BOUND (NM < 0): max_j P_ij, max_i P_ij (atomicMax)
+    uint32_t* colmax;
     double alpha, beta;
     const int32_t* e;
     const int32_t* f;
@@ -221,6 +223,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
               const Params p) {
     using C_ = Cfg<CG, NH>;
     constexpr bool FUSED = NM > 0;
+    constexpr bool BOUND = NM < 0;                    // OS II-accu line-1 bound GEMM (unsigned, maxima only)
     constexpr int TB = C_::TILE_BYTES;
     extern __shared__ uint8_t smem_raw[];
     Smem<CG, NH>& s = *reinterpret_cast<Smem<CG, NH>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -315,7 +318,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA) =====================
         if (lane == 0 && leader) {
-            const uint32_t idesc = idesc_i8(C_::TILE_M, BN);
+            const uint32_t idesc = idesc_i8(C_::TILE_M, BN, !BOUND);
             int stage = 0; uint32_t ph = 0;
             int acc = 0; uint32_t aph = 0;     // NH = 1: buffer and its phase; NH = 2: phase of the halves
             for_each_subunit(p, cid, ncl, [&](int, int, int, int, int kb0, int kb1) {
@@ -425,6 +428,28 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     if (v[0] == 0x12345678u && v[31] == 0x9abcdef0u) p.cprod[0] = 1;   // keep the loads alive
                 }
                 release();
+            } else if constexpr (BOUND) {
+                // row maxima in registers, column maxima by a warp max-reduction per
+                // column (REDUX), one atomicMax per column and chunk
+                uint32_t rm = 0;
+                #pragma unroll 1
+                for (int cc = 0; cc < CH; cc++) {
+                    const int c = half * CH + cc;
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(tbase + (uint32_t)(c * 32), v);
+                    tmem_ld_wait();
+                    uint32_t mine = 0;
+                    #pragma unroll
+                    for (int j = 0; j < 32; j++) {
+                        rm = max(rm, v[j]);
+                        const uint32_t x = __reduce_max_sync(0xffffffffu, v[j]);
+                        mine = lane == j ? x : mine;
+                    }
+                    const int col = tn * C_::TILE_N + c * 32 + lane;
+                    if (col < p.n && mine) atomicMax(p.colmax + col, mine);
+                }
+                release();
+                if (row < p.m && rm) atomicMax(p.rowmax + row, rm);
             } else if constexpr (!FUSED) {
                 #pragma unroll 1
                 for (int cc = 0; cc < CH; cc++) {
@@ -597,6 +622,20 @@ int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int
     p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
     if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
     return gemm::launch_shape<0>(gemm_shape(), tmA, tmB, p, grid, st);
+}
+
+int launch_bound_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
+                      uint32_t* rowmax, uint32_t* colmax, uint32_t* sync_ctr, int num_sms, cudaStream_t st) {
+    int grid;
+    gemm::Params p = make_params(m, n, k, 1, num_sms, gemm_cta_group(), gemm_halves(), &grid);
+    p.rowmax = rowmax; p.colmax = colmax;
+    p.kb_chunk = std::max(1, p.num_kb);               // one exact int32 accumulation (k < 2^17)
+    p.nchunk = 1;
+    p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
+    if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
+    cudaMemsetAsync(rowmax, 0, sizeof(uint32_t) * (size_t)m, st);
+    cudaMemsetAsync(colmax, 0, sizeof(uint32_t) * (size_t)n, st);
+    return gemm::launch_shape<-1>(gemm_shape(), tmA, tmB, p, grid, st);
 }
 
 int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,

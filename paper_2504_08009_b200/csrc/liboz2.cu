@@ -3,5 +3,6 @@
 #include "oz2_device.cuh"
 #include "scale.cu"
 #include "crt.cu"
+#include "accu.cu"
 #include "gemm.cu"
 #include "api.cu"

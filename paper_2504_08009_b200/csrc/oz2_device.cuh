@@ -7,6 +7,7 @@
 #include "oz2_tables.h"
 
 #define OZ2_EXP_NONFINITE_DEV INT32_MIN
+#define OZ2_EXP_ZERO_DEV (INT32_MIN + 1)     // accu-internal: max exponent of an all-zero row/column
 
 // per-N constants, filled once per device by api.cu (the library is one
 // translation unit, liboz2.cu, so this is the single definition)
@@ -170,10 +171,10 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     return d;
 }
 // instruction descriptor, kind::i8: s8 x s8 -> s32, both K-major, M x N
-__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool is_signed = true) {
     return (2u << 4)                 // c_format = S32
-         | (1u << 7)                 // a_format = signed int8
-         | (1u << 10)                // b_format = signed int8
+         | ((is_signed ? 1u : 0u) << 7)    // a_format: signed / unsigned int8
+         | ((is_signed ? 1u : 0u) << 10)   // b_format: signed / unsigned int8
          | ((uint32_t)(N >> 3) << 17)
          | ((uint32_t)(M >> 4) << 24);
 }

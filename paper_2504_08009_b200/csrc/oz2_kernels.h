@@ -18,6 +18,7 @@ __host__ __device__ constexpr int crt_swords(int N) { return (m_bits(N) + 13 + 3
 __host__ __device__ constexpr int crt_words(int N) { return (m_bits(N) + 2 + 31) / 32; }
 
 int host_T(int N);   // floor(L/2) for N moduli (host copy of the table)
+int host_L(int N);   // floor(log2(M/2 - 1))
 
 // scale.cu -- Alg. 1 lines 1-5
 // what: 1 = exponents e, 2 = residues (given e), 3 = both (one pass per row)
@@ -46,6 +47,17 @@ int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t 
                         double beta = 0.0);
 // C = beta C (beta != 0) or 0: the alpha = 0 / k = 0 cases of the DGEMM surface
 void launch_scale_c(double* C, int64_t m, int64_t n, int64_t ldc, double beta, cudaStream_t st);
+
+// accu.cu -- Alg. 1 line 1 by the OS II-accu rule (reading R18)
+void launch_rows_hat7(const double* X, int64_t rows, int64_t k, int64_t ld, int32_t* E, uint8_t* hat, int64_t ldr,
+                      cudaStream_t st);
+void launch_cols_hat7(const double* X, int64_t k, int64_t cols, int64_t ld, const int32_t* F, uint8_t* hat,
+                      int64_t ldr, cudaStream_t st);
+void launch_accu_finalize(const int32_t* E, const uint32_t* Pmax, int64_t cnt, int N, int32_t* e, cudaStream_t st);
+// the line-1 bound GEMM P = Ahat Bhat^T (unsigned int8): only row / column maxima
+// of P leave the chip (atomicMax into rowmax[m], colmax[n], zeroed here first)
+int launch_bound_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
+                      uint32_t* rowmax, uint32_t* colmax, uint32_t* sync_ctr, int num_sms, cudaStream_t st);
 
 // crt.cu -- Alg. 1 lines 7-10
 void launch_crt(const int32_t* cprod, int64_t m, int64_t n, const int32_t* e, const int32_t* f,

@@ -387,6 +387,10 @@ __global__ void cols_finalize_kernel(const int32_t* __restrict__ Ec, const unsig
     int E = INT32_MIN;
     for (int c = 0; c < nch; c++) E = max(E, Ec[(int64_t)c * n + j]);
     int e;
+    if (MODE == 2) {                                  // accu: the raw max exponent (zero column marked)
+        f[j] = bad[j] ? OZ2_EXP_NONFINITE_DEV : (E == INT32_MIN ? OZ2_EXP_ZERO_DEV : E);
+        return;
+    }
     if (E == INT32_MIN) {
         e = 0;
     } else if (MODE == 0) {
@@ -542,7 +546,8 @@ void launch_cols_exponents(const double* B, int64_t k, int64_t n, int64_t ldb, i
     else cols_stats_kernel<1><<<grid, 32 * CS_WARPS, 0, st>>>(B, k, n, ldb, Ec, Sc, bad);
     unsigned g2 = (unsigned)((n + 255) / 256);
     if (mode == 0) cols_finalize_kernel<0><<<g2, 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, host_T(N), kstar, f);
-    else cols_finalize_kernel<1><<<g2, 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, host_T(N), kstar, f);
+    else if (mode == 1) cols_finalize_kernel<1><<<g2, 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, host_T(N), kstar, f);
+    else cols_finalize_kernel<2><<<g2, 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, host_T(N), kstar, f);
 }
 
 void launch_cols_residues(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f, int N,

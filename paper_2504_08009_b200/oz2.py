@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "liboz2.so")
 OK = 0
 MODE_FAST = 0
 MODE_EQ17 = 1
+MODE_ACCU = 2
 EXP_NONFINITE = -(2**31)
 MAX_K = 2**20          # oz2_modmul (raw int32 products): 2**17
 
@@ -29,6 +30,7 @@ SYMBOLS = [
     "oz2_scale_cols", "oz2_trunc_rows", "oz2_trunc_cols", "oz2_residues_rows", "oz2_residues_cols",
     "oz2_modmul", "oz2_crt", "oz2_tables", "oz2_eq17_k", "oz2_strerror", "oz2_version",
     "oz2_set_profiling", "oz2_stage_times", "oz2_dgemm_op", "oz2_dgemm_strided_batched",
+    "oz2_scale_accu",
 ]
 OP_N, OP_T = 0, 1
 # stage 0 times A's conversion (and B's too with OZ2_CONV_OVERLAP=1; the two column
@@ -74,6 +76,7 @@ def lib() -> ctypes.CDLL:
                                                         d, P, i64, i64, i64, i32]
                 L.oz2_scale_rows.argtypes = [P, i64, i64, P, i64, i32, P]
                 L.oz2_scale_cols.argtypes = [P, i64, i64, P, i64, i32, P]
+                L.oz2_scale_accu.argtypes = [P, i64, i64, i64, P, i64, P, i64, i32, P, P]
                 L.oz2_trunc_rows.argtypes = [P, i64, i64, P, i64, P, P]
                 L.oz2_trunc_cols.argtypes = [P, i64, i64, P, i64, P, P]
                 L.oz2_residues_rows.argtypes = [P, i64, i64, P, i64, P, i32, P, i64]
@@ -99,7 +102,7 @@ def _check(rc: int, what: str):
 def _mode_id(mode) -> int:
     if isinstance(mode, int):
         return mode
-    return {"fast": MODE_FAST, "eq17": MODE_EQ17}[mode.lower()]
+    return {"fast": MODE_FAST, "eq17": MODE_EQ17, "accu": MODE_ACCU}[mode.lower()]
 
 
 # ---------------------------------------------------------------------------
@@ -315,6 +318,23 @@ def scale_rows(A, N: int, mode="fast"):
     h.prepare(mode)
     _check(lib().oz2_scale_rows(h.ptr, m, k, _vp(A), _ld(A), N, _vp(e)), "oz2_scale_rows")
     return e
+
+
+def scale_accu(A, B, N: int):
+    """OS II-accu exponents (reading R18) of the product A B: (e, f)."""
+    import torch
+
+    A = _rowmajor(A, torch.float64)
+    B = _rowmajor(B, torch.float64)
+    m, k = A.shape
+    n = B.shape[1]
+    e = torch.empty(m, dtype=torch.int32, device=A.device)
+    f = torch.empty(n, dtype=torch.int32, device=A.device)
+    h = handle(A.device.index)
+    h.prepare("fast", workspace_bytes(m, n, k, 1))
+    _check(lib().oz2_scale_accu(h.ptr, m, n, k, _vp(A), _ld(A), _vp(B), _ld(B), N, _vp(e), _vp(f)),
+           "oz2_scale_accu")
+    return e, f
 
 
 def scale_cols(B, N: int, mode="fast"):

@@ -280,3 +280,31 @@ def test_gemm_strided_batched(oz2, oracle):
                                  transB=True).cpu().numpy()
     for i in range(3):
         assert_bitwise(C[i], oracle.gemm(A[i], B[i], 13, transB=True), f"batch item {i}")
+
+
+@pytest.mark.parametrize("N", [2, 8, 14, 16, 17, 20])
+def test_accu_exponents_and_dgemm(oz2, oracle, N):
+    """OS II-accu (reading R18): the line-1 exponents (bound GEMM on the tensor
+    cores, row/column maxima) and the whole product, bitwise vs the oracle."""
+    A = phi_matrix_np(301, 257, 4.0, seed=91)
+    B = phi_matrix_np(257, 515, 4.0, seed=92)
+    A[5, :] = 0.0
+    A[7, 3] = np.inf
+    B[:, 9] = 0.0
+    B[:, 11] *= 1e-310                                   # a subnormal column
+    e_ref, f_ref, _, _ = oracle.scale_accu(A, B, N)
+    e, f = oz2.scale_accu(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), N)
+    assert np.array_equal(e.cpu().numpy(), e_ref), "accu e"
+    assert np.array_equal(f.cpu().numpy(), f_ref), "accu f"
+    C = oz2.dgemm(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), N, mode="accu").cpu().numpy()
+    assert_bitwise(C, oracle.dgemm(A, B, N, oracle.MODE_ACCU), f"accu dgemm N={N}")
+
+
+def test_accu_transposed_operands(oz2, oracle):
+    Aop = phi_matrix_np(200, 300, 2.0, seed=93)
+    Bop = phi_matrix_np(300, 260, 2.0, seed=94)
+    C = oz2.gemm(torch.from_numpy(Aop.T.copy()).to(DEV), torch.from_numpy(Bop.T.copy()).to(DEV), 15,
+                 transA=True, transB=True, mode="accu").cpu().numpy()
+    assert_bitwise(C, oracle.dgemm(Aop, Bop, 15, oracle.MODE_ACCU), "accu transposed")
+    Ch = oz2.dgemm_host(Aop, Bop, 15, mode="accu")
+    assert_bitwise(Ch, C, "accu host path")
