@@ -46,6 +46,8 @@ def parse():
     p.add_argument("--k", type=int, default=None)
     p.add_argument("--moduli", type=int, default=14)
     p.add_argument("--phi", type=float, default=1.0)
+    p.add_argument("--mode", default="fast", choices=["fast", "accu", "eq17"],
+                   help="Alg. 1 line-1 rule: OS II-fast (headline), OS II-accu or Eq. (17)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-context", action="store_true")
@@ -140,10 +142,11 @@ def measured_peaks():
 # ---------------------------------------------------------------------------
 # CPU baseline / reference arm: the oracle on a bounded sample of the workload
 # ---------------------------------------------------------------------------
-def oracle_sample(A_rows: np.ndarray, B_cols: np.ndarray, N: int):
+def oracle_sample(A_rows: np.ndarray, B_cols: np.ndarray, N: int, mode: str = "fast"):
     import oracle
     t0 = time.perf_counter()
-    oracle.dgemm(A_rows, B_cols, N)
+    oracle.dgemm(A_rows, B_cols, N, {"fast": oracle.MODE_FAST, "eq17": oracle.MODE_EQ17,
+                                      "accu": oracle.MODE_ACCU}[mode])
     return time.perf_counter() - t0
 
 
@@ -196,7 +199,11 @@ def main():
                       "m_per_rank": m, "n": n, "k": k, "num_moduli": N, "phi": args.phi,
                       "parallelism": f"rowblock-dp{world}" if world > 1 else "single-gpu",
                       "l2": "no flush: every step streams A, B (2.1 GB each at n=16384) > 126 MB L2",
-                      "mode": "fast (OS II-fast, Cauchy-Schwarz)"}}
+                      "mode": {"fast": "fast (OS II-fast, Cauchy-Schwarz)",
+                               "accu": "accu (OS II-accu, INT8 bound GEMM)",
+                               "eq17": "eq17 (Eqs. 15-17)"}[args.mode]}}
+    if args.mode != "fast":
+        cfg["config"]["workload"] += f", {args.mode}"
     if args.impl == "reference":
         return run_reference(args, cfg)
 
@@ -222,10 +229,10 @@ def main():
     def step():
         if world > 1:
             # B broadcast from rank 0, local row block, C gathered to rank 0 (NCCL)
-            dgemm_rowblock(A, B, N, "fast", m_total=m * world,
+            dgemm_rowblock(A, B, N, args.mode, m_total=m * world,
                            local_fn=lambda a, b, nm, md: oz2.dgemm(a, b, nm, md, out=C))
         else:
-            oz2.dgemm(A, B, N, out=C)
+            oz2.dgemm(A, B, N, args.mode, out=C)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -309,7 +316,9 @@ def main():
             "stage_ms": {s: v / max(calls, 1) for s, v in stages.items()},
             "roofline": roofline,
             "n_scaled_roofline_frac": value / world / (4500.0 / N),
-            "gpu_launches": 5 * args.steps,   # rows, cols_stats, cols_finalize, cols_residues, modmul
+            # fast / eq17: rows, cols_stats, cols_finalize, cols_residues, modmul; accu adds
+            # rows_hat7, cols_stats, cols_finalize, cols_hat7, the bound GEMM and 2 finalizes
+            "gpu_launches": (10 if args.mode == "accu" else 5) * args.steps,
             "clocks": clk.summary()}
 
     # e2e: same metric through the C ABI with host buffers (pinned), copies timed
@@ -322,13 +331,13 @@ def main():
         del C
         torch.cuda.empty_cache()
         An, Bn, Cn = Ah.numpy(), Bh.numpy(), Ch.numpy()
-        oz2.dgemm_host(An, Bn, N, out=Cn)
+        oz2.dgemm_host(An, Bn, N, args.mode, out=Cn)
         steps_e2e = min(args.steps, 3)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(torch.cuda.current_stream())
         for _ in range(steps_e2e):
-            oz2.dgemm_host(An, Bn, N, out=Cn)
+            oz2.dgemm_host(An, Bn, N, args.mode, out=Cn)
         e1.record(torch.cuda.current_stream())
         torch.cuda.synchronize()
         ms_e2e = e0.elapsed_time(e1) / steps_e2e
@@ -375,7 +384,7 @@ def main():
         r, c = 64, 512
         Ar = A[:r].cpu().numpy()
         Bc = B[:, :c].cpu().numpy()
-        dt = oracle_sample(Ar, Bc, N)
+        dt = oracle_sample(Ar, Bc, N, args.mode)
         line["cpu_baseline"] = {"value": 2.0 * r * c * k / dt / 1e12, "unit": "TFLOPS",
                                 "cores": oracle.get_threads(), "kind": "oracle",
                                 "sample": f"rows 0..{r - 1} x cols 0..{c - 1} of the same product "

@@ -108,6 +108,14 @@ int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* 
 int oz2_dgemm_op(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, int64_t k,
                  double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
                  double beta, double* C, int64_t ldc, int num_moduli);
+/* Alg. 1 lines 2-10 with caller-supplied line-1 exponents e[m], f[n] (device
+ * int32, OZ2_EXP_NONFINITE allowed): C = D^-1 X E^-1.  For sharded line-1 rules
+ * (e.g. OS II-accu across row blocks, where f is a MIN all-reduce of the
+ * ranks' partial f).  The caller guarantees condition (13);
+ * otherwise X is not unique and C is undefined. */
+int oz2_dgemm_scaled(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A,
+                     int64_t lda, const double* B, int64_t ldb, const int32_t* e,
+                     const int32_t* f, double* C, int64_t ldc, int num_moduli);
 /* batch independent products: A + b*strideA, B + b*strideB, C + b*strideC
  * (elements), b = 0..batch-1, in stream order on one workspace. */
 int oz2_dgemm_strided_batched(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n,

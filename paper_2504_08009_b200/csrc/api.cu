@@ -539,11 +539,14 @@ int accu_line1(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
 // op(A) = A^T means the stored A is k x m: its "rows of op(A)" are the columns
 // of the stored matrix, so the column kernels produce e and the K-major planes;
 // likewise op(B) = B^T (stored n x k) goes through the row kernel.
+// e_given / f_given (both or neither): caller-supplied line-1 exponents (lines 2-10 only).
 int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
-               int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int N) {
+               int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int N,
+               const int32_t* e_given = nullptr, const int32_t* f_given = nullptr) {
     if (m == 0 || n == 0) return OZ2_OK;
+    const bool given = e_given && f_given;
     int rc, kstar = 0;
-    if (k > 0 && alpha != 0.0 && (rc = kstar_for(h, N, k, &kstar))) return rc;
+    if (!given && k > 0 && alpha != 0.0 && (rc = kstar_for(h, N, k, &kstar))) return rc;
     DevGuard g(h->device);
     if (k == 0 || alpha == 0.0) {                     // no product: C = beta C (0 if beta == 0)
         if (beta == 1.0) return OZ2_OK;
@@ -555,8 +558,8 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     if ((rc = get_workspace(h, L.total, &ws))) return rc;
     int8_t* Ares = (int8_t*)(ws + L.off_Ares);
     int8_t* Bres = (int8_t*)(ws + L.off_Bres);
-    int32_t* e = (int32_t*)(ws + L.off_e);
-    int32_t* f = (int32_t*)(ws + L.off_f);
+    int32_t* e = given ? const_cast<int32_t*>(e_given) : (int32_t*)(ws + L.off_e);
+    int32_t* f = given ? const_cast<int32_t*>(f_given) : (int32_t*)(ws + L.off_f);
     uint8_t* scratch = ws + L.off_scratch;
     CUtensorMap tA, tB;
     if ((rc = make_plane_map(&tA, Ares, m, k, L.ldr, N, 128))) return rc;
@@ -564,18 +567,20 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     // Part 1 + 2-a (Alg. 1 lines 1-5) for op(A) and op(B).  With the accu rule
     // the exponents come first from both operands (accu_line1, timed in stage
     // ROWS), and the conversions below only form the residues.
-    const bool accu = h->mode == OZ2_MODE_ACCU;
-    const int what = accu ? 2 : 3;
+    const bool accu = h->mode == OZ2_MODE_ACCU && !given;
+    const bool skip_line1 = accu || given;              // e, f known before the residue passes
+    const int what = skip_line1 ? 2 : 3;
     auto convert_A = [&](cudaStream_t st) {
         if (ta == OZ2_OP_N) {
             oz2::launch_rows(A, m, k, lda, N, what, h->mode, kstar, e, Ares, L.ldr, st);
         } else {
-            if (!accu) oz2::launch_cols_exponents(A, k, m, lda, N, h->mode, kstar, e, ws + L.off_stats, st);
+            if (!skip_line1) oz2::launch_cols_exponents(A, k, m, lda, N, h->mode, kstar, e, ws + L.off_stats, st);
             oz2::launch_cols_residues(A, k, m, lda, e, N, Ares, L.ldr, st);
         }
     };
     auto convert_B_stats = [&](cudaStream_t st) {
-        if (tb == OZ2_OP_N && !accu) oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, st);
+        if (tb == OZ2_OP_N && !skip_line1)
+            oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, st);
     };
     auto convert_B_res = [&](cudaStream_t st) {
         if (tb == OZ2_OP_N) oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, st);
@@ -587,7 +592,7 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     // stream concurrently with A's (stage ROWS then times both, the column stages
     // read 0).  Default off: measured no gain, both passes are issue-bound.  (Not
     // with op(A) = A^T, whose column statistics share B's scratch.)
-    const bool overlap = env_flag("OZ2_CONV_OVERLAP", 0) && ta == OZ2_OP_N && !accu;
+    const bool overlap = env_flag("OZ2_CONV_OVERLAP", 0) && ta == OZ2_OP_N && !skip_line1;
     if (overlap) {
         if ((rc = ensure_aux(h))) return rc;
         cudaEventRecord(h->ev_fork, h->stream);
@@ -636,6 +641,16 @@ int oz2_dgemm_op(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, i
     int rc = check_op_args(transA, transB, m, n, k, A, lda, B, ldb, C, ldc, N);
     if (rc) return rc;
     return dgemm_core(h, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, N);
+}
+
+int oz2_dgemm_scaled(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                     const double* B, int64_t ldb, const int32_t* e, const int32_t* f, double* C, int64_t ldc,
+                     int N) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_op_args(OZ2_OP_N, OZ2_OP_N, m, n, k, A, lda, B, ldb, C, ldc, N);
+    if (rc) return rc;
+    if (m > 0 && n > 0 && k > 0 && (!e || !f)) return OZ2_ERR_INVALID_ARG;
+    return dgemm_core(h, OZ2_OP_N, OZ2_OP_N, m, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldc, N, e, f);
 }
 
 int oz2_dgemm_strided_batched(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, int64_t k,

@@ -22,7 +22,7 @@ def row_partition(m: int, world: int, rank: int) -> tuple[int, int]:
 
 def dgemm_rowblock(A_local, B, num_moduli: int = 14, mode: str = "fast", group=None, src: int = 0,
                    gather_to: Optional[int] = 0, m_total: Optional[int] = None,
-                   local_fn: Optional[Callable] = None):
+                   local_fn: Optional[Callable] = None, accu_fns: Optional[tuple] = None):
     """C = A B with A sharded by rows.
 
     A_local: this rank's rows of A (rows `row_partition(m_total, world, rank)`).
@@ -33,6 +33,14 @@ def dgemm_rowblock(A_local, B, num_moduli: int = 14, mode: str = "fast", group=N
 
     local_fn(A_local, B, num_moduli, mode) computes the local block; the default
     is the CUDA library (paper_2504_08009_b200.oz2.dgemm).
+
+    mode "accu" (OS II-accu, reading R18): e_i needs row i and all of B (local),
+    but f_j needs the bound P over ALL rows.  Each rank computes its partial f
+    from its rows; since f_j = h_j - F_j with F_j common to all ranks and h_j
+    non-increasing in max_i P_ij, the global f is the element-wise MIN over the
+    ranks (one n-element int32 all-reduce) -- bit-identical to one GPU.
+    accu_fns = (scale_fn(A_local, B, N) -> (e, f_partial), scaled_fn(A_local, B,
+    e, f, N) -> C_local) replaces the CUDA library (oz2.scale_accu / dgemm_scaled).
     """
     import torch
     import torch.distributed as dist
@@ -43,7 +51,16 @@ def dgemm_rowblock(A_local, B, num_moduli: int = 14, mode: str = "fast", group=N
         from . import oz2
         local_fn = oz2.dgemm
     dist.broadcast(B, src=src, group=group)
-    C_local = local_fn(A_local, B, num_moduli, mode)
+    if mode == "accu":
+        if accu_fns is None:
+            from . import oz2
+            accu_fns = (oz2.scale_accu, oz2.dgemm_scaled)
+        scale_fn, scaled_fn = accu_fns
+        e, f = scale_fn(A_local, B, num_moduli)
+        dist.all_reduce(f, op=dist.ReduceOp.MIN, group=group)
+        C_local = scaled_fn(A_local, B, e, f, num_moduli)
+    else:
+        C_local = local_fn(A_local, B, num_moduli, mode)
     if gather_to is None:
         return C_local, None
     if m_total is None:

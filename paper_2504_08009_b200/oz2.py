@@ -30,7 +30,7 @@ SYMBOLS = [
     "oz2_scale_cols", "oz2_trunc_rows", "oz2_trunc_cols", "oz2_residues_rows", "oz2_residues_cols",
     "oz2_modmul", "oz2_crt", "oz2_tables", "oz2_eq17_k", "oz2_strerror", "oz2_version",
     "oz2_set_profiling", "oz2_stage_times", "oz2_dgemm_op", "oz2_dgemm_strided_batched",
-    "oz2_scale_accu",
+    "oz2_scale_accu", "oz2_dgemm_scaled",
 ]
 OP_N, OP_T = 0, 1
 # stage 0 times A's conversion (and B's too with OZ2_CONV_OVERLAP=1; the two column
@@ -77,6 +77,7 @@ def lib() -> ctypes.CDLL:
                 L.oz2_scale_rows.argtypes = [P, i64, i64, P, i64, i32, P]
                 L.oz2_scale_cols.argtypes = [P, i64, i64, P, i64, i32, P]
                 L.oz2_scale_accu.argtypes = [P, i64, i64, i64, P, i64, P, i64, i32, P, P]
+                L.oz2_dgemm_scaled.argtypes = [P, i64, i64, i64, P, i64, P, i64, P, P, P, i64, i32]
                 L.oz2_trunc_rows.argtypes = [P, i64, i64, P, i64, P, P]
                 L.oz2_trunc_cols.argtypes = [P, i64, i64, P, i64, P, P]
                 L.oz2_residues_rows.argtypes = [P, i64, i64, P, i64, P, i32, P, i64]
@@ -236,6 +237,24 @@ def dgemm(A, B, num_moduli: int = 14, mode="fast", out=None):
     h.prepare(mode, workspace_bytes(m, n, k, num_moduli))
     _check(lib().oz2_dgemm_ex(h.ptr, m, n, k, _vp(A), _ld(A), _vp(B), _ld(B), _vp(C), _ld(C),
                               num_moduli), "oz2_dgemm_ex")
+    return C
+
+
+def dgemm_scaled(A, B, e, f, num_moduli: int = 14, out=None):
+    """Alg. 1 lines 2-10 with given exponent vectors e (rows of A), f (columns of B)."""
+    import torch
+
+    A = _rowmajor(A, torch.float64)
+    B = _rowmajor(B, torch.float64)
+    m, k = A.shape
+    n = B.shape[1]
+    e = e.to(device=A.device, dtype=torch.int32).contiguous()
+    f = f.to(device=A.device, dtype=torch.int32).contiguous()
+    C = out if out is not None else torch.empty((m, n), dtype=torch.float64, device=A.device)
+    h = handle(A.device.index)
+    h.prepare("fast", workspace_bytes(m, n, k, num_moduli))
+    _check(lib().oz2_dgemm_scaled(h.ptr, m, n, k, _vp(A), _ld(A), _vp(B), _ld(B), _vp(e), _vp(f), _vp(C), _ld(C),
+                                  num_moduli), "oz2_dgemm_scaled")
     return C
 
 

@@ -44,6 +44,54 @@ def _oracle_local(A_local, B, N, mode):
     return torch.from_numpy(C)
 
 
+def _oracle_scale_accu(A_local, B, N):
+    import oracle
+    e, f, _, _ = oracle.scale_accu(A_local.numpy(), B.numpy(), N)
+    return torch.from_numpy(e), torch.from_numpy(f)
+
+
+def _oracle_scaled(A_local, B, e, f, N):
+    import oracle
+    e, f = e.numpy(), f.numpy()
+    Ap = oracle.trunc_rows(A_local.numpy(), e)
+    BpT = oracle.trunc_cols(B.numpy(), f)
+    Cp = oracle.modmul(oracle.residues(Ap, N), oracle.residues(BpT, N))
+    return torch.from_numpy(oracle.crt(Cp, e, f))
+
+
+def _worker_accu(rank, world, port, m, n, k, N, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = phi_matrix_np(m, k, 4.0, seed=7)
+        r0, r1 = row_partition(m, world, rank)
+        A_local = torch.from_numpy(A[r0:r1].copy())
+        B = torch.from_numpy(phi_matrix_np(k, n, 4.0, seed=8)) if rank == 0 else torch.empty((k, n), dtype=torch.float64)
+        _, C_full = dgemm_rowblock(A_local, B, N, "accu", m_total=m, accu_fns=(_oracle_scale_accu, _oracle_scaled))
+        if rank == 0:
+            np.save(out_path, C_full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rowblock_accu_gloo_world2(tmp_path, oracle):
+    """OS II-accu sharded by rows: the MIN all-reduce of the partial f reproduces
+    the single-process accu exponents, so C is bit-identical (reading R18)."""
+    m, n, k, N = 40, 23, 200, 16
+    out = str(tmp_path / "Ca.npy")
+    mp.spawn(_worker_accu, args=(2, _free_port(), m, n, k, N, out), nprocs=2, join=True)
+    C = np.load(out)
+    A = phi_matrix_np(m, k, 4.0, seed=7)
+    B = phi_matrix_np(k, n, 4.0, seed=8)
+    ref = oracle.dgemm(A, B, N, oracle.MODE_ACCU)
+    assert np.array_equal(C.view(np.int64), ref.view(np.int64))
+    # and the sharding matters: rank 0's rows alone give a different (larger) f somewhere
+    _, f_full, _, _ = oracle.scale_accu(A, B, N)
+    _, f_half, _, _ = oracle.scale_accu(A[:20], B, N)
+    assert np.all(f_half >= f_full)
+
+
 def _worker(rank, world, port, m, n, k, N, out_path):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)

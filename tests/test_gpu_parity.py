@@ -308,3 +308,20 @@ def test_accu_transposed_operands(oz2, oracle):
     assert_bitwise(C, oracle.dgemm(Aop, Bop, 15, oracle.MODE_ACCU), "accu transposed")
     Ch = oz2.dgemm_host(Aop, Bop, 15, mode="accu")
     assert_bitwise(Ch, C, "accu host path")
+
+
+def test_dgemm_scaled_and_sharded_accu(oz2, oracle):
+    """oz2_dgemm_scaled with given exponents, and the row-sharded accu recipe of
+    dist.dgemm_rowblock (partial f, element-wise MIN) on one GPU, bitwise."""
+    A = phi_matrix_np(400, 300, 4.0, seed=95)
+    B = phi_matrix_np(300, 270, 4.0, seed=96)
+    Ad, Bd = torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV)
+    ref = oracle.dgemm(A, B, 16, oracle.MODE_ACCU)
+    e, f, _, _ = oracle.scale_accu(A, B, 16)
+    C = oz2.dgemm_scaled(Ad, Bd, torch.from_numpy(e), torch.from_numpy(f), 16).cpu().numpy()
+    assert_bitwise(C, ref, "dgemm_scaled with oracle accu exponents")
+    parts = [(0, 130), (130, 400)]
+    ef = [oz2.scale_accu(Ad[a:b], Bd, 16) for a, b in parts]
+    fmin = torch.minimum(ef[0][1], ef[1][1])
+    Cs = torch.cat([oz2.dgemm_scaled(Ad[a:b], Bd, ef[i][0], fmin, 16) for i, (a, b) in enumerate(parts)])
+    assert_bitwise(Cs.cpu().numpy(), ref, "row-sharded accu (MIN of partial f)")
