@@ -444,15 +444,24 @@ cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t
         }
     }
     __syncthreads();
-    // write out: 16 lanes per (t, col) row segment of 64 bytes, 2 segments per warp store
-    const int sub = lane >> 4, wl = lane & 15;
-    for (int rowi = 2 * warp + sub; rowi < NM * 32; rowi += 16) {
+    // write out: 4 threads per (t, col) row segment of 64 bytes, 16 bytes each
+    // (64 segments per pass of the block); the two 8-byte chunks of a 16-byte
+    // piece sit side by side in smem (XOR swizzle keeps pairs), swapped when
+    // (col & 7) is odd
+    const int piece = threadIdx.x & 3;
+    for (int rowi = threadIdx.x >> 2; rowi < NM * 32; rowi += 64) {
         const int t = rowi >> 5, col = rowi & 31;
         if (j0 + col >= n) continue;
-        const int ch = (wl >> 1) ^ (col & 7);
-        const uint32_t v = *reinterpret_cast<const uint32_t*>(sres + (size_t)rowi * 64 + ch * 8 + (wl & 1) * 4);
-        if (l0 + 4 * wl < ldr)                               // stay inside the plane row (ld_res)
-            *reinterpret_cast<uint32_t*>(out + (int64_t)t * n * ldr + (j0 + col) * ldr + l0 + 4 * wl) = v;
+        const int sw = col & 7;
+        const uint4 v = *reinterpret_cast<const uint4*>(sres + (size_t)rowi * 64 + (((2 * piece) ^ sw) >> 1) * 16);
+        const uint4 o = (sw & 1) ? make_uint4(v.z, v.w, v.x, v.y) : v;
+        const int64_t l = l0 + 16 * piece;
+        int8_t* dst = out + (int64_t)t * n * ldr + (j0 + col) * ldr + l;
+        if (l + 16 <= ldr) {
+            *reinterpret_cast<uint4*>(dst) = o;
+        } else if (l < ldr) {                                // ldr % 16 == 0: never partial
+            *reinterpret_cast<uint2*>(dst) = make_uint2(o.x, o.y);
+        }
     }
 }
 
