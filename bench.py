@@ -41,7 +41,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="oz2", choices=["oz2", "reference"])
-    p.add_argument("--n", type=int, default=16384)
+    p.add_argument("--n", "--size", dest="n", type=int, default=16384)
     p.add_argument("--m", type=int, default=None, help="rows per rank (default n)")
     p.add_argument("--k", type=int, default=None)
     p.add_argument("--moduli", type=int, default=14)
@@ -49,6 +49,9 @@ def parse():
     p.add_argument("--mode", default="fast", choices=["fast", "accu", "eq17"],
                    help="Alg. 1 line-1 rule: OS II-fast (headline), OS II-accu or Eq. (17)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    p.add_argument("--chunks", type=int, default=0, help="multi-GPU gather pipeline pieces (0: auto)")
+    p.add_argument("--reserve-sms", type=int, default=8, help="SMs left to NCCL when chunks > 1")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-context", action="store_true")
     p.add_argument("--acc-samples", type=int, default=256)
@@ -198,6 +201,7 @@ def main():
                       f"m={m}, n={n}, k={k}, N={N}, phi={args.phi:g}",
                       "m_per_rank": m, "n": n, "k": k, "num_moduli": N, "phi": args.phi,
                       "parallelism": f"rowblock-dp{world}" if world > 1 else "single-gpu",
+                      "gather": "rank 0, NCCL, pipelined in row pieces" if world > 1 else None,
                       "l2": "no flush: every step streams A, B (2.1 GB each at n=16384) > 126 MB L2",
                       "mode": {"fast": "fast (OS II-fast, Cauchy-Schwarz)",
                                "accu": "accu (OS II-accu, INT8 bound GEMM)",
@@ -212,10 +216,17 @@ def main():
     from paper_2504_08009_b200 import oz2
     from paper_2504_08009_b200.inputs import phi_matrix_torch, SEED_A, SEED_B
 
+    if args.dist_backend == "gloo":
+        local = 0                                   # functional check: every rank on cuda:0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # --dist-backend gloo: two ranks on ONE GPU (a functional check of the
+        # multi-GPU path on a 1-GPU box; NCCL refuses duplicate devices)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     # inputs resident in HBM before the timed region
     A = phi_matrix_torch(m, k, args.phi, SEED_A, device=dev, row_offset=rank * m)
@@ -226,11 +237,17 @@ def main():
 
     from paper_2504_08009_b200.dist import dgemm_rowblock
 
+    # multi-GPU: B converted once per step (B-stationary), the local rows in
+    # `chunks` pieces whose NCCL gathers overlap the next piece's GEMM on SMs
+    # left free by the GEMM's SM budget (at 4+ GPUs, where the gather is large)
+    chunks = args.chunks if args.chunks else (4 if world >= 4 else 1)
+    if world > 1 and chunks > 1:
+        oz2.set_sm_limit(torch.cuda.get_device_properties(dev).multi_processor_count - args.reserve_sms, local)
+
     def step():
         if world > 1:
             # B broadcast from rank 0, local row block, C gathered to rank 0 (NCCL)
-            dgemm_rowblock(A, B, N, args.mode, m_total=m * world,
-                           local_fn=lambda a, b, nm, md: oz2.dgemm(a, b, nm, md, out=C))
+            dgemm_rowblock(A, B, N, args.mode, m_total=m * world, chunks=chunks, C_local=C)
         else:
             oz2.dgemm(A, B, N, args.mode, out=C)
 

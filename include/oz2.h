@@ -116,6 +116,22 @@ int oz2_dgemm_op(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, i
 int oz2_dgemm_scaled(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A,
                      int64_t lda, const double* B, int64_t ldb, const int32_t* e,
                      const int32_t* f, double* C, int64_t ldc, int num_moduli);
+/* B-stationary products: oz2_prepare_b converts B (k x n) once into
+ * handle-owned device memory (Alg. 1 lines 1, 3, 5 for B: f and the residue
+ * planes); each oz2_dgemm_prepared(m, A, C) then runs lines 1, 2, 4 for A and
+ * 6-10 against it -- bit-identical to oz2_dgemm_ex(A, B), since e_i depends on
+ * row i of A only and f_j on column j of B only (FAST / EQ17; ACCU couples the
+ * operands and is rejected).  Used by the row-block pipelines (one B, many row
+ * blocks of A).  Valid until the next oz2_prepare_b or oz2_release_b; the
+ * handle's mode must not change in between. */
+int oz2_prepare_b(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb,
+                  int num_moduli);
+int oz2_dgemm_prepared(oz2_handle_t h, int64_t m, const double* A, int64_t lda, double* C,
+                       int64_t ldc);
+int oz2_release_b(oz2_handle_t h);
+/* Limit the persistent GEMM to `sms` SMs (0 = all; rounded down to even), e.g.
+ * to leave SMs to NCCL kernels that overlap it.  Results do not depend on it. */
+int oz2_set_sm_limit(oz2_handle_t h, int sms);
 /* batch independent products: A + b*strideA, B + b*strideB, C + b*strideC
  * (elements), b = 0..batch-1, in stream order on one workspace. */
 int oz2_dgemm_strided_batched(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n,

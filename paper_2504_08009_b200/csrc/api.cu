@@ -94,7 +94,21 @@ struct oz2_context {
     // B's conversion runs on s_aux concurrently with A's (fork / join events)
     cudaStream_t s_aux;
     cudaEvent_t ev_fork, ev_join;
+    int sm_limit;                      // 0 = all SMs; else the persistent GEMM's SM budget
+    // B-stationary products (oz2_prepare_b): f and B's residue planes, owned here
+    void* bprep;
+    size_t bprep_bytes;
+    int bprep_valid, bprep_N, bprep_mode;
+    int64_t bprep_k, bprep_n, bprep_ldr;
 };
+
+namespace {
+// SMs the persistent GEMM may use (even: CTA pairs)
+inline int gemm_sms(const oz2_context* h) {
+    const int s = h->sm_limit > 0 && h->sm_limit < h->num_sms ? h->sm_limit : h->num_sms;
+    return s & ~1;
+}
+}  // namespace
 
 namespace {
 // stage boundary marker (profiling only): one event per boundary, no sync
@@ -122,13 +136,14 @@ struct Layout {
     size_t total;
 };
 
-Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms, int64_t stats_cols = -1) {
+Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms, int64_t stats_cols = -1,
+                  bool with_B = true) {
     Layout L;
     L.ldr = round_up(k > 0 ? k : 1, 16);
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = (size_t)round_up((int64_t)(off + bytes), 256); return o; };
     L.off_Ares = take((size_t)N * (size_t)m * (size_t)L.ldr);
-    L.off_Bres = take((size_t)N * (size_t)n * (size_t)L.ldr);
+    L.off_Bres = take(with_B ? (size_t)N * (size_t)n * (size_t)L.ldr : 0);
     L.off_e = take(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));
     L.off_f = take(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
     L.off_stats = take(oz2::cols_stats_bytes(k, stats_cols >= 0 ? stats_cols : n));
@@ -297,6 +312,7 @@ int oz2_destroy(oz2_handle_t h) {
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->ws_own) cudaFree(h->ws_own);
+    if (h->bprep) cudaFree(h->bprep);
     delete h;
     return OZ2_OK;
 }
@@ -317,6 +333,12 @@ int oz2_set_workspace(oz2_handle_t h, void* ptr, size_t bytes) {
     if (!h) return OZ2_ERR_INVALID_ARG;
     h->ws_user = ptr;
     h->ws_user_bytes = ptr ? bytes : 0;
+    return OZ2_OK;
+}
+
+int oz2_set_sm_limit(oz2_handle_t h, int sms) {
+    if (!h || sms < 0) return OZ2_ERR_INVALID_ARG;
+    h->sm_limit = sms;
     return OZ2_OK;
 }
 
@@ -403,7 +425,7 @@ int oz2_scale_accu(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
         if (n > 0) cudaMemsetAsync(f, 0, sizeof(int32_t) * (size_t)n, h->stream);
         return cuda_status();
     }
-    Layout L = layout_for(m, n, k, 1, h->num_sms);
+    Layout L = layout_for(m, n, k, 1, gemm_sms(h));
     uint8_t* ws;
     if ((rc = get_workspace(h, L.total, &ws))) return rc;
     return accu_line1(h, OZ2_OP_N, OZ2_OP_N, m, n, k, A, lda, B, ldb, N, ws, L, e, f);
@@ -465,7 +487,7 @@ int oz2_modmul(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const int8_t* Ar
     if ((rc = make_plane_map(&tB, Bres, n, k, ld_res, N, 256 / oz2::gemm_cta_group()))) return rc;
     uint8_t* ws;
     if ((rc = get_workspace(h, 256, &ws))) return rc;
-    if (oz2::launch_modmul(&tA, &tB, m, n, k, N, Cprod, (uint32_t*)ws, h->num_sms, h->stream)) return OZ2_ERR_CUDA;
+    if (oz2::launch_modmul(&tA, &tB, m, n, k, N, Cprod, (uint32_t*)ws, gemm_sms(h), h->stream)) return OZ2_ERR_CUDA;
     return cuda_status();
 }
 
@@ -528,7 +550,7 @@ int accu_line1(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     int rc;
     if ((rc = make_plane_map(&tA, (const int8_t*)Ah, m, k, L.ldr, 1, 128))) return rc;
     if ((rc = make_plane_map(&tB, (const int8_t*)Bh, n, k, L.ldr, 1, 256 / oz2::gemm_cta_group()))) return rc;
-    if (oz2::launch_bound_gemm(&tA, &tB, m, n, k, pr, pc, (uint32_t*)(ws + L.off_sync), h->num_sms, h->stream))
+    if (oz2::launch_bound_gemm(&tA, &tB, m, n, k, pr, pc, (uint32_t*)(ws + L.off_sync), gemm_sms(h), h->stream))
         return OZ2_ERR_CUDA;
     oz2::launch_accu_finalize(E, pr, m, N, e, h->stream);
     oz2::launch_accu_finalize(F, pc, n, N, f, h->stream);
@@ -553,7 +575,7 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
         oz2::launch_scale_c(C, m, n, ldc, beta, h->stream);
         return cuda_status();
     }
-    Layout L = layout_for(m, n, k, N, h->num_sms, ta == OZ2_OP_T ? std::max(m, n) : n);
+    Layout L = layout_for(m, n, k, N, gemm_sms(h), ta == OZ2_OP_T ? std::max(m, n) : n);
     uint8_t* ws;
     if ((rc = get_workspace(h, L.total, &ws))) return rc;
     int8_t* Ares = (int8_t*)(ws + L.off_Ares);
@@ -615,7 +637,7 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     }
     // Part 2-b (line 6) with Parts 2-c, 3, 4 (lines 7-10) fused into the epilogue
     if (oz2::launch_modmul_fused(&tA, &tB, m, n, k, N, scratch, e, f, C, ldc, (uint32_t*)(ws + L.off_sync),
-                                 h->num_sms, h->stream, alpha, beta))
+                                 gemm_sms(h), h->stream, alpha, beta))
         return OZ2_ERR_CUDA;
     mark(h);
     mark(h);                                          // (no separate CRT stage)
@@ -641,6 +663,81 @@ int oz2_dgemm_op(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, i
     int rc = check_op_args(transA, transB, m, n, k, A, lda, B, ldb, C, ldc, N);
     if (rc) return rc;
     return dgemm_core(h, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, N);
+}
+
+int oz2_prepare_b(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb, int N) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(1, n, k, N);
+    if (rc) return rc;
+    if (h->mode == OZ2_MODE_ACCU) return OZ2_ERR_INVALID_ARG;        // accu couples A and B
+    if (ldb < (n > 0 ? n : 1) || (k > 0 && n > 0 && !B)) return OZ2_ERR_INVALID_ARG;
+    int kstar = 0;
+    if (k > 0 && (rc = kstar_for(h, N, k, &kstar))) return rc;
+    DevGuard g(h->device);
+    const int64_t ldr = round_up(k > 0 ? k : 1, 16);
+    const size_t off_planes = (size_t)round_up((int64_t)sizeof(int32_t) * (n > 0 ? n : 1), 256);
+    const size_t off_stats = (size_t)round_up((int64_t)(off_planes + (size_t)N * (size_t)n * (size_t)ldr), 256);
+    const size_t total = off_stats + oz2::cols_stats_bytes(k, n);
+    if (h->bprep_bytes < total) {
+        if (h->bprep) { cudaStreamSynchronize(h->stream); cudaFree(h->bprep); h->bprep = nullptr; h->bprep_bytes = 0; }
+        if (cudaMalloc(&h->bprep, total) != cudaSuccess) return OZ2_ERR_CUDA;
+        h->bprep_bytes = total;
+    }
+    uint8_t* base = (uint8_t*)h->bprep;
+    int32_t* f = (int32_t*)base;
+    if (k > 0 && n > 0) {
+        oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, base + off_stats, h->stream);
+        oz2::launch_cols_residues(B, k, n, ldb, f, N, (int8_t*)(base + off_planes), ldr, h->stream);
+    }
+    h->bprep_valid = 1; h->bprep_N = N; h->bprep_mode = h->mode;
+    h->bprep_k = k; h->bprep_n = n; h->bprep_ldr = ldr;
+    return cuda_status();
+}
+
+int oz2_release_b(oz2_handle_t h) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    h->bprep_valid = 0;
+    return OZ2_OK;
+}
+
+int oz2_dgemm_prepared(oz2_handle_t h, int64_t m, const double* A, int64_t lda, double* C, int64_t ldc) {
+    if (!h || !h->bprep_valid || h->mode != h->bprep_mode) return OZ2_ERR_INVALID_ARG;
+    const int64_t k = h->bprep_k, n = h->bprep_n;
+    const int N = h->bprep_N;
+    int rc = check_common(m, n, k, N);
+    if (rc) return rc;
+    if (lda < (k > 0 ? k : 1) || ldc < (n > 0 ? n : 1) || (m > 0 && n > 0 && (!C || (k > 0 && !A))))
+        return OZ2_ERR_INVALID_ARG;
+    if (m == 0 || n == 0) return OZ2_OK;
+    DevGuard g(h->device);
+    if (k == 0) {
+        oz2::launch_scale_c(C, m, n, ldc, 0.0, h->stream);
+        return cuda_status();
+    }
+    int kstar = 0;
+    if ((rc = kstar_for(h, N, k, &kstar))) return rc;
+    Layout L = layout_for(m, n, k, N, gemm_sms(h), 0, false);
+    uint8_t* ws;
+    if ((rc = get_workspace(h, L.total, &ws))) return rc;
+    int8_t* Ares = (int8_t*)(ws + L.off_Ares);
+    int32_t* e = (int32_t*)(ws + L.off_e);
+    uint8_t* base = (uint8_t*)h->bprep;
+    const int32_t* f = (const int32_t*)base;
+    const int8_t* Bres = (const int8_t*)(base + (size_t)round_up((int64_t)sizeof(int32_t) * n, 256));
+    CUtensorMap tA, tB;
+    if ((rc = make_plane_map(&tA, Ares, m, k, L.ldr, N, 128))) return rc;
+    if ((rc = make_plane_map(&tB, Bres, n, k, h->bprep_ldr, N, 256 / oz2::gemm_cta_group()))) return rc;
+    mark(h);
+    oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
+    mark(h);
+    mark(h);
+    mark(h);
+    if (oz2::launch_modmul_fused(&tA, &tB, m, n, k, N, ws + L.off_scratch, e, f, C, ldc,
+                                 (uint32_t*)(ws + L.off_sync), gemm_sms(h), h->stream))
+        return OZ2_ERR_CUDA;
+    mark(h);
+    mark(h);
+    return cuda_status();
 }
 
 int oz2_dgemm_scaled(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
@@ -700,7 +797,7 @@ int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
     }
     if (h->mode == OZ2_MODE_ACCU) {
         // f depends on every row of A under the accu rule: no row-block pipeline
-        Layout L = layout_for(m, n, k, N, h->num_sms, std::max(m, n));
+        Layout L = layout_for(m, n, k, N, gemm_sms(h), std::max(m, n));
         const size_t offA = (size_t)round_up((int64_t)L.total, 256);
         const size_t offB = (size_t)round_up((int64_t)(offA + sizeof(double) * (size_t)m * k), 256);
         const size_t offC = (size_t)round_up((int64_t)(offB + sizeof(double) * (size_t)k * n), 256);
@@ -734,7 +831,7 @@ int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
     const int64_t R = std::max<int64_t>(1, std::min<int64_t>(8, m / 4096));
     const int64_t mb = round_up((m + R - 1) / R, 256);
     const int64_t nblk = (m + mb - 1) / mb;
-    Layout L = layout_for(mb, n, k, N, h->num_sms);          // A planes and e for one row block
+    Layout L = layout_for(mb, n, k, N, gemm_sms(h));          // A planes and e for one row block
     const size_t bytesA = sizeof(double) * (size_t)m * (size_t)k;
     const size_t bytesB = sizeof(double) * (size_t)k * (size_t)n;
     const size_t bytesC = sizeof(double) * (size_t)m * (size_t)n;
@@ -791,7 +888,7 @@ int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
         CUtensorMap tA;
         if ((rc = make_plane_map(&tA, Ares, rows, k, L.ldr, N, 128))) return rc;
         if (oz2::launch_modmul_fused(&tA, &tB, rows, n, k, N, ws + L.off_scratch, e, f, dC + r0 * n, n,
-                                     (uint32_t*)(ws + L.off_sync), h->num_sms, h->stream))
+                                     (uint32_t*)(ws + L.off_sync), gemm_sms(h), h->stream))
             return OZ2_ERR_CUDA;
         cudaEventRecord(evC[b], h->stream);
         cudaStreamWaitEvent(h->s_d2h, evC[b], 0);

@@ -22,7 +22,8 @@ def row_partition(m: int, world: int, rank: int) -> tuple[int, int]:
 
 def dgemm_rowblock(A_local, B, num_moduli: int = 14, mode: str = "fast", group=None, src: int = 0,
                    gather_to: Optional[int] = 0, m_total: Optional[int] = None,
-                   local_fn: Optional[Callable] = None, accu_fns: Optional[tuple] = None):
+                   local_fn: Optional[Callable] = None, accu_fns: Optional[tuple] = None,
+                   chunks: int = 1, C_local=None):
     """C = A B with A sharded by rows.
 
     A_local: this rank's rows of A (rows `row_partition(m_total, world, rank)`).
@@ -31,8 +32,15 @@ def dgemm_rowblock(A_local, B, num_moduli: int = 14, mode: str = "fast", group=N
     Returns (C_local, C_full): C_full is the gathered m_total x n result on rank
     `gather_to` (None elsewhere, or everywhere when gather_to is None).
 
-    local_fn(A_local, B, num_moduli, mode) computes the local block; the default
-    is the CUDA library (paper_2504_08009_b200.oz2.dgemm).
+    local_fn(A_rows, B, num_moduli, mode) computes a block of rows; the default
+    is the CUDA library: B is converted once (oz2.PreparedB, B-stationary) and
+    every chunk of rows is one oz2_dgemm_prepared call.
+
+    chunks > 1 pipelines the gather: the rows of every rank are cut into
+    `chunks` pieces; piece c's gather (an asynchronous NCCL collective) runs
+    while piece c + 1 computes, so only the last piece's transfer is exposed.
+    (The caller leaves SMs to NCCL with oz2.set_sm_limit; results are
+    bit-identical for any chunking.)
 
     mode "accu" (OS II-accu, reading R18): e_i needs row i and all of B (local),
     but f_j needs the bound P over ALL rows.  Each rank computes its partial f
@@ -47,42 +55,88 @@ def dgemm_rowblock(A_local, B, num_moduli: int = 14, mode: str = "fast", group=N
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    if local_fn is None:
-        from . import oz2
-        local_fn = oz2.dgemm
-    dist.broadcast(B, src=src, group=group)
+    # gloo (CPU tests, or several ranks on one GPU as a functional check) moves
+    # CUDA tensors through host copies; NCCL takes them directly
+    host_coll = dist.get_backend(group) == "gloo" and B.is_cuda
+    if host_coll:
+        Bh = B.cpu()
+        dist.broadcast(Bh, src=src, group=group)
+        B.copy_(Bh)
+    else:
+        dist.broadcast(B, src=src, group=group)
+    if m_total is None:
+        sizes = torch.tensor([A_local.shape[0]], dtype=torch.int64, device=A_local.device)
+        all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
+        dist.all_gather(all_sizes, sizes, group=group)
+        rows = [int(v.item()) for v in all_sizes]
+    else:
+        rows = [row_partition(m_total, world, r)[1] - row_partition(m_total, world, r)[0] for r in range(world)]
+    n = B.shape[1]
     if mode == "accu":
         if accu_fns is None:
             from . import oz2
             accu_fns = (oz2.scale_accu, oz2.dgemm_scaled)
         scale_fn, scaled_fn = accu_fns
         e, f = scale_fn(A_local, B, num_moduli)
-        dist.all_reduce(f, op=dist.ReduceOp.MIN, group=group)
-        C_local = scaled_fn(A_local, B, e, f, num_moduli)
+        if host_coll:
+            fh = f.cpu()
+            dist.all_reduce(fh, op=dist.ReduceOp.MIN, group=group)
+            f.copy_(fh)
+        else:
+            dist.all_reduce(f, op=dist.ReduceOp.MIN, group=group)
+        res = scaled_fn(A_local, B, e, f, num_moduli)
+        if C_local is None:
+            C_local = res
+        else:
+            C_local.copy_(res)
+        chunks = 1
+        pieces = [C_local]
     else:
-        C_local = local_fn(A_local, B, num_moduli, mode)
-    if gather_to is None:
+        if local_fn is None:
+            from . import oz2
+            prep = oz2.PreparedB(B, num_moduli, mode)
+            block_fn = lambda a, out: prep.dgemm(a, out=out)
+        else:
+            def block_fn(a, out):
+                out.copy_(local_fn(a, B, num_moduli, mode))
+                return out
+        if C_local is None:
+            C_local = torch.empty((A_local.shape[0], n), dtype=torch.float64, device=A_local.device)
+        chunks = max(1, int(chunks))
+        pieces = []
+    works, recv = [], []
+    for c in range(chunks):
+        # piece c of every rank: rows row_partition(rows[r], chunks, c) of that rank's block
+        pr = [row_partition(rr, chunks, c) for rr in rows]
+        p0, p1 = pr[rank]
+        if mode != "accu":
+            if p1 > p0:
+                block_fn(A_local[p0:p1], C_local[p0:p1])
+            piece = C_local[p0:p1]
+        else:
+            piece = pieces[0]
+        if gather_to is None:
+            continue
+        mr = max(b - a for a, b in pr)
+        if piece.shape[0] < mr:
+            send = torch.zeros((mr, n), dtype=C_local.dtype, device=C_local.device)
+            send[:piece.shape[0]] = piece
+        else:
+            send = piece.contiguous()
+        cdev = "cpu" if host_coll else C_local.device
+        if host_coll:
+            send = send.cpu()
+        bufs = [torch.empty((mr, n), dtype=C_local.dtype, device=cdev) for _ in range(world)] \
+            if rank == gather_to else None
+        works.append(dist.gather(send, bufs, dst=gather_to, group=group, async_op=True))
+        recv.append((bufs, pr, send))
+    for w in works:
+        w.wait()
+    if gather_to is None or rank != gather_to:
         return C_local, None
-    if m_total is None:
-        sizes = torch.tensor([A_local.shape[0]], dtype=torch.int64, device=C_local.device)
-        all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
-        dist.all_gather(all_sizes, sizes, group=group)
-        rows = [int(s.item()) for s in all_sizes]
-    else:
-        rows = [row_partition(m_total, world, r)[1] - row_partition(m_total, world, r)[0] for r in range(world)]
-    # dist.gather needs equal shapes: pad every block to the largest
-    mr = max(rows)
-    n = C_local.shape[1]
-    if C_local.shape[0] < mr:
-        pad = torch.zeros((mr, n), dtype=C_local.dtype, device=C_local.device)
-        pad[:C_local.shape[0]] = C_local
-        send = pad
-    else:
-        send = C_local.contiguous()
-    if rank == gather_to:
-        bufs = [torch.empty((mr, n), dtype=C_local.dtype, device=C_local.device) for _ in range(world)]
-        dist.gather(send, bufs, dst=gather_to, group=group)
-        C_full = torch.cat([b[:r] for b, r in zip(bufs, rows)], dim=0)
-        return C_local, C_full
-    dist.gather(send, None, dst=gather_to, group=group)
-    return C_local, None
+    parts = []
+    for r in range(world):                           # rank-major, piece order within a rank
+        for bufs, pr, _ in recv:
+            a, b = pr[r]
+            parts.append(bufs[r][:b - a])
+    return C_local, torch.cat(parts, dim=0).to(C_local.device)

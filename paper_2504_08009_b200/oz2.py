@@ -30,7 +30,8 @@ SYMBOLS = [
     "oz2_scale_cols", "oz2_trunc_rows", "oz2_trunc_cols", "oz2_residues_rows", "oz2_residues_cols",
     "oz2_modmul", "oz2_crt", "oz2_tables", "oz2_eq17_k", "oz2_strerror", "oz2_version",
     "oz2_set_profiling", "oz2_stage_times", "oz2_dgemm_op", "oz2_dgemm_strided_batched",
-    "oz2_scale_accu", "oz2_dgemm_scaled",
+    "oz2_scale_accu", "oz2_dgemm_scaled", "oz2_prepare_b", "oz2_dgemm_prepared", "oz2_release_b",
+    "oz2_set_sm_limit",
 ]
 OP_N, OP_T = 0, 1
 # stage 0 times A's conversion (and B's too with OZ2_CONV_OVERLAP=1; the two column
@@ -77,6 +78,10 @@ def lib() -> ctypes.CDLL:
                 L.oz2_scale_rows.argtypes = [P, i64, i64, P, i64, i32, P]
                 L.oz2_scale_cols.argtypes = [P, i64, i64, P, i64, i32, P]
                 L.oz2_scale_accu.argtypes = [P, i64, i64, i64, P, i64, P, i64, i32, P, P]
+                L.oz2_prepare_b.argtypes = [P, i64, i64, P, i64, i32]
+                L.oz2_dgemm_prepared.argtypes = [P, i64, P, i64, P, i64]
+                L.oz2_release_b.argtypes = [P]
+                L.oz2_set_sm_limit.argtypes = [P, i32]
                 L.oz2_dgemm_scaled.argtypes = [P, i64, i64, i64, P, i64, P, i64, P, P, P, i64, i32]
                 L.oz2_trunc_rows.argtypes = [P, i64, i64, P, i64, P, P]
                 L.oz2_trunc_cols.argtypes = [P, i64, i64, P, i64, P, P]
@@ -238,6 +243,42 @@ def dgemm(A, B, num_moduli: int = 14, mode="fast", out=None):
     _check(lib().oz2_dgemm_ex(h.ptr, m, n, k, _vp(A), _ld(A), _vp(B), _ld(B), _vp(C), _ld(C),
                               num_moduli), "oz2_dgemm_ex")
     return C
+
+
+class PreparedB:
+    """B-stationary products (oz2_prepare_b / oz2_dgemm_prepared): B converted
+    once on this device's handle, then any number of row blocks of A."""
+
+    def __init__(self, B, num_moduli: int = 14, mode="fast"):
+        import torch
+
+        self._B = _rowmajor(B, torch.float64)          # kept alive while prepared
+        self.k, self.n = self._B.shape
+        self.N = num_moduli
+        self.mode = mode
+        self.h = handle(self._B.device.index)
+        self.h.prepare(mode)
+        _check(lib().oz2_prepare_b(self.h.ptr, self.k, self.n, _vp(self._B), _ld(self._B), num_moduli),
+               "oz2_prepare_b")
+
+    def dgemm(self, A, out=None):
+        import torch
+
+        A = _rowmajor(A, torch.float64)
+        m = A.shape[0]
+        assert A.shape[1] == self.k
+        C = out if out is not None else torch.empty((m, self.n), dtype=torch.float64, device=A.device)
+        self.h.prepare(self.mode, workspace_bytes(m, self.n, self.k, self.N))
+        _check(lib().oz2_dgemm_prepared(self.h.ptr, m, _vp(A), _ld(A), _vp(C), _ld(C)), "oz2_dgemm_prepared")
+        return C
+
+    def release(self):
+        _check(lib().oz2_release_b(self.h.ptr), "oz2_release_b")
+
+
+def set_sm_limit(sms: int, device=None):
+    """Persistent-GEMM SM budget on this device's handle (0 = all)."""
+    _check(lib().oz2_set_sm_limit(handle(device).ptr, int(sms)), "oz2_set_sm_limit")
 
 
 def dgemm_scaled(A, B, e, f, num_moduli: int = 14, out=None):

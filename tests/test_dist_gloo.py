@@ -92,7 +92,7 @@ def test_rowblock_accu_gloo_world2(tmp_path, oracle):
     assert np.all(f_half >= f_full)
 
 
-def _worker(rank, world, port, m, n, k, N, out_path):
+def _worker(rank, world, port, m, n, k, N, out_path, chunks=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -101,7 +101,7 @@ def _worker(rank, world, port, m, n, k, N, out_path):
         r0, r1 = row_partition(m, world, rank)
         A_local = torch.from_numpy(A[r0:r1].copy())
         B = torch.from_numpy(phi_matrix_np(k, n, 1.0, seed=6)) if rank == 0 else torch.empty((k, n), dtype=torch.float64)
-        C_local, C_full = dgemm_rowblock(A_local, B, N, "fast", local_fn=_oracle_local, m_total=m)
+        C_local, C_full = dgemm_rowblock(A_local, B, N, "fast", local_fn=_oracle_local, m_total=m, chunks=chunks)
         if rank == 0:
             np.save(out_path, C_full.numpy())
         # the broadcast delivered B everywhere
@@ -111,11 +111,13 @@ def _worker(rank, world, port, m, n, k, N, out_path):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("m", [37, 64])
-def test_rowblock_gloo_world2(tmp_path, oracle, m):
+@pytest.mark.parametrize("m,chunks", [(37, 1), (64, 1), (37, 3), (64, 4)])
+def test_rowblock_gloo_world2(tmp_path, oracle, m, chunks):
+    """chunks > 1: the pipelined gather (piece c transfers while c + 1 computes)
+    reassembles the rows in order, ragged pieces included."""
     n, k, N = 29, 300, 14
     out = str(tmp_path / "C.npy")
-    mp.spawn(_worker, args=(2, _free_port(), m, n, k, N, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), m, n, k, N, out, chunks), nprocs=2, join=True)
     C = np.load(out)
     A = phi_matrix_np(m, k, 1.0, seed=5)
     B = phi_matrix_np(k, n, 1.0, seed=6)

@@ -325,3 +325,26 @@ def test_dgemm_scaled_and_sharded_accu(oz2, oracle):
     fmin = torch.minimum(ef[0][1], ef[1][1])
     Cs = torch.cat([oz2.dgemm_scaled(Ad[a:b], Bd, ef[i][0], fmin, 16) for i, (a, b) in enumerate(parts)])
     assert_bitwise(Cs.cpu().numpy(), ref, "row-sharded accu (MIN of partial f)")
+
+
+def test_prepared_b_and_sm_limit(oz2, oracle):
+    """B-stationary products (oz2_prepare_b / oz2_dgemm_prepared) and a reduced
+    GEMM SM budget give the same bits as oz2_dgemm."""
+    B = phi_matrix_np(700, 650, 1.0, seed=97)
+    Bd = torch.from_numpy(B).to(DEV)
+    pb = oz2.PreparedB(Bd, 14)
+    for seed, m in ((98, 300), (99, 1030)):
+        A = phi_matrix_np(m, 700, 1.0, seed=seed)
+        Ad = torch.from_numpy(A).to(DEV)
+        ref = oz2.dgemm(Ad, Bd, 14).cpu().numpy()
+        assert_bitwise(pb.dgemm(Ad).cpu().numpy(), ref, f"prepared B m={m}")
+        assert_bitwise(ref[:5], oracle.dgemm(A[:5], B, 14), "dgemm rows vs oracle")
+    pb.release()
+    oz2.set_sm_limit(100)
+    try:
+        A = phi_matrix_np(900, 700, 1.0, seed=100)
+        Ad = torch.from_numpy(A).to(DEV)
+        C = oz2.dgemm(Ad, Bd, 14).cpu().numpy()
+    finally:
+        oz2.set_sm_limit(0)
+    assert_bitwise(C, oz2.dgemm(Ad, Bd, 14).cpu().numpy(), "sm limit 100")
