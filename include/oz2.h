@@ -141,10 +141,11 @@ int oz2_dgemm_strided_batched(oz2_handle_t h, int transA, int transB, int64_t m,
                               int64_t batch, int num_moduli);
 
 /* End-to-end variant with HOST buffers: copies A and B to the device, runs
- * Algorithm 1 and copies C back, then synchronises.  Pipelined over up to 8
- * row blocks of A / C (rows multiple of 256, >= 4096 rows each): B is copied
- * and converted first, each row block is converted and multiplied as soon as
- * it lands, and its C block is copied back on a second copy stream while the
+ * Algorithm 1 and copies C back, then synchronises.  Pipelined over row blocks
+ * of A / C (multiples of 256 rows; for m >= 12288 a 1024-row first block,
+ * 4096-row middle blocks and a 2048..256 shrinking tail): B is copied and
+ * converted first, each row block is converted and multiplied as soon as it
+ * lands, and its C block is copied back on a second copy stream while the
  * next block computes.  The result is bit-identical to oz2_dgemm_ex.  Copies
  * overlap only if the host buffers are page-locked.  Workspace (ctx-owned or
  * oz2_set_workspace): oz2_workspace_bytes(m, n, k, N) + 8 (mk + kn + mn) + 1 KiB. */

@@ -828,9 +828,29 @@ int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
     // multiplied as soon as its copy lands, and its C block leaves on the D2H
     // stream while block i + 1 computes.  Results are bit-identical to one call
     // (e_i depends on row i only).
-    const int64_t R = std::max<int64_t>(1, std::min<int64_t>(8, m / 4096));
-    const int64_t mb = round_up((m + R - 1) / R, 256);
-    const int64_t nblk = (m + mb - 1) / mb;
+    // Block schedule: a small first block (the GEMMs start as soon as B and 1024
+    // rows have landed), 4096-row middle blocks, then a shrinking tail (2048,
+    // 1024, 512, 256, 256) so the last block's GEMM and copy-back are short.
+    // Small m: equal blocks of >= 4096 rows.
+    std::vector<int64_t> blk_r0, blk_rows;
+    {
+        std::vector<int64_t> sizes;
+        if (m >= 12288) {
+            const int64_t tail[5] = {2048, 1024, 512, 256, 256};
+            int64_t mid = m - 1024 - 4096;
+            sizes.push_back(1024);
+            while (mid > 0) { const int64_t b = std::min<int64_t>(4096, mid); sizes.push_back(b); mid -= b; }
+            for (int64_t t : tail) sizes.push_back(t);
+        } else {
+            const int64_t R = std::max<int64_t>(1, std::min<int64_t>(8, m / 4096));
+            const int64_t eq = round_up((m + R - 1) / R, 256);
+            for (int64_t r = 0; r < m; r += eq) sizes.push_back(std::min(eq, m - r));
+        }
+        int64_t r0 = 0;
+        for (int64_t sz : sizes) { blk_r0.push_back(r0); blk_rows.push_back(sz); r0 += sz; }
+    }
+    const int64_t nblk = (int64_t)blk_r0.size();
+    const int64_t mb = *std::max_element(blk_rows.begin(), blk_rows.end());
     Layout L = layout_for(mb, n, k, N, gemm_sms(h));          // A planes and e for one row block
     const size_t bytesA = sizeof(double) * (size_t)m * (size_t)k;
     const size_t bytesB = sizeof(double) * (size_t)k * (size_t)n;
@@ -862,7 +882,7 @@ int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
                           cudaMemcpyHostToDevice, h->s_h2d) != cudaSuccess) return OZ2_ERR_CUDA;
     cudaEventRecord(evB, h->s_h2d);
     for (int64_t b = 0; b < nblk; b++) {
-        const int64_t r0 = b * mb, rows = std::min(mb, m - r0);
+        const int64_t r0 = blk_r0[b], rows = blk_rows[b];
         if (cudaMemcpy2DAsync(dA + r0 * k, sizeof(double) * k, A + r0 * lda, sizeof(double) * lda,
                               sizeof(double) * k, rows, cudaMemcpyHostToDevice, h->s_h2d) != cudaSuccess)
             return OZ2_ERR_CUDA;
@@ -882,7 +902,7 @@ int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
     CUtensorMap tB;
     if ((rc = make_plane_map(&tB, Bres, n, k, L.ldr, N, 256 / oz2::gemm_cta_group()))) return rc;
     for (int64_t b = 0; b < nblk; b++) {
-        const int64_t r0 = b * mb, rows = std::min(mb, m - r0);
+        const int64_t r0 = blk_r0[b], rows = blk_rows[b];
         cudaStreamWaitEvent(h->stream, evA[b], 0);
         oz2::launch_rows(dA + r0 * k, rows, k, k, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
         CUtensorMap tA;
