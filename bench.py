@@ -335,7 +335,8 @@ def main():
             "n_scaled_roofline_frac": value / world / (4500.0 / N),
             # fast / eq17: rows, cols_stats, cols_finalize, cols_residues, modmul; accu adds
             # rows_hat7, cols_stats, cols_finalize, cols_hat7, the bound GEMM and 2 finalizes
-            "gpu_launches": (10 if args.mode == "accu" else 5) * args.steps,
+            # multi-GPU (fast): cols_stats, cols_finalize, cols_residues once, rows + GEMM per piece
+            "gpu_launches": (10 if args.mode == "accu" else (5 if world == 1 else 3 + 2 * chunks)) * args.steps,
             "clocks": clk.summary()}
 
     # e2e: same metric through the C ABI with host buffers (pinned), copies timed

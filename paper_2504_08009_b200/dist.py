@@ -105,6 +105,12 @@ def dgemm_rowblock(A_local, B, num_moduli: int = 14, mode: str = "fast", group=N
         chunks = max(1, int(chunks))
         pieces = []
     works, recv = [], []
+    # the gathered result: pieces land directly in their rows of C_full when no
+    # padding is needed (every rank's piece c has the same size)
+    C_full = None
+    rstart = [sum(rows[:r]) for r in range(world)]
+    if gather_to is not None and rank == gather_to:
+        C_full = torch.empty((sum(rows), n), dtype=torch.float64, device="cpu" if host_coll else B.device)
     for c in range(chunks):
         # piece c of every rank: rows row_partition(rows[r], chunks, c) of that rank's block
         pr = [row_partition(rr, chunks, c) for rr in rows]
@@ -126,17 +132,21 @@ def dgemm_rowblock(A_local, B, num_moduli: int = 14, mode: str = "fast", group=N
         cdev = "cpu" if host_coll else C_local.device
         if host_coll:
             send = send.cpu()
-        bufs = [torch.empty((mr, n), dtype=C_local.dtype, device=cdev) for _ in range(world)] \
-            if rank == gather_to else None
+        bufs, direct = None, all(b - a == mr for a, b in pr)
+        if rank == gather_to:
+            if direct:
+                bufs = [C_full[rstart[r] + pr[r][0]: rstart[r] + pr[r][1]] for r in range(world)]
+            else:
+                bufs = [torch.empty((mr, n), dtype=C_local.dtype, device=cdev) for _ in range(world)]
         works.append(dist.gather(send, bufs, dst=gather_to, group=group, async_op=True))
-        recv.append((bufs, pr, send))
+        recv.append((bufs, pr, send, direct))
     for w in works:
         w.wait()
     if gather_to is None or rank != gather_to:
         return C_local, None
-    parts = []
-    for r in range(world):                           # rank-major, piece order within a rank
-        for bufs, pr, _ in recv:
-            a, b = pr[r]
-            parts.append(bufs[r][:b - a])
-    return C_local, torch.cat(parts, dim=0).to(C_local.device)
+    for bufs, pr, _, direct in recv:                 # padded pieces: copy into place
+        if not direct:
+            for r in range(world):
+                a, b = pr[r]
+                C_full[rstart[r] + a: rstart[r] + b] = bufs[r][:b - a]
+    return C_local, C_full.to(C_local.device)
