@@ -105,7 +105,9 @@ struct oz2_context {
 namespace {
 // SMs the persistent GEMM may use (even: CTA pairs)
 inline int gemm_sms(const oz2_context* h) {
-    const int s = h->sm_limit > 0 && h->sm_limit < h->num_sms ? h->sm_limit : h->num_sms;
+    static const int env_limit = [] { const char* v = getenv("OZ2_SM_LIMIT"); return v && *v ? atoi(v) : 0; }();
+    const int lim = h->sm_limit > 0 ? h->sm_limit : env_limit;
+    const int s = lim > 0 && lim < h->num_sms ? lim : h->num_sms;
     return s & ~1;
 }
 }  // namespace
