@@ -141,14 +141,19 @@ int oz2_dgemm_strided_batched(oz2_handle_t h, int transA, int transB, int64_t m,
                               int64_t batch, int num_moduli);
 
 /* End-to-end variant with HOST buffers: copies A and B to the device, runs
- * Algorithm 1 and copies C back, then synchronises.  Pipelined over row blocks
- * of A / C (multiples of 256 rows; for m >= 12288 a 1024-row first block,
- * 4096-row middle blocks and a 2048..256 shrinking tail): B is copied and
- * converted first, each row block is converted and multiplied as soon as it
- * lands, and its C block is copied back on a second copy stream while the
- * next block computes.  The result is bit-identical to oz2_dgemm_ex.  Copies
- * overlap only if the host buffers are page-locked.  Workspace (ctx-owned or
- * oz2_set_workspace): oz2_workspace_bytes(m, n, k, N) + 8 (mk + kn + mn) + 1 KiB. */
+ * Algorithm 1 and copies C back, then synchronises.  Copies and computation
+ * are pipelined (bit-identical to oz2_dgemm_ex):
+ *  - m, n >= 8192 (FAST / EQ17): 4 column panels of B x row blocks of A; the
+ *    H2D stream interleaves B0, A0, B1, A1, ..., each panel / block is
+ *    converted once when it lands, each (block, panel) product runs as soon as
+ *    both are on the device, and its C tile is copied back at once on a second
+ *    copy stream (OZ2_HOST_2D=0 selects the row-block pipeline below);
+ *  - otherwise row blocks of A / C (multiples of 256 rows; for m >= 12288 a
+ *    1024-row head, 4096-row middle blocks and a shrinking tail) after B;
+ *  - OZ2_MODE_ACCU (f depends on all of A): copy, compute, copy back.
+ * Copies overlap only if the host buffers are page-locked.  Workspace
+ * (ctx-owned or oz2_set_workspace): oz2_workspace_bytes(m, n, k, N) +
+ * 8 (mk + kn + mn) + 1 KiB. */
 int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A,
                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                    int num_moduli);

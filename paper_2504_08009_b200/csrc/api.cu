@@ -646,6 +646,121 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     return cuda_status();
 }
 
+// 2-D host pipeline (FAST / EQ17, large m and n): the H2D stream interleaves
+// column panels of B and row blocks of A (B0, A0, B1, A1, ..., then the rest
+// of A); every panel and block is converted once when it lands, and each
+// (block, panel) product runs as soon as both sides are on the device, its C
+// tile going back on the D2H stream at once.  Compute starts after the first
+// panel and block instead of after all of B; bit-identical to one call (e_i
+// depends on row i only, f_j on column j only).
+int dgemm_host_2d(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                  const double* B, int64_t ldb, double* C, int64_t ldc, int N, int kstar) {
+    const int64_t P = 4, R = std::max<int64_t>(4, std::min<int64_t>(16, m / 2048));
+    const int64_t nb = round_up((n + P - 1) / P, 512), mb = round_up((m + R - 1) / R, 256);
+    std::vector<int64_t> c0s, ncs, r0s, nrs;
+    for (int64_t c = 0; c < n; c += nb) { c0s.push_back(c); ncs.push_back(std::min(nb, n - c)); }
+    for (int64_t r = 0; r < m; r += mb) { r0s.push_back(r); nrs.push_back(std::min(mb, m - r)); }
+    const int64_t np = (int64_t)c0s.size(), nr = (int64_t)r0s.size();
+    Layout L = layout_for(m, n, k, N, gemm_sms(h), nb);
+    const size_t bytesA = sizeof(double) * (size_t)m * (size_t)k;
+    const size_t bytesB = sizeof(double) * (size_t)k * (size_t)n;
+    const size_t offA = (size_t)round_up((int64_t)L.total, 256);
+    const size_t offB = (size_t)round_up((int64_t)(offA + bytesA), 256);
+    const size_t offC = (size_t)round_up((int64_t)(offB + bytesB), 256);
+    uint8_t* ws;
+    int rc;
+    if ((rc = get_workspace(h, offC + sizeof(double) * (size_t)m * (size_t)n, &ws))) return rc;
+    double* dA = (double*)(ws + offA);
+    double* dB = (double*)(ws + offB);
+    double* dC = (double*)(ws + offC);
+    if (!h->s_h2d && cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking) != cudaSuccess) return OZ2_ERR_CUDA;
+    if (!h->s_d2h && cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking) != cudaSuccess) return OZ2_ERR_CUDA;
+    const size_t nev = (size_t)(np + nr + nr * np + 1);
+    while (h->pipe_ev.size() < nev) {
+        cudaEvent_t ev;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return OZ2_ERR_CUDA;
+        h->pipe_ev.push_back(ev);
+    }
+    cudaEvent_t evStart = h->pipe_ev[0];
+    cudaEvent_t* evB = &h->pipe_ev[1];
+    cudaEvent_t* evA = &h->pipe_ev[1 + np];
+    cudaEvent_t* evP = &h->pipe_ev[1 + np + nr];
+    if (cudaEventRecord(evStart, h->stream) != cudaSuccess) return OZ2_ERR_CUDA;
+    cudaStreamWaitEvent(h->s_h2d, evStart, 0);
+    cudaStreamWaitEvent(h->s_d2h, evStart, 0);
+    // transfer order: B0, A0, B1, A1, ..., then the remaining blocks of A
+    std::vector<std::pair<int, int64_t>> order;                  // (0 = panel of B, 1 = block of A, index)
+    for (int64_t x = 0; x < std::max(np, nr); x++) {
+        if (x < np) order.push_back({0, x});
+        if (x < nr) order.push_back({1, x});
+    }
+    for (auto& o : order) {
+        cudaError_t ce;
+        if (o.first == 0) {
+            const int64_t c0 = c0s[o.second], nc = ncs[o.second];
+            ce = cudaMemcpy2DAsync(dB + c0, sizeof(double) * n, B + c0, sizeof(double) * ldb, sizeof(double) * nc, k,
+                                   cudaMemcpyHostToDevice, h->s_h2d);
+            if (ce == cudaSuccess) ce = cudaEventRecord(evB[o.second], h->s_h2d);
+        } else {
+            const int64_t r0 = r0s[o.second], rows = nrs[o.second];
+            ce = cudaMemcpy2DAsync(dA + r0 * k, sizeof(double) * k, A + r0 * lda, sizeof(double) * lda,
+                                   sizeof(double) * k, rows, cudaMemcpyHostToDevice, h->s_h2d);
+            if (ce == cudaSuccess) ce = cudaEventRecord(evA[o.second], h->s_h2d);
+        }
+        if (ce != cudaSuccess) return OZ2_ERR_CUDA;
+    }
+    int8_t* Ares = (int8_t*)(ws + L.off_Ares);                 // block-major: block i at N * r0 * ldr
+    int8_t* Bres = (int8_t*)(ws + L.off_Bres);                 // panel-major: panel j at N * c0 * ldr
+    int32_t* e = (int32_t*)(ws + L.off_e);
+    int32_t* f = (int32_t*)(ws + L.off_f);
+    std::vector<char> haveA(nr, 0), haveB(np, 0);
+    mark(h);
+    mark(h);
+    mark(h);
+    mark(h);                                                   // conversions are timed inside the GEMM stage
+    auto product = [&](int64_t i, int64_t j) -> int {
+        const int64_t r0 = r0s[i], rows = nrs[i], c0 = c0s[j], nc = ncs[j];
+        CUtensorMap tA, tB;
+        int rr;
+        if ((rr = make_plane_map(&tA, Ares + (size_t)N * r0 * L.ldr, rows, k, L.ldr, N, 128))) return rr;
+        if ((rr = make_plane_map(&tB, Bres + (size_t)N * c0 * L.ldr, nc, k, L.ldr, N, 256 / oz2::gemm_cta_group())))
+            return rr;
+        if (oz2::launch_modmul_fused(&tA, &tB, rows, nc, k, N, ws + L.off_scratch, e + r0, f + c0, dC + r0 * n + c0, n,
+                                     (uint32_t*)(ws + L.off_sync), gemm_sms(h), h->stream))
+            return OZ2_ERR_CUDA;
+        cudaEvent_t ev = evP[i * np + j];
+        cudaEventRecord(ev, h->stream);
+        cudaStreamWaitEvent(h->s_d2h, ev, 0);
+        if (cudaMemcpy2DAsync(C + r0 * ldc + c0, sizeof(double) * ldc, dC + r0 * n + c0, sizeof(double) * n,
+                              sizeof(double) * nc, rows, cudaMemcpyDeviceToHost, h->s_d2h) != cudaSuccess)
+            return OZ2_ERR_CUDA;
+        return OZ2_OK;
+    };
+    for (auto& o : order) {
+        const int64_t x = o.second;
+        if (o.first == 0) {
+            const int64_t c0 = c0s[x], nc = ncs[x];
+            cudaStreamWaitEvent(h->stream, evB[x], 0);
+            oz2::launch_cols_exponents(dB + c0, k, nc, n, N, h->mode, kstar, f + c0, ws + L.off_stats, h->stream);
+            oz2::launch_cols_residues(dB + c0, k, nc, n, f + c0, N, Bres + (size_t)N * c0 * L.ldr, L.ldr, h->stream);
+            haveB[x] = 1;
+            for (int64_t i = 0; i < nr; i++) if (haveA[i] && (rc = product(i, x))) return rc;
+        } else {
+            const int64_t r0 = r0s[x], rows = nrs[x];
+            cudaStreamWaitEvent(h->stream, evA[x], 0);
+            oz2::launch_rows(dA + r0 * k, rows, k, k, N, 3, h->mode, kstar, e + r0, Ares + (size_t)N * r0 * L.ldr,
+                             L.ldr, h->stream);
+            haveA[x] = 1;
+            for (int64_t j = 0; j < np; j++) if (haveB[j] && (rc = product(x, j))) return rc;
+        }
+    }
+    mark(h);
+    mark(h);
+    if ((rc = cuda_status())) return rc;
+    return cudaStreamSynchronize(h->s_d2h) == cudaSuccess && cudaStreamSynchronize(h->stream) == cudaSuccess
+               ? OZ2_OK : OZ2_ERR_CUDA;
+}
+
 }  // namespace
 
 extern "C" {
@@ -825,6 +940,7 @@ int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
                               cudaMemcpyDeviceToHost, h->stream) != cudaSuccess) return OZ2_ERR_CUDA;
         return cudaStreamSynchronize(h->stream) == cudaSuccess ? OZ2_OK : OZ2_ERR_CUDA;
     }
+    if (m >= 8192 && n >= 8192 && env_flag("OZ2_HOST_2D", 1)) return dgemm_host_2d(h, m, n, k, A, lda, B, ldb, C, ldc, N, kstar);
     // Pipeline over R row blocks of A and C (rows a multiple of 256): B goes
     // first on the H2D stream and is converted once; row block i is converted and
     // multiplied as soon as its copy lands, and its C block leaves on the D2H

@@ -189,6 +189,22 @@ def test_host_entry_point_pipelined(oz2, oracle):
     assert_bitwise(Ch[rows], oracle.dgemm(A[rows], B, 14), "pipelined host path vs oracle")
 
 
+def test_host_entry_point_2d(oz2, oracle):
+    """m, n >= 8192: the 2-D host pipeline (panels of B x blocks of A, ragged
+    last panel 520 columns and last block 2088 rows), bitwise vs the device path."""
+    m, n, k = 9000, 8200, 300
+    A = phi_matrix_np(m, k, 1.0, seed=23)
+    B = phi_matrix_np(k, n, 1.0, seed=24)
+    Ah = torch.from_numpy(A).pin_memory().numpy()
+    Bh = torch.from_numpy(B).pin_memory().numpy()
+    Ch = torch.empty((m, n), dtype=torch.float64).pin_memory().numpy()
+    oz2.dgemm_host(Ah, Bh, 14, out=Ch)
+    Cd = oz2.dgemm(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), 14).cpu().numpy()
+    assert_bitwise(Ch, Cd, "2-D host pipeline vs device path")
+    rows = np.array([0, 2303, 2304, 8999])
+    assert_bitwise(Ch[rows], oracle.dgemm(A[rows], B, 14), "2-D host pipeline vs oracle")
+
+
 def test_k_blocking_forced(oz2, oracle, monkeypatch):
     """K blocking exercised at small k: OZ2_KB_CHUNK=2 splits the
     8 k-blocks of k = 1000 into 4 int32 accumulations whose residues are added."""
