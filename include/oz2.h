@@ -132,6 +132,35 @@ int oz2_release_b(oz2_handle_t h);
 /* Limit the persistent GEMM to `sms` SMs (0 = all; rounded down to even), e.g.
  * to leave SMs to NCCL kernels that overlap it.  Results do not depend on it. */
 int oz2_set_sm_limit(oz2_handle_t h, int sms);
+/* ---- K-split (2-D multi-GPU) pieces, FAST / EQ17 --------------------------
+ * Each rank holds A[:, K_r] (m x k_r) and B[K_r, :] (k_r x n), K_r starting on
+ * a multiple of 256 (the FAST rule's chunk grid, reading R4).  The exponents of
+ * the whole product then follow from two small all-reduces:
+ *   phase 1: oz2_kslice_stats_rows / _cols(E_global = NULL) -> E_out: the max
+ *            chunk exponent (INT32_MIN: no non-zero entry; INT32_MAX: Inf/NaN)
+ *            -> all-reduce MAX;
+ *   phase 2: the same with E_global -> S_out: sum of ceil(S_c / 4^(E - E_c))
+ *            over the rank's chunks (uint64) -> all-reduce SUM;
+ *   oz2_exponents_from_stats(E, S, k_total) -> e (or f), bit-identical to the
+ *   one-GPU rule (EQ17: phase 1 and k_total suffice).
+ * oz2_modmul_residues: Alg. 1 lines 6-7 on the rank's residue planes,
+ * R = C'_t mod m_t in [0, m_t) as uint8, layout [m/rpb][N][rpb][n]
+ * (rows_per_block rpb; 0 = m), ready for an all-to-all to row-block owners.
+ * oz2_crt_sum: c''_t = (sum over the parts g of R + g * part_stride) mod m_t
+ * (linearity of mod), then lines 8-10: C = D^-1 X E^-1 for the local rows.
+ * All device pointers; asynchronous on the handle's stream. */
+int oz2_kslice_stats_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda,
+                          const int32_t* E_global, int32_t* E_out, uint64_t* S_out);
+int oz2_kslice_stats_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb,
+                          const int32_t* E_global, int32_t* E_out, uint64_t* S_out);
+int oz2_exponents_from_stats(oz2_handle_t h, int64_t count, const int32_t* E, const uint64_t* S,
+                             int64_t k_total, int num_moduli, int32_t* e);
+int oz2_modmul_residues(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const int8_t* Ares,
+                        const int8_t* Bres, int64_t ld_res, int num_moduli, uint8_t* R,
+                        int64_t rows_per_block);
+int oz2_crt_sum(oz2_handle_t h, int parts, int64_t m, int64_t n, const uint8_t* R,
+                int64_t part_stride, const int32_t* e, const int32_t* f, int num_moduli,
+                double* C, int64_t ldc);
 /* batch independent products: A + b*strideA, B + b*strideB, C + b*strideC
  * (elements), b = 0..batch-1, in stream order on one workspace. */
 int oz2_dgemm_strided_batched(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n,

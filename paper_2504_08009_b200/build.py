@@ -14,7 +14,7 @@ LIB = os.path.join(HERE, "liboz2.so")
 ROOT = os.path.dirname(HERE)
 
 SOURCES = ["liboz2.cu", "tables.cpp"]
-DEPS = ["liboz2.cu", "tables.cpp", "scale.cu", "gemm.cu", "crt.cu", "accu.cu", "api.cu", "oz2_device.cuh",
+DEPS = ["liboz2.cu", "tables.cpp", "scale.cu", "gemm.cu", "crt.cu", "accu.cu", "kslice.cu", "api.cu", "oz2_device.cuh",
         "oz2_kernels.h", "oz2_tables.h"]
 
 NVCC_FLAGS = [

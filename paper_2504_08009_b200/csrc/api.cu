@@ -857,6 +857,78 @@ int oz2_dgemm_prepared(oz2_handle_t h, int64_t m, const double* A, int64_t lda, 
     return cuda_status();
 }
 
+// ---------------------------------------------------------------------------
+// K-split pieces (2-D multi-GPU, kslice.cu)
+// ---------------------------------------------------------------------------
+int oz2_kslice_stats_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda,
+                          const int32_t* E_global, int32_t* E_out, uint64_t* S_out) {
+    if (!h || h->mode == OZ2_MODE_ACCU || m < 0 || k < 0 || k >= OZ2_MAX_K || lda < (k > 0 ? k : 1)) return OZ2_ERR_INVALID_ARG;
+    if (m > 0 && ((k > 0 && !A) || (!E_global && !E_out) || (E_global && !S_out))) return OZ2_ERR_INVALID_ARG;
+    DevGuard g(h->device);
+    oz2::launch_kslice_rows(A, m, k, lda, h->mode, E_global, E_out, (unsigned long long*)S_out, h->stream);
+    return cuda_status();
+}
+
+int oz2_kslice_stats_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb,
+                          const int32_t* E_global, int32_t* E_out, uint64_t* S_out) {
+    if (!h || h->mode == OZ2_MODE_ACCU || n < 0 || k < 0 || k >= OZ2_MAX_K || ldb < (n > 0 ? n : 1)) return OZ2_ERR_INVALID_ARG;
+    if (n > 0 && ((k > 0 && !B) || (!E_global && !E_out) || (E_global && !S_out))) return OZ2_ERR_INVALID_ARG;
+    DevGuard g(h->device);
+    uint8_t* ws;
+    int rc;
+    if ((rc = get_workspace(h, oz2::cols_stats_bytes(k, n), &ws))) return rc;
+    oz2::launch_kslice_cols(B, k, n, ldb, h->mode, E_global, E_out, (unsigned long long*)S_out, ws, h->stream);
+    return cuda_status();
+}
+
+int oz2_exponents_from_stats(oz2_handle_t h, int64_t count, const int32_t* E, const uint64_t* S, int64_t k_total,
+                             int N, int32_t* e) {
+    if (!h || h->mode == OZ2_MODE_ACCU || count < 0 || (count > 0 && (!E || !S || !e))) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(1, 1, k_total, N);
+    if (rc) return rc;
+    int kstar = 0;
+    if ((rc = kstar_for(h, N, k_total, &kstar))) return rc;
+    DevGuard g(h->device);
+    oz2::launch_exponents_from_stats(E, (const unsigned long long*)S, count, N, h->mode, kstar, e, h->stream);
+    return cuda_status();
+}
+
+int oz2_modmul_residues(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const int8_t* Ares, const int8_t* Bres,
+                        int64_t ld_res, int N, uint8_t* R, int64_t rows_per_block) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(m, n, k, N);
+    if (rc) return rc;
+    if (ld_res < k || ld_res % 16 || rows_per_block < 0 || (m > 0 && n > 0 && !R)) return OZ2_ERR_INVALID_ARG;
+    if (rows_per_block == 0) rows_per_block = m;
+    if (m == 0 || n == 0) return OZ2_OK;
+    DevGuard g(h->device);
+    if (k == 0) {
+        const int64_t nblk = (m + rows_per_block - 1) / rows_per_block;
+        return cudaMemsetAsync(R, 0, (size_t)nblk * N * rows_per_block * n, h->stream) == cudaSuccess ? OZ2_OK : OZ2_ERR_CUDA;
+    }
+    CUtensorMap tA, tB;
+    if ((rc = make_plane_map(&tA, Ares, m, k, ld_res, N, 128))) return rc;
+    if ((rc = make_plane_map(&tB, Bres, n, k, ld_res, N, 256 / oz2::gemm_cta_group()))) return rc;
+    uint8_t* ws;
+    const size_t scr = oz2::fused_scratch_bytes(m, n, N, gemm_sms(h));
+    if ((rc = get_workspace(h, scr + 512, &ws))) return rc;
+    if (oz2::launch_modmul_residues(&tA, &tB, m, n, k, N, ws, R, rows_per_block, (uint32_t*)(ws + scr + 256),
+                                    gemm_sms(h), h->stream))
+        return OZ2_ERR_CUDA;
+    return cuda_status();
+}
+
+int oz2_crt_sum(oz2_handle_t h, int parts, int64_t m, int64_t n, const uint8_t* R, int64_t part_stride,
+                const int32_t* e, const int32_t* f, int N, double* C, int64_t ldc) {
+    if (!h || parts < 1 || parts > (1 << 20)) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(m, n, 0, N);
+    if (rc) return rc;
+    if (ldc < (n > 0 ? n : 1) || (m > 0 && n > 0 && (!R || !e || !f || !C))) return OZ2_ERR_INVALID_ARG;
+    DevGuard g(h->device);
+    oz2::launch_crt_sum(R, parts, part_stride, m, n, e, f, N, C, ldc, h->stream);
+    return cuda_status();
+}
+
 int oz2_dgemm_scaled(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
                      const double* B, int64_t ldb, const int32_t* e, const int32_t* f, double* C, int64_t ldc,
                      int N) {

@@ -92,6 +92,8 @@ struct Params {
     double* C;                      // FUSED
     int64_t ldc;
     int axpby;                      // FUSED: 0 -> C = AB; 1 -> C = alpha AB (+ beta C if beta != 0)
+    uint8_t* res_out;               // FUSED, K-split: final c''_t planes to global instead of the CRT
+    int64_t res_rpb;                //   layout [m / res_rpb][N][res_rpb][n]
     uint32_t* rowmax;               // BOUND (NM < 0): max_j P_ij, max_i P_ij (atomicMax)
     uint32_t* colmax;
     double alpha, beta;
@@ -492,7 +494,28 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     store_residues(reinterpret_cast<uint4*>(tile_scr + ((size_t)((c + 1) * BM + r)) * 32), w, ch, t);
                 }
                 release();
-                if (ch == p.nchunk - 1) {                         // the last K chunk of (tile, t)
+                if (ch == p.nchunk - 1 && p.res_out) {           // K-split: c''_t out, no CRT here
+                    if (row < p.m) {
+                        const int64_t blk = row / p.res_rpb;
+                        uint8_t* orow = p.res_out + ((blk * p.N + t) * p.res_rpb + (row - blk * p.res_rpb)) * p.n;
+                        #pragma unroll 1
+                        for (int cc = 0; cc < CH; cc++) {
+                            const int c = half * CH + cc;
+                            const int col0 = tn * C_::TILE_N + c * 32;
+                            if (col0 >= p.n) break;
+                            const uint4* src = reinterpret_cast<const uint4*>(tile_scr + ((size_t)(c * BM + r)) * 32);
+                            const uint4 v0 = src[0], v1 = src[1];
+                            if (col0 + 32 <= p.n && (p.n & 15) == 0) {
+                                reinterpret_cast<uint4*>(orow + col0)[0] = v0;
+                                reinterpret_cast<uint4*>(orow + col0)[1] = v1;
+                            } else {
+                                const uint32_t wv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                                for (int b = 0; b < 32 && col0 + b < p.n; b++)
+                                    orow[col0 + b] = (uint8_t)(wv[b >> 2] >> (8 * (b & 3)));
+                            }
+                        }
+                    }
+                } else if (ch == p.nchunk - 1) {                  // the last K chunk of (tile, t)
                     // lines 8-10 of the previous tile, SLICES slices of 8 columns spread
                     // over this tile's N units (no burst that would hold TMEM back)
                     if (pend) {
@@ -622,6 +645,27 @@ int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int
     p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
     if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
     return gemm::launch_shape<0>(gemm_shape(), tmA, tmB, p, grid, st);
+}
+
+int launch_modmul_residues(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k, int N,
+                           uint8_t* scratch, uint8_t* R, int64_t rows_per_block, uint32_t* sync_ctr, int num_sms,
+                           cudaStream_t st) {
+    int grid;
+    gemm::Params p = make_params(m, n, k, N, num_sms, gemm_cta_group(), gemm_halves(), &grid);
+    p.scratch = scratch;
+    p.res_out = R;
+    p.res_rpb = rows_per_block > 0 ? rows_per_block : m;
+    p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
+    if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
+    const int shape = gemm_shape();
+    switch (N) {
+#define OZ2_CASE(NN) case NN: return gemm::launch_shape<NN>(shape, tmA, tmB, p, grid, st);
+        OZ2_CASE(2) OZ2_CASE(3) OZ2_CASE(4) OZ2_CASE(5) OZ2_CASE(6) OZ2_CASE(7) OZ2_CASE(8)
+        OZ2_CASE(9) OZ2_CASE(10) OZ2_CASE(11) OZ2_CASE(12) OZ2_CASE(13) OZ2_CASE(14) OZ2_CASE(15)
+        OZ2_CASE(16) OZ2_CASE(17) OZ2_CASE(18) OZ2_CASE(19) OZ2_CASE(20)
+#undef OZ2_CASE
+        default: return (int)cudaErrorInvalidValue;
+    }
 }
 
 int launch_bound_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,

@@ -4,5 +4,6 @@
 #include "scale.cu"
 #include "crt.cu"
 #include "accu.cu"
+#include "kslice.cu"
 #include "gemm.cu"
 #include "api.cu"

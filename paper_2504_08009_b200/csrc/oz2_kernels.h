@@ -59,6 +59,21 @@ void launch_accu_finalize(const int32_t* E, const uint32_t* Pmax, int64_t cnt, i
 int launch_bound_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                       uint32_t* rowmax, uint32_t* colmax, uint32_t* sync_ctr, int num_sms, cudaStream_t st);
 
+// kslice.cu -- K-split pieces (statistics phases, residue sum + CRT)
+void launch_kslice_rows(const double* A, int64_t m, int64_t k, int64_t lda, int mode, const int32_t* Eg,
+                        int32_t* E_out, unsigned long long* S_out, cudaStream_t st);
+void launch_kslice_cols(const double* B, int64_t k, int64_t n, int64_t ldb, int mode, const int32_t* Eg,
+                        int32_t* E_out, unsigned long long* S_out, void* scratch, cudaStream_t st);
+void launch_exponents_from_stats(const int32_t* E, const unsigned long long* S, int64_t cnt, int N, int mode,
+                                 int kstar, int32_t* e, cudaStream_t st);
+void launch_crt_sum(const uint8_t* R, int G, int64_t part_stride, int64_t m, int64_t n, const int32_t* e,
+                    const int32_t* f, int N, double* C, int64_t ldc, cudaStream_t st);
+// line 6 + 7 only: c''_t = C'_t mod m_t in [0, m_t) as uint8 planes, K-blocked;
+// layout [m / rows_per_block][N][rows_per_block][n] (rows_per_block = m: [N][m][n])
+int launch_modmul_residues(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k, int N,
+                           uint8_t* scratch, uint8_t* R, int64_t rows_per_block, uint32_t* sync_ctr, int num_sms,
+                           cudaStream_t st);
+
 // crt.cu -- Alg. 1 lines 7-10
 void launch_crt(const int32_t* cprod, int64_t m, int64_t n, const int32_t* e, const int32_t* f,
                 int N, double* C, int64_t ldc, cudaStream_t st);

@@ -190,10 +190,10 @@ __device__ __forceinline__ int combine_chunks(const int* Ec, const unsigned long
     return bad ? OZ2_EXP_NONFINITE_DEV : e;
 }
 
-// exponent of one row (CTA-wide), first pass over the row; loads keep the row
-// in L2 (evict_last) for the residue pass that follows
+// chunk statistics of one row (CTA-wide) into sm (E_c, S_c per chunk, the
+// non-finite flag); loads keep the row in L2 (evict_last) for the residue pass
 template <int MODE>
-__device__ int row_exponent(const double* __restrict__ X, int64_t k, int Tb, int kstar, RowSmem& sm) {
+__device__ void row_chunk_stats(const double* __restrict__ X, int64_t k, RowSmem& sm) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nwarps = blockDim.x >> 5;
     const int nch = (int)((k + KC - 1) / KC);
@@ -241,8 +241,15 @@ __device__ int row_exponent(const double* __restrict__ X, int64_t k, int Tb, int
         if (lane == 0) { sm.Ec[c] = Ec; sm.Sc[c] = (unsigned long long)S; }
     }
     __syncthreads();
+}
+
+// exponent of one row (CTA-wide), first pass over the row
+template <int MODE>
+__device__ int row_exponent(const double* __restrict__ X, int64_t k, int Tb, int kstar, RowSmem& sm) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    row_chunk_stats<MODE>(X, k, sm);
     if (warp == 0) {
-        const int e = combine_chunks<MODE>(sm.Ec, sm.Sc, nch, sm.misc[0], Tb, kstar);
+        const int e = combine_chunks<MODE>(sm.Ec, sm.Sc, (int)((k + KC - 1) / KC), sm.misc[0], Tb, kstar);
         if (lane == 0) sm.misc[1] = e;
     }
     __syncthreads();

@@ -150,3 +150,89 @@ def dgemm_rowblock(A_local, B, num_moduli: int = 14, mode: str = "fast", group=N
                 a, b = pr[r]
                 C_full[rstart[r] + a: rstart[r] + b] = bufs[r][:b - a]
     return C_local, C_full.to(C_local.device)
+
+
+def kslice_partition(k: int, world: int, rank: int, chunk: int = 256) -> tuple[int, int]:
+    """Balanced K range [l0, l1) of rank `rank`, boundaries on the FAST rule's
+    256-element chunk grid (reading R4) -- the last range takes the ragged tail."""
+    nch = (k + chunk - 1) // chunk
+    c0, c1 = row_partition(nch, world, rank)
+    return min(k, c0 * chunk), min(k, c1 * chunk)
+
+
+def dgemm_ksplit(A_ks, B_ks, k_total: int, num_moduli: int = 14, mode: str = "fast", group=None,
+                 gather_to: Optional[int] = 0):
+    """C = A B with the inner dimension split across the ranks (2-D / K-split
+    multi-GPU): rank r holds A[:, K_r] (m x k_r) and B[K_r, :]
+    (k_r x n), K_r = kslice_partition(k_total, world, r).  No operand is
+    broadcast; the exchange is
+      1. two all-reduces of the per-row / per-column statistics (int32 MAX, then
+         uint64 SUM; m + n values each) that give the exponents of the whole
+         product, bit-identical to one GPU (reading R4 is built from per-chunk
+         integer statistics);
+      2. one all-to-all of the rank's reduced partial residues c''_t (uint8,
+         N bytes per element of C) so that every rank receives, for its own
+         row block, the partial residues of all K slices;
+    then oz2_crt_sum adds them mod m_t and runs lines 8-10.  Returns (C_local,
+    C_full) like dgemm_rowblock: rank r's rows are row_partition(m, world, r)
+    padded to equal blocks of ceil(m / world).  FAST / EQ17."""
+    import torch
+    import torch.distributed as dist
+    from . import oz2
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    m, n = A_ks.shape[0], B_ks.shape[1]
+    N = num_moduli
+    host_coll = dist.get_backend(group) == "gloo" and A_ks.is_cuda
+
+    def allreduce(t, op):
+        if host_coll:
+            th = t.cpu()
+            dist.all_reduce(th, op=op, group=group)
+            t.copy_(th)
+        else:
+            dist.all_reduce(t, op=op, group=group)
+
+    # exponents of the whole product (phase 1: MAX of chunk exponents, phase 2: SUM)
+    E = torch.cat([oz2.kslice_stats_rows(A_ks, mode=mode), oz2.kslice_stats_cols(B_ks, mode=mode)])
+    allreduce(E, dist.ReduceOp.MAX)
+    EA, EB = E[:m], E[m:]
+    S = torch.cat([oz2.kslice_stats_rows(A_ks, EA, mode=mode), oz2.kslice_stats_cols(B_ks, EB, mode=mode)])
+    allreduce(S, dist.ReduceOp.SUM)
+    e = oz2.exponents_from_stats(EA, S[:m], k_total, N, mode)
+    f = oz2.exponents_from_stats(EB.contiguous(), S[m:].contiguous(), k_total, N, mode)
+    # residues of the local slices and their reduced products, laid out by destination row block
+    k_loc = A_ks.shape[1]
+    Ar = oz2.residues_rows(A_ks, e, N)
+    Br = oz2.residues_cols(B_ks, f, N)
+    rpb = (m + world - 1) // world
+    if k_loc > 0:
+        R = oz2.modmul_residues(Ar, Br, k_loc, rows_per_block=rpb)          # [ceil(m/rpb)][N][rpb][n]
+    else:
+        R = torch.zeros(((m + rpb - 1) // rpb, N, rpb, n), dtype=torch.uint8, device=A_ks.device)
+    if R.shape[0] < world:                                                 # fewer rows than ranks
+        R = torch.cat([R, torch.zeros((world - R.shape[0], N, rpb, n), dtype=torch.uint8, device=R.device)])
+    recv = torch.empty_like(R)
+    if host_coll:
+        rh = torch.empty_like(R, device="cpu")
+        dist.all_to_all_single(rh, R.cpu(), group=group)
+        recv.copy_(rh)
+    else:
+        dist.all_to_all_single(recv, R, group=group)
+    r0 = min(m, rank * rpb)
+    r1 = min(m, r0 + rpb)
+    C_local = torch.empty((r1 - r0, n), dtype=torch.float64, device=A_ks.device)
+    if r1 > r0:
+        oz2.crt_sum(recv, world, N * rpb * n, r1 - r0, n, e[r0:r1], f, N, out=C_local)
+    if gather_to is None:
+        return C_local, None
+    send = torch.zeros((rpb, n), dtype=torch.float64, device=A_ks.device)
+    send[:r1 - r0] = C_local
+    if host_coll:
+        send = send.cpu()
+    bufs = [torch.empty_like(send) for _ in range(world)] if rank == gather_to else None
+    dist.gather(send, bufs, dst=gather_to, group=group)
+    if rank != gather_to:
+        return C_local, None
+    return C_local, torch.cat(bufs, dim=0)[:m].to(A_ks.device)

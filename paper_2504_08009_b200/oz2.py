@@ -31,7 +31,8 @@ SYMBOLS = [
     "oz2_modmul", "oz2_crt", "oz2_tables", "oz2_eq17_k", "oz2_strerror", "oz2_version",
     "oz2_set_profiling", "oz2_stage_times", "oz2_dgemm_op", "oz2_dgemm_strided_batched",
     "oz2_scale_accu", "oz2_dgemm_scaled", "oz2_prepare_b", "oz2_dgemm_prepared", "oz2_release_b",
-    "oz2_set_sm_limit",
+    "oz2_set_sm_limit", "oz2_kslice_stats_rows", "oz2_kslice_stats_cols", "oz2_exponents_from_stats",
+    "oz2_modmul_residues", "oz2_crt_sum",
 ]
 OP_N, OP_T = 0, 1
 # stage 0 times A's conversion (and B's too with OZ2_CONV_OVERLAP=1; the two column
@@ -82,6 +83,11 @@ def lib() -> ctypes.CDLL:
                 L.oz2_dgemm_prepared.argtypes = [P, i64, P, i64, P, i64]
                 L.oz2_release_b.argtypes = [P]
                 L.oz2_set_sm_limit.argtypes = [P, i32]
+                L.oz2_kslice_stats_rows.argtypes = [P, i64, i64, P, i64, P, P, P]
+                L.oz2_kslice_stats_cols.argtypes = [P, i64, i64, P, i64, P, P, P]
+                L.oz2_exponents_from_stats.argtypes = [P, i64, P, P, i64, i32, P]
+                L.oz2_modmul_residues.argtypes = [P, i64, i64, i64, P, P, i64, i32, P, i64]
+                L.oz2_crt_sum.argtypes = [P, i32, i64, i64, P, i64, P, P, i32, P, i64]
                 L.oz2_dgemm_scaled.argtypes = [P, i64, i64, i64, P, i64, P, i64, P, P, P, i64, i32]
                 L.oz2_trunc_rows.argtypes = [P, i64, i64, P, i64, P, P]
                 L.oz2_trunc_cols.argtypes = [P, i64, i64, P, i64, P, P]
@@ -279,6 +285,86 @@ class PreparedB:
 def set_sm_limit(sms: int, device=None):
     """Persistent-GEMM SM budget on this device's handle (0 = all)."""
     _check(lib().oz2_set_sm_limit(handle(device).ptr, int(sms)), "oz2_set_sm_limit")
+
+
+# ---------------------------------------------------------------------------
+# K-split (2-D multi-GPU) pieces: see include/oz2.h
+# ---------------------------------------------------------------------------
+def kslice_stats_rows(A, E_global=None, mode="fast"):
+    """Phase 1 (E_global None): max chunk exponents of the rows of this K slice
+    (int32; INT32_MIN none, INT32_MAX non-finite).  Phase 2: the uint64 partial
+    sums (returned as int64) relative to the global exponents."""
+    import torch
+
+    A = _rowmajor(A, torch.float64)
+    m, k = A.shape
+    h = handle(A.device.index)
+    h.prepare(mode)
+    if E_global is None:
+        E = torch.empty(m, dtype=torch.int32, device=A.device)
+        _check(lib().oz2_kslice_stats_rows(h.ptr, m, k, _vp(A), _ld(A), None, _vp(E), None), "oz2_kslice_stats_rows")
+        return E
+    S = torch.empty(m, dtype=torch.int64, device=A.device)
+    _check(lib().oz2_kslice_stats_rows(h.ptr, m, k, _vp(A), _ld(A), _vp(E_global.contiguous()), None, _vp(S)),
+           "oz2_kslice_stats_rows")
+    return S
+
+
+def kslice_stats_cols(B, E_global=None, mode="fast"):
+    import torch
+
+    B = _rowmajor(B, torch.float64)
+    k, n = B.shape
+    h = handle(B.device.index)
+    h.prepare(mode, 16 * n * ((k + 255) // 256) + 4 * n + 4096)
+    if E_global is None:
+        E = torch.empty(n, dtype=torch.int32, device=B.device)
+        _check(lib().oz2_kslice_stats_cols(h.ptr, k, n, _vp(B), _ld(B), None, _vp(E), None), "oz2_kslice_stats_cols")
+        return E
+    S = torch.empty(n, dtype=torch.int64, device=B.device)
+    _check(lib().oz2_kslice_stats_cols(h.ptr, k, n, _vp(B), _ld(B), _vp(E_global.contiguous()), None, _vp(S)),
+           "oz2_kslice_stats_cols")
+    return S
+
+
+def exponents_from_stats(E, S, k_total: int, N: int, mode="fast"):
+    import torch
+
+    cnt = E.numel()
+    e = torch.empty(cnt, dtype=torch.int32, device=E.device)
+    h = handle(E.device.index)
+    h.prepare(mode)
+    _check(lib().oz2_exponents_from_stats(h.ptr, cnt, _vp(E.contiguous()), _vp(S.contiguous()), int(k_total), N,
+                                          _vp(e)), "oz2_exponents_from_stats")
+    return e
+
+
+def modmul_residues(Ares, Bres, k: int, rows_per_block: int = 0):
+    """Lines 6-7: uint8 c''_t planes, [ceil(m/rpb)][N][rpb][n] (rpb = m: [1][N][m][n])."""
+    import torch
+
+    N, m, ldr = Ares.shape
+    n = Bres.shape[1]
+    rpb = rows_per_block or m
+    nblk = (m + rpb - 1) // rpb
+    R = torch.empty((nblk, N, rpb, n), dtype=torch.uint8, device=Ares.device)
+    h = handle(Ares.device.index)
+    h.prepare("fast", workspace_bytes(m, n, k, N))
+    _check(lib().oz2_modmul_residues(h.ptr, m, n, k, _vp(Ares), _vp(Bres), ldr, N, _vp(R), rpb),
+           "oz2_modmul_residues")
+    return R
+
+
+def crt_sum(R, parts: int, part_stride: int, m: int, n: int, e, f, N: int, out=None):
+    """Lines 7-10 over `parts` partial residue planes: C = D^-1 X E^-1."""
+    import torch
+
+    C = out if out is not None else torch.empty((m, n), dtype=torch.float64, device=R.device)
+    h = handle(R.device.index)
+    h.prepare("fast")
+    _check(lib().oz2_crt_sum(h.ptr, parts, m, n, _vp(R), part_stride, _vp(e.contiguous()), _vp(f.contiguous()), N,
+                             _vp(C), _ld(C)), "oz2_crt_sum")
+    return C
 
 
 def dgemm_scaled(A, B, e, f, num_moduli: int = 14, out=None):
