@@ -50,6 +50,9 @@ def parse():
                    help="Alg. 1 line-1 rule: OS II-fast (headline), OS II-accu or Eq. (17)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    p.add_argument("--parallel", default="rowblock", choices=["rowblock", "ksplit"],
+                   help="multi-GPU partition: output row blocks (weak scaling, the default) or the "
+                        "inner dimension (K-split, strong scaling of one m x n x k product)")
     p.add_argument("--chunks", type=int, default=0, help="multi-GPU gather pipeline pieces (0: auto)")
     p.add_argument("--reserve-sms", type=int, default=8, help="SMs left to NCCL when chunks > 1")
     p.add_argument("--no-e2e", action="store_true")
@@ -200,8 +203,9 @@ def main():
            "config": {"workload": f"m=n=k={n}, N={N}, phi={args.phi:g}" if m == n == k else
                       f"m={m}, n={n}, k={k}, N={N}, phi={args.phi:g}",
                       "m_per_rank": m, "n": n, "k": k, "num_moduli": N, "phi": args.phi,
-                      "parallelism": f"rowblock-dp{world}" if world > 1 else "single-gpu",
-                      "gather": "rank 0, NCCL, pipelined in row pieces" if world > 1 else None,
+                      "parallelism": f"{args.parallel}-dp{world}" if world > 1 else "single-gpu",
+                      "gather": ("rank 0, NCCL, pipelined in row pieces" if args.parallel == "rowblock" else
+                                 "stats all-reduces + residue all-to-all + rank-0 gather") if world > 1 else None,
                       "l2": "no flush: every step streams A, B (2.1 GB each at n=16384) > 126 MB L2",
                       "mode": {"fast": "fast (OS II-fast, Cauchy-Schwarz)",
                                "accu": "accu (OS II-accu, INT8 bound GEMM)",
@@ -228,10 +232,22 @@ def main():
         else:
             dist.init_process_group("gloo")
 
+    ksplit = world > 1 and args.parallel == "ksplit"
     # inputs resident in HBM before the timed region
-    A = phi_matrix_torch(m, k, args.phi, SEED_A, device=dev, row_offset=rank * m)
-    B = phi_matrix_torch(k, n, args.phi, SEED_B, device=dev) if rank == 0 else \
-        torch.empty((k, n), dtype=torch.float64, device=dev)
+    if ksplit:
+        # K-split: one m x n x k product, rank r holds A[:, K_r] and B[K_r, :]
+        from paper_2504_08009_b200.dist import dgemm_ksplit, kslice_partition
+        ka, kb = kslice_partition(k, world, rank)
+        A = phi_matrix_torch(m, k, args.phi, SEED_A, device=dev)
+        B = phi_matrix_torch(k, n, args.phi, SEED_B, device=dev)
+        A_ks, B_ks = A[:, ka:kb].contiguous(), B[ka:kb].contiguous()
+        if rank != 0:
+            del A, B
+            A = B = None
+    else:
+        A = phi_matrix_torch(m, k, args.phi, SEED_A, device=dev, row_offset=rank * m)
+        B = phi_matrix_torch(k, n, args.phi, SEED_B, device=dev) if rank == 0 else \
+            torch.empty((k, n), dtype=torch.float64, device=dev)
     C = torch.empty((m, n), dtype=torch.float64, device=dev)
     h = oz2.handle(local)
 
@@ -241,11 +257,15 @@ def main():
     # `chunks` pieces whose NCCL gathers overlap the next piece's GEMM on SMs
     # left free by the GEMM's SM budget (at 4+ GPUs, where the gather is large)
     chunks = args.chunks if args.chunks else (4 if world >= 4 else 1)
-    if world > 1 and chunks > 1:
+    if world > 1 and chunks > 1 and not ksplit:
         oz2.set_sm_limit(torch.cuda.get_device_properties(dev).multi_processor_count - args.reserve_sms, local)
 
     def step():
-        if world > 1:
+        if ksplit:
+            _, C_full = dgemm_ksplit(A_ks, B_ks, k, N, args.mode)
+            if rank == 0:
+                C.copy_(C_full)
+        elif world > 1:
             # B broadcast from rank 0, local row block, C gathered to rank 0 (NCCL)
             dgemm_rowblock(A, B, N, args.mode, m_total=m * world, chunks=chunks, C_local=C)
         else:
@@ -280,9 +300,13 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    flops = 2.0 * m * world * n * k
+    flops = 2.0 * m * (1 if ksplit else world) * n * k
     value = flops / (ms_step * 1e-3) / 1e12
 
+    if rank != 0 and ksplit:                  # rank 0 holds the full operands and C
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     # accuracy on sampled entries (bench-local exact reference)
     rng = np.random.Generator(np.random.PCG64(3))
     ii = rng.integers(0, m, args.acc_samples)
@@ -306,7 +330,7 @@ def main():
     # dominant kernel: the tcgen05 modular GEMM (Alg. 1 line 6)
     t_gemm = stages["gemm"] / max(calls, 1)
     int8_ops = 2.0 * m * n * k * N
-    achieved = int8_ops / (t_gemm * 1e-3) / 1e12
+    achieved = int8_ops / (t_gemm * 1e-3) / 1e12 if calls else 0.0
     peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
     traffic = None
     prof = os.path.join(ROOT, "profiles", "gemm_traffic.json")
@@ -325,9 +349,11 @@ def main():
                                "(int8 dense = 2 x bf16 nominal)",
                 "work": f"2*m*n*k*N = {int8_ops:.4g} int8 ops per launch"}
 
+    if not calls:                              # K-split path: no oz2_dgemm_ex stages to time
+        roofline = None
     line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int8 (tensor-core s8*s8->s32), f64 in/out",
+            "scaling": "strong" if ksplit else "weak", "vs_baseline": None, "dtype": "int8 (tensor-core s8*s8->s32), f64 in/out",
             "data": "synthetic", "config": cfg["config"],
             "max_rel_err": relerr, "compwise_err": compwise, "acc_samples": int(args.acc_samples),
             "stage_ms": {s: v / max(calls, 1) for s, v in stages.items()},

@@ -8,3 +8,7 @@ for extra in "--chunks 1" "--chunks 3" "--chunks 2 --mode accu"; do
     > gpurun_out/dist_check.json 2> gpurun_out/dist_check.err; echo "dist check [$extra] rc=$?"
   python -c "import json; d=json.load(open('gpurun_out/dist_check.json')); print(d['value'], d['compwise_err'], d['max_rel_err'], d['config']['workload'])"; grep -i error gpurun_out/dist_check.err | tail -3
 done
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 \
+  bench.py --gpus 2 --steps 2 --warmup 3 --size 2048 --k 4096 --dist-backend gloo --parallel ksplit --no-e2e --no-context --no-cpu-baseline \
+  > gpurun_out/dist_check.json 2> gpurun_out/dist_check.err; echo "dist check [ksplit] rc=$?"
+python -c "import json; d=json.load(open('gpurun_out/dist_check.json')); print(d['value'], d['compwise_err'], d['max_rel_err'], d['config']['workload'], d['config']['parallelism'], d['scaling'])"; grep -i error gpurun_out/dist_check.err | tail -3
