@@ -135,6 +135,7 @@ struct Layout {
     int64_t ldr;
     size_t off_Ares, off_Bres, off_e, off_f, off_stats, off_scratch, off_sync;
     size_t off_E, off_F, off_pr, off_pc;     // accu line 1: max exponents, row / column maxima of P
+    size_t off_R;                            // small problems: uint8 c''_t planes [N][m][n]
     size_t total;
 };
 
@@ -155,6 +156,7 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms, int64_t s
     L.off_F = take(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
     L.off_pr = take(sizeof(uint32_t) * (size_t)(m > 0 ? m : 1));
     L.off_pc = take(sizeof(uint32_t) * (size_t)(n > 0 ? n : 1));
+    L.off_R = take(oz2::gemm_unit_parallel(m, n, num_sms) ? (size_t)N * (size_t)m * (size_t)n : 0);
     L.total = off;
     return L;
 }
@@ -636,6 +638,19 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
         mark(h);
         convert_B_res(h->stream);
         mark(h);
+    }
+    if (oz2::gemm_unit_parallel(m, n, gemm_sms(h)) && alpha == 1.0 && beta == 0.0) {
+        // small problem (fewer output tiles than CTA pairs): the (tile, modulus)
+        // units spread over all SMs (line 6-7 into uint8 planes), then lines 8-10
+        // in a separate elementwise kernel
+        uint8_t* R = ws + L.off_R;
+        if (oz2::launch_modmul_residues(&tA, &tB, m, n, k, N, scratch, R, m, (uint32_t*)(ws + L.off_sync),
+                                        gemm_sms(h), h->stream))
+            return OZ2_ERR_CUDA;
+        mark(h);
+        oz2::launch_crt_sum(R, 1, (int64_t)N * m * n, m, n, e, f, N, C, ldc, h->stream);
+        mark(h);
+        return cuda_status();
     }
     // Part 2-b (line 6) with Parts 2-c, 3, 4 (lines 7-10) fused into the epilogue
     if (oz2::launch_modmul_fused(&tA, &tB, m, n, k, N, scratch, e, f, C, ldc, (uint32_t*)(ws + L.off_sync),

@@ -92,6 +92,7 @@ struct Params {
     double* C;                      // FUSED
     int64_t ldc;
     int axpby;                      // FUSED: 0 -> C = AB; 1 -> C = alpha AB (+ beta C if beta != 0)
+    int unit_parallel;              // schedule (tile, modulus) units individually (res_out only)
     uint8_t* res_out;               // FUSED, K-split: final c''_t planes to global instead of the CRT
     int64_t res_rpb;                //   layout [m / res_rpb][N][res_rpb][n]
     uint32_t* rowmax;               // BOUND (NM < 0): max_j P_ij, max_i P_ij (atomicMax)
@@ -119,11 +120,19 @@ __device__ __forceinline__ void tile_coords(const Params& p, int j, int& tm, int
 
 template <typename F>
 __device__ __forceinline__ void for_each_unit(const Params& p, int cid, int ncl, F&& fn) {
+    // unit_parallel (small problems, res_out only): the (tile, modulus) units
+    // themselves are spread over the clusters.  One call site of fn: the
+    // epilogue body must stay inlined (a second call site made it a function
+    // with a 600-byte stack frame)
     const int tiles = p.num_tm * p.num_tn;
-    for (int j = cid; j < tiles; j += ncl) {
+    const int total = p.unit_parallel ? tiles * p.N : tiles;
+    for (int j = cid; j < total; j += ncl) {
+        const int tile = p.unit_parallel ? j / p.N : j;
+        const int t0 = p.unit_parallel ? j % p.N : 0;
+        const int t1 = p.unit_parallel ? t0 + 1 : p.N;
         int tm, tn;
-        tile_coords(p, j, tm, tn);
-        for (int t = 0; t < p.N; t++) fn(tm, tn, t);
+        tile_coords(p, tile, tm, tn);
+        for (int t = t0; t < t1; t++) fn(tm, tn, t);
     }
 }
 
@@ -215,6 +224,24 @@ __device__ __forceinline__ void crt_slice(const Params& p, const uint8_t* tile_s
                 if (j < ncol) crow[j] = o[0];
                 if (j + 1 < ncol) crow[j + 1] = o[1];
             }
+        }
+    }
+}
+
+// residues of K chunk ch: stored (ch = 0) or added mod m_t to the earlier chunks'
+template <int NM>
+__device__ __forceinline__ void store_residues(uint4* d4, const uint32_t (&w)[8], int ch, int t) {
+    if (ch == 0) {
+        d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else {
+        if constexpr (NM > 0) {
+            const uint32_t mt = (uint32_t)c_tab[NM].m[t];
+            const uint4 o0 = d4[0], o1 = d4[1];
+            d4[0] = make_uint4(add_mod_bytes(o0.x, w[0], mt), add_mod_bytes(o0.y, w[1], mt),
+                               add_mod_bytes(o0.z, w[2], mt), add_mod_bytes(o0.w, w[3], mt));
+            d4[1] = make_uint4(add_mod_bytes(o1.x, w[4], mt), add_mod_bytes(o1.y, w[5], mt),
+                               add_mod_bytes(o1.z, w[6], mt), add_mod_bytes(o1.w, w[7], mt));
         }
     }
 }
@@ -389,22 +416,6 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 else mbar_arrive(bar);
             }
         };
-        // residues of K chunk ch: stored (ch = 0) or added mod m_t to the earlier chunks'
-        auto store_residues = [&](uint4* d4, const uint32_t (&w)[8], int ch, int t) {
-            if (ch == 0) {
-                d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
-                d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
-            } else {
-                if constexpr (FUSED) {
-                    const uint32_t mt = (uint32_t)c_tab[NM].m[t];
-                    const uint4 o0 = d4[0], o1 = d4[1];
-                    d4[0] = make_uint4(add_mod_bytes(o0.x, w[0], mt), add_mod_bytes(o0.y, w[1], mt),
-                                       add_mod_bytes(o0.z, w[2], mt), add_mod_bytes(o0.w, w[3], mt));
-                    d4[1] = make_uint4(add_mod_bytes(o1.x, w[4], mt), add_mod_bytes(o1.y, w[5], mt),
-                                       add_mod_bytes(o1.z, w[6], mt), add_mod_bytes(o1.w, w[7], mt));
-                }
-            }
-        };
         auto run_slice = [&](int sl) {
           if constexpr (FUSED) {
             const int c = half * CH + (sl >> 2), hh = sl & 3;
@@ -478,7 +489,12 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 // line 7 for this warp's chunks -> uint8 residues in this tile's scratch slot;
                 // TMEM loads double-buffered: chunk cc + 1 is in flight while cc is reduced
                 uint8_t* tile_scr = p.scratch + (((size_t)blockIdx.x * 2 + slot) * NM) * TB + (size_t)t * TB;
+                // only the chunks that hold output columns (and lanes that hold rows) matter:
+                // small / ragged tiles drain a fraction of TMEM
+                const int ch_valid = min(CH, max(0, (p.n - tn * C_::TILE_N - half * CH * 32 + 31) / 32));
+                const bool quad_live = tm * C_::TILE_M + (int)rank * BM + q * 32 < p.m;
                 uint32_t va[32], vb[32];
+                if (quad_live && ch_valid == CH) {
                 tmem_ld_32x32b_x32(tbase + (uint32_t)(half * CH * 32), va);
                 #pragma unroll
                 for (int cc = 0; cc < CH; cc += 2) {
@@ -487,11 +503,22 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     tmem_ld_wait_regs(va);
                     tmem_ld_32x32b_x32(tbase + (uint32_t)((c + 1) * 32), vb);
                     reduce32<NM>(va, t, w);
-                    store_residues(reinterpret_cast<uint4*>(tile_scr + ((size_t)(c * BM + r)) * 32), w, ch, t);
+                    store_residues<NM>(reinterpret_cast<uint4*>(tile_scr + ((size_t)(c * BM + r)) * 32), w, ch, t);
                     tmem_ld_wait_regs(vb);
                     if (cc + 2 < CH) tmem_ld_32x32b_x32(tbase + (uint32_t)((c + 2) * 32), va);
                     reduce32<NM>(vb, t, w);
-                    store_residues(reinterpret_cast<uint4*>(tile_scr + ((size_t)((c + 1) * BM + r)) * 32), w, ch, t);
+                    store_residues<NM>(reinterpret_cast<uint4*>(tile_scr + ((size_t)((c + 1) * BM + r)) * 32), w, ch, t);
+                }
+                } else if (quad_live) {                           // partial tile: the live chunks only
+                    #pragma unroll 1
+                    for (int cc = 0; cc < ch_valid; cc++) {
+                        const int c = half * CH + cc;
+                        uint32_t w[8];
+                        tmem_ld_32x32b_x32(tbase + (uint32_t)(c * 32), va);
+                        tmem_ld_wait_regs(va);
+                        reduce32<NM>(va, t, w);
+                        store_residues<NM>(reinterpret_cast<uint4*>(tile_scr + ((size_t)(c * BM + r)) * 32), w, ch, t);
+                    }
                 }
                 release();
                 if (ch == p.nchunk - 1 && p.res_out) {           // K-split: c''_t out, no CRT here
@@ -510,8 +537,9 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                                 reinterpret_cast<uint4*>(orow + col0)[1] = v1;
                             } else {
                                 const uint32_t wv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-                                for (int b = 0; b < 32 && col0 + b < p.n; b++)
-                                    orow[col0 + b] = (uint8_t)(wv[b >> 2] >> (8 * (b & 3)));
+                                #pragma unroll
+                                for (int b = 0; b < 32; b++)              // constant indices: registers
+                                    if (col0 + b < p.n) orow[col0 + b] = (uint8_t)(wv[b >> 2] >> (8 * (b & 3)));
                             }
                         }
                     }
@@ -631,8 +659,16 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
 size_t fused_scratch_bytes(int64_t m, int64_t n, int N, int num_sms) {
     int grid;
     const int cg = gemm_cta_group(), nh = gemm_halves();
-    make_params(m, n, 1, N, num_sms, cg, nh, &grid);
+    gemm::Params p = make_params(m, n, 1, N, num_sms, cg, nh, &grid);
+    const int tiles = p.num_tm * p.num_tn, ncl_max = num_sms / cg;
+    if (tiles < ncl_max) grid = std::max(grid, std::min(tiles * N, ncl_max) * cg);   // unit-parallel grid
     return (size_t)grid * 2 * N * gemm::BM * gemm::BN * nh;
+}
+
+bool gemm_unit_parallel(int64_t m, int64_t n, int num_sms) {
+    int grid;
+    gemm::Params p = make_params(m, n, 1, 2, num_sms, gemm_cta_group(), gemm_halves(), &grid);
+    return p.num_tm * p.num_tn < num_sms / gemm_cta_group() && env_int("OZ2_UNIT_PARALLEL", 1);
 }
 
 int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
@@ -652,6 +688,17 @@ int launch_modmul_residues(const CUtensorMap* tmA, const CUtensorMap* tmB, int64
                            cudaStream_t st) {
     int grid;
     gemm::Params p = make_params(m, n, k, N, num_sms, gemm_cta_group(), gemm_halves(), &grid);
+    {
+        // fewer tiles than clusters: spread the (tile, modulus) units instead
+        const int tiles = p.num_tm * p.num_tn, ncl_max = num_sms / gemm_cta_group();
+        if (tiles < ncl_max && env_int("OZ2_UNIT_PARALLEL", 1)) {
+            p.unit_parallel = 1;
+            grid = std::min(tiles * N, ncl_max) * gemm_cta_group();
+            const int ncl = grid / gemm_cta_group();
+            const int64_t kbs = (int64_t)((tiles * N + ncl - 1) / ncl) * p.num_kb;
+            p.sync_steps_max = p.sync_kb > 0 ? (int)((kbs + p.sync_kb - 1) / p.sync_kb) + 1 : 0;
+        }
+    }
     p.scratch = scratch;
     p.res_out = R;
     p.res_rpb = rows_per_block > 0 ? rows_per_block : m;

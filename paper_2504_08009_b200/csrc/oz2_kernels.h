@@ -40,6 +40,8 @@ int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int
                   int N, int32_t* cprod, uint32_t* sync_ctr, int num_sms, cudaStream_t st);
 // + Alg. 1 lines 7-10 fused into the epilogue (uint8 residue scratch, exact CRT)
 size_t fused_scratch_bytes(int64_t m, int64_t n, int N, int num_sms);
+// fewer output tiles than CTA pairs: spread (tile, modulus) units (launch_modmul_residues + CRT kernel)
+bool gemm_unit_parallel(int64_t m, int64_t n, int num_sms);
 // (alpha, beta) != (1, 0): C = alpha AB + beta C in the epilogue (BLAS semantics)
 int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                         int N, uint8_t* scratch, const int32_t* e, const int32_t* f, double* C, int64_t ldc,

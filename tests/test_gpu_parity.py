@@ -364,3 +364,24 @@ def test_prepared_b_and_sm_limit(oz2, oracle):
     finally:
         oz2.set_sm_limit(0)
     assert_bitwise(C, oz2.dgemm(Ad, Bd, 14).cpu().numpy(), "sm limit 100")
+
+
+def test_cuda_graph_capture(oz2, oracle):
+    """oz2_dgemm is capturable (no host synchronisation, no allocation once the
+    workspace exists): a CUDA graph of the whole Algorithm 1 replays bit-identically
+    -- the launch-bound small sizes (config c1) are meant to run this way."""
+    A = torch.from_numpy(phi_matrix_np(64, 64, 0.5, seed=131)).to(DEV)
+    B = torch.from_numpy(phi_matrix_np(64, 64, 0.5, seed=132)).to(DEV)
+    C = torch.empty((64, 64), dtype=torch.float64, device=DEV)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        oz2.dgemm(A, B, 14, out=C)                        # warm-up: workspace, TMA encode, attributes
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            oz2.dgemm(A, B, 14, out=C)
+    torch.cuda.current_stream().wait_stream(s)
+    C.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert_bitwise(C.cpu().numpy(), oracle.dgemm(A.cpu().numpy(), B.cpu().numpy(), 14), "graph replay")
