@@ -627,6 +627,11 @@ int gemm_cta_group() { return env_int("OZ2_CG", 2) == 1 ? 1 : 2; }
 int gemm_halves() { return gemm_cta_group() == 2 && env_int("OZ2_NH", 2) == 2 ? 2 : 1; }
 static int gemm_shape() { return gemm_cta_group() * 10 + gemm_halves(); }
 
+// threshold in output tiles below which the unit-parallel path is used
+static int unit_parallel_tiles(int num_sms) {
+    return env_int("OZ2_UNIT_PARALLEL", 1) ? env_int("OZ2_UP_TILES", num_sms / gemm_cta_group()) : 0;
+}
+
 static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_sms, int cg, int nh, int* grid_out) {
     using namespace gemm;
     Params p{};
@@ -661,14 +666,14 @@ size_t fused_scratch_bytes(int64_t m, int64_t n, int N, int num_sms) {
     const int cg = gemm_cta_group(), nh = gemm_halves();
     gemm::Params p = make_params(m, n, 1, N, num_sms, cg, nh, &grid);
     const int tiles = p.num_tm * p.num_tn, ncl_max = num_sms / cg;
-    if (tiles < ncl_max) grid = std::max(grid, std::min(tiles * N, ncl_max) * cg);   // unit-parallel grid
+    if (tiles < unit_parallel_tiles(num_sms)) grid = std::max(grid, std::min(tiles * N, ncl_max) * cg);   // unit-parallel
     return (size_t)grid * 2 * N * gemm::BM * gemm::BN * nh;
 }
 
 bool gemm_unit_parallel(int64_t m, int64_t n, int num_sms) {
     int grid;
     gemm::Params p = make_params(m, n, 1, 2, num_sms, gemm_cta_group(), gemm_halves(), &grid);
-    return p.num_tm * p.num_tn < num_sms / gemm_cta_group() && env_int("OZ2_UNIT_PARALLEL", 1);
+    return p.num_tm * p.num_tn < unit_parallel_tiles(num_sms);
 }
 
 int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
@@ -691,7 +696,7 @@ int launch_modmul_residues(const CUtensorMap* tmA, const CUtensorMap* tmB, int64
     {
         // fewer tiles than clusters: spread the (tile, modulus) units instead
         const int tiles = p.num_tm * p.num_tn, ncl_max = num_sms / gemm_cta_group();
-        if (tiles < ncl_max && env_int("OZ2_UNIT_PARALLEL", 1)) {
+        if (tiles < unit_parallel_tiles(num_sms)) {
             p.unit_parallel = 1;
             grid = std::min(tiles * N, ncl_max) * gemm_cta_group();
             const int ncl = grid / gemm_cta_group();

@@ -85,25 +85,59 @@ __global__ void exponents_from_stats_kernel(const int32_t* __restrict__ E, const
 }
 
 // lines 7-10 for G partial products: c''_t = (sum_g R[g][t][i][j]) mod m_t, then
-// the CRT and scaling (crt_from_packed).  R[g] at R + g * part_stride, [N][m][n]
+// the CRT and scaling (crt_from_packed).  R[g] at R + g * part_stride, [N][m][n].
+// One thread per row i and 4 consecutive columns: one 4-byte load per plane
+// (coalesced rows), no 64-bit index division; G = 1 (the single-GPU small-problem
+// path) needs no reduction at all -- the planes already hold c''_t.
 template <int NM>
 __global__ void __launch_bounds__(256)
 crt_sum_kernel(const uint8_t* __restrict__ R, int G, int64_t part_stride, int64_t m, int64_t n,
                const int32_t* __restrict__ e, const int32_t* __restrict__ f, double* __restrict__ C, int64_t ldc) {
-    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (idx >= m * n) return;
-    const int64_t i = idx / n, j = idx % n;
     constexpr int G4 = (NM + 3) / 4;
-    uint32_t P[G4];
-    #pragma unroll
-    for (int g = 0; g < G4; g++) P[g] = 0;
-    #pragma unroll
-    for (int t = 0; t < NM; t++) {
-        int32_t s = 0;
-        for (int g = 0; g < G; g++) s += R[(int64_t)g * part_stride + ((int64_t)t * m) * n + idx];
-        P[t / 4] |= reduce_line7<NM>(s, t) << (8 * (t % 4));
+    const int64_t c0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+    if (c0 >= n) return;
+    const bool full = c0 + 4 <= n && (n & 3) == 0;
+    for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
+        uint32_t wt[NM];                                   // byte j of wt[t] = c''_t of column c0 + j
+        #pragma unroll
+        for (int t = 0; t < NM; t++) {
+            const uint8_t* base = R + ((int64_t)t * m + i) * n + c0;
+            if (G == 1) {
+                if (full) {
+                    wt[t] = *reinterpret_cast<const uint32_t*>(base);
+                } else {
+                    uint32_t w = 0;
+                    for (int j = 0; j < 4; j++) if (c0 + j < n) w |= (uint32_t)base[j] << (8 * j);
+                    wt[t] = w;
+                }
+            } else {
+                int32_t s4[4] = {0, 0, 0, 0};
+                for (int g = 0; g < G; g++) {
+                    const uint8_t* b = base + (int64_t)g * part_stride;
+                    #pragma unroll
+                    for (int j = 0; j < 4; j++) if (c0 + j < n) s4[j] += b[j];
+                }
+                uint32_t w = 0;
+                #pragma unroll
+                for (int j = 0; j < 4; j++) w |= reduce_line7<NM>(s4[j], t) << (8 * j);
+                wt[t] = w;
+            }
+        }
+        uint32_t P[4][G4];
+        #pragma unroll
+        for (int g = 0; g < G4; g++) {
+            uint32_t o[4];
+            transpose4x4(wt[4 * g], 4 * g + 1 < NM ? wt[4 * g + 1] : 0u, 4 * g + 2 < NM ? wt[4 * g + 2] : 0u,
+                         4 * g + 3 < NM ? wt[4 * g + 3] : 0u, o);
+            #pragma unroll
+            for (int j = 0; j < 4; j++) P[j][g] = o[j];
+        }
+        const int ei = e[i];
+        double* crow = C + i * ldc + c0;
+        #pragma unroll
+        for (int j = 0; j < 4; j++)
+            if (c0 + j < n) crow[j] = crt_from_packed<NM>(P[j], ei, __ldg(f + c0 + j));
     }
-    C[i * ldc + j] = crt_from_packed<NM>(P, e[i], f[j]);
 }
 
 void launch_kslice_rows(const double* A, int64_t m, int64_t k, int64_t lda, int mode, const int32_t* Eg,
@@ -142,8 +176,8 @@ void launch_exponents_from_stats(const int32_t* E, const unsigned long long* S, 
 template <int NM>
 static void launch_crt_sum_nm(const uint8_t* R, int G, int64_t part_stride, int64_t m, int64_t n, const int32_t* e,
                               const int32_t* f, double* C, int64_t ldc, cudaStream_t st) {
-    const int64_t tot = m * n;
-    crt_sum_kernel<NM><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(R, G, part_stride, m, n, e, f, C, ldc);
+    dim3 grid((unsigned)((n + 4 * 64 - 1) / (4 * 64)), (unsigned)(m < 65535 ? m : 65535));
+    crt_sum_kernel<NM><<<grid, 64, 0, st>>>(R, G, part_stride, m, n, e, f, C, ldc);
 }
 
 void launch_crt_sum(const uint8_t* R, int G, int64_t part_stride, int64_t m, int64_t n, const int32_t* e,
