@@ -9,4 +9,9 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 timeout 600 python bench.py --mode accu --no-e2e --no-context --no-cpu-baseline > gpurun_out/bench_accu.json 2>&1; echo "bench accu rc=$?"
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2>&1; echo "ref rc=$?"; cat gpurun_out/bench_ref.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-context --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; echo "ncu list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"modmul|rows_kernel|cols_stats|cols_residues" -s 4 -c 4 -o gpurun_out/prof_full python bench.py --steps 1 --warmup 1 --no-e2e --no-context --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"modmul|rows_kernel|cols_stats|cols_residues" -s 4 -c 4 -o /tmp/prof_full python bench.py --steps 1 --warmup 1 --no-e2e --no-context --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+# the .ncu-rep stays on the box (too large for gpurun_out): bring back the summary, raw and source pages
+python tools/ncu_summary.py /tmp/prof_full.ncu-rep > gpurun_out/ncu_full_summary.txt 2>&1
+ncu -i /tmp/prof_full.ncu-rep --page raw --csv > gpurun_out/ncu_full_raw.csv 2>/dev/null
+ncu -i /tmp/prof_full.ncu-rep --page details --csv > gpurun_out/ncu_full_details.csv 2>/dev/null
+ls -la gpurun_out; du -sh gpurun_out
