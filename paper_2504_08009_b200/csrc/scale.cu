@@ -19,6 +19,8 @@
 
 #include <stdlib.h>
 
+#include <algorithm>
+
 namespace oz2 {
 
 constexpr int KC = 256;            // FAST chunk length (reading R4)
@@ -67,11 +69,27 @@ __device__ __forceinline__ uint32_t residue_odd(int t, const uint32_t (&w)[3]) {
     return q * T.negm[t] + y;                                   // y - q m_t (mod 2^32)
 }
 
-// U = trunc(2^e a) + 2^63 (WORDS = 2) or + 2^95 (WORDS = 3) as words; zeros
-// (residue 0 after the bias is undone... not used) for e = sentinel -> x = 0
+// 2^e as the product s1 * s2 of two doubles (the two multiplications of
+// scale_pow2, hoisted out of the per-element loops: x s1 s2 is bitwise
+// scale_pow2(x, e) for every finite x)
+__device__ __forceinline__ void pow2_factors(int e, double& s1, double& s2) {
+    if (e > 1023) {
+        s1 = __longlong_as_double((long long)(1023 + 1023) << 52);    // 2^1023
+        s2 = __longlong_as_double((long long)(e - 1023 + 1023) << 52);
+    } else if (e < -1022) {
+        s1 = __longlong_as_double((long long)1 << 52);                // 2^-1022
+        s2 = e + 1022 < -1022 ? 0.0 : __longlong_as_double((long long)(e + 1022 + 1023) << 52);
+    } else {
+        s1 = __longlong_as_double((long long)(e + 1023) << 52);
+        s2 = 1.0;
+    }
+}
+
+// U = trunc(2^e a) + 2^63 (WORDS = 2) or + 2^95 (WORDS = 3) as words, with
+// 2^e = s1 s2 (pow2_factors); a = 0 for rows / columns of the exponent sentinel
 template <int WORDS>
-__device__ __forceinline__ void to_words(double a, int e, uint32_t (&w)[3]) {
-    double v = e == OZ2_EXP_NONFINITE_DEV ? 0.0 : scale_pow2(a, e);
+__device__ __forceinline__ void to_words(double a, double s1, double s2, uint32_t (&w)[3]) {
+    double v = (a * s1) * s2;
     if (WORDS == 2) {
         const long long x = __double2ll_rz(v);                  // trunc
         w[0] = (uint32_t)x;
@@ -256,39 +274,52 @@ __device__ int row_exponent(const double* __restrict__ X, int64_t k, int Tb, int
     return sm.misc[1];
 }
 
-// residues of one row for all N moduli: planes out[t][l], 8 elements per thread
-// per step (64 B loads, 8 B streaming stores per modulus; a warp covers 256
-// consecutive elements and writes 256 contiguous bytes of every plane)
+// residues of one row for all N moduli: planes out[t][l], RV elements per
+// thread per step (RV = 16: 128 B of loads, one 16-byte streaming store per
+// modulus; the plane row stride is a multiple of 16, so the last step may write
+// residues of zeros into [k, round_up(k, 16)), inside the row's ld_res bytes)
+constexpr int RV = 16;
 template <int NM, int WORDS>
 __device__ void row_residues(const double* __restrict__ X, int64_t k, int e, int8_t* __restrict__ out,
                              int64_t plane_stride) {
     const bool vec = ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
     const uint64_t pol = l2_evict_first();
-    for (int64_t l0 = 8 * (int64_t)threadIdx.x; l0 < k; l0 += 8 * (int64_t)blockDim.x) {
-        double a[8];
-        if (vec && l0 + 8 <= k) {
+    const int64_t step = RV * (int64_t)blockDim.x;
+    if (e == OZ2_EXP_NONFINITE_DEV) {                 // x = 0: every residue is 0
+        for (int64_t l0 = RV * (int64_t)threadIdx.x; l0 < k; l0 += step)
+            #pragma unroll 1
+            for (int t = 0; t < NM; t++) st_cs_v4(out + t * plane_stride + l0, 0u, 0u, 0u, 0u);
+        return;
+    }
+    double s1, s2;
+    pow2_factors(e, s1, s2);
+    for (int64_t l0 = RV * (int64_t)threadIdx.x; l0 < k; l0 += step) {
+        double a[RV];
+        if (vec && l0 + RV <= k) {
             #pragma unroll
-            for (int j = 0; j < 4; j++) {
+            for (int j = 0; j < RV / 2; j++) {
                 const double2 p = ld2_hint(X + l0 + 2 * j, pol);
                 a[2 * j] = p.x; a[2 * j + 1] = p.y;
             }
         } else {
             #pragma unroll
-            for (int j = 0; j < 8; j++) a[j] = (l0 + j < k) ? ld1_hint(X + l0 + j, pol) : 0.0;
+            for (int j = 0; j < RV; j++) a[j] = (l0 + j < k) ? ld1_hint(X + l0 + j, pol) : 0.0;
         }
-        uint32_t w[8][3];
+        uint32_t w[RV][3];
         #pragma unroll
-        for (int j = 0; j < 8; j++) to_words<WORDS>(a[j], e, w[j]);
+        for (int j = 0; j < RV; j++) to_words<WORDS>(a[j], s1, s2, w[j]);
+        int8_t* o = out + l0;
         // t = 0: m = 256, the low byte of x
-        st_cs_v2(out + l0, pack_lo_bytes(w[0][0], w[1][0], w[2][0], w[3][0]),
-                 pack_lo_bytes(w[4][0], w[5][0], w[6][0], w[7][0]));
+        st_cs_v4(o, pack_lo_bytes(w[0][0], w[1][0], w[2][0], w[3][0]), pack_lo_bytes(w[4][0], w[5][0], w[6][0], w[7][0]),
+                 pack_lo_bytes(w[8][0], w[9][0], w[10][0], w[11][0]), pack_lo_bytes(w[12][0], w[13][0], w[14][0], w[15][0]));
         #pragma unroll
         for (int t = 1; t < NM; t++) {
-            uint32_t r[8];
+            uint32_t r[RV];
             #pragma unroll
-            for (int j = 0; j < 8; j++) r[j] = residue_odd<NM, WORDS>(t, w[j]);
-            st_cs_v2(out + t * plane_stride + l0, pack_lo_bytes(r[0], r[1], r[2], r[3]),
-                     pack_lo_bytes(r[4], r[5], r[6], r[7]));
+            for (int j = 0; j < RV; j++) r[j] = residue_odd<NM, WORDS>(t, w[j]);
+            o += plane_stride;
+            st_cs_v4(o, pack_lo_bytes(r[0], r[1], r[2], r[3]), pack_lo_bytes(r[4], r[5], r[6], r[7]),
+                     pack_lo_bytes(r[8], r[9], r[10], r[11]), pack_lo_bytes(r[12], r[13], r[14], r[15]));
         }
     }
 }
@@ -307,17 +338,19 @@ rows_kernel(const double* __restrict__ A, int64_t m, int64_t k, int64_t lda, int
     sm.Sc = reinterpret_cast<unsigned long long*>(row_smem);
     sm.Ec = reinterpret_cast<int*>(row_smem + sizeof(unsigned long long) * (nch > 0 ? nch : 1));
     sm.misc = sm.Ec + (nch > 0 ? nch : 1);
-    const int64_t i = blockIdx.x;
-    if (i >= m) return;
-    const double* X = A + i * lda;
-    int e;
-    if (what & 1) {
-        e = row_exponent<MODE>(X, k, c_tab[NM].T, kstar, sm);
-        if (threadIdx.x == 0) e_io[i] = e;
-    } else {
-        e = e_io[i];
+    // rows blockIdx.x, + gridDim.x, ...: a grid of a few CTAs per SM keeps the
+    // rows in flight (x 8k bytes) small enough that pass 2 re-reads them from L2
+    for (int64_t i = blockIdx.x; i < m; i += gridDim.x) {
+        const double* X = A + i * lda;
+        int e;
+        if (what & 1) {
+            e = row_exponent<MODE>(X, k, c_tab[NM].T, kstar, sm);
+            if (threadIdx.x == 0) e_io[i] = e;
+        } else {
+            e = e_io[i];
+        }
+        if (what & 2) row_residues<NM, WORDS>(X, k, e, res + i * ldr, m * ldr);
     }
-    if (what & 2) row_residues<NM, WORDS>(X, k, e, res + i * ldr, m * ldr);
 }
 
 // A' = trunc(D A) as FP64 (split API)
@@ -433,12 +466,15 @@ cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t
     const uint64_t pol = l2_evict_first();
     {
         const int e = j < n ? f[j] : 0;
+        const bool live = j < n && e != OZ2_EXP_NONFINITE_DEV;     // sentinel column: x = 0
+        double s1, s2;
+        pow2_factors(e, s1, s2);
         uint32_t w[8][3];
         #pragma unroll
         for (int q = 0; q < 8; q++) {
             const int64_t l = l0 + warp * 8 + q;
-            const double a = (j < n && l < k) ? ld1_hint(B + l * ldb + j, pol) : 0.0;
-            to_words<WORDS>(a, e, w[q]);
+            const double a = (live && l < k) ? ld1_hint(B + l * ldb + j, pol) : 0.0;
+            to_words<WORDS>(a, s1, s2, w[q]);
         }
         const int chunk = warp ^ (lane & 7);                 // swizzled 8-byte chunk within the 64 B row
         #pragma unroll
@@ -489,7 +525,17 @@ static void launch_rows_nm(const double* A, int64_t m, int64_t k, int64_t lda, i
                            int kstar, int32_t* e, int8_t* res, int64_t ldr, cudaStream_t st) {
     constexpr int W = NM <= 16 ? 2 : 3;
     static const int threads = [] { const char* v = getenv("OZ2_ROW_THREADS"); return v && atoi(v) == 512 ? 512 : 256; }();
-    dim3 grid((unsigned)m), block((unsigned)threads);
+    // OZ2_ROW_CTAS_PER_SM = R > 0: a persistent grid of R CTAs per SM (rows in
+    // flight R * SMs, each 8k bytes, sized against the L2); 0: one CTA per row
+    static const int per_sm = [] { const char* v = getenv("OZ2_ROW_CTAS_PER_SM"); return v && *v ? atoi(v) : 0; }();
+    int64_t g = m;
+    if (per_sm > 0) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        g = std::min<int64_t>(m, (int64_t)sms * per_sm);
+    }
+    dim3 grid((unsigned)g), block((unsigned)threads);
     const size_t smem = row_smem_bytes(k);
     auto kern = threads == 512 ? (mode == 0 ? rows_kernel<NM, W, 0, 512> : rows_kernel<NM, W, 1, 512>)
                                : (mode == 0 ? rows_kernel<NM, W, 0, 256> : rows_kernel<NM, W, 1, 256>);
