@@ -173,6 +173,11 @@ __device__ __forceinline__ double u_sq(double x, double s1, double s2) {
     const double u = fmax(1.0, ceil(fabs(x) * s1 * s2));
     return x != 0.0 ? u * u : 0.0;
 }
+// the same for s2 = 1 (every chunk whose maximum is a normal number >= 2^-1008)
+__device__ __forceinline__ double u_sq1(double x, double s1) {
+    const double u = fmax(1.0, ceil(fabs(x) * s1));
+    return x != 0.0 ? u * u : 0.0;
+}
 
 // per-row chunk statistics in dynamic shared memory: Sc[nch], Ec[nch], then bad, e
 struct RowSmem {
@@ -219,44 +224,87 @@ __device__ void row_chunk_stats(const double* __restrict__ X, int64_t k, RowSmem
     const uint64_t pol = l2_evict_last();
     if (threadIdx.x == 0) sm.misc[0] = 0;
     __syncthreads();
-    for (int c = warp; c < nch; c += nwarps) {
-        double v[KC / 32];
-        const int64_t base = (int64_t)c * KC;
-        if (vec && base + KC <= k) {
-            #pragma unroll
-            for (int j = 0; j < KC / 64; j++) {
-                const double2 p = ld2_hint(X + base + 2 * lane + 64 * j, pol);
-                v[2 * j] = p.x; v[2 * j + 1] = p.y;
-            }
-        } else {
-            #pragma unroll
-            for (int j = 0; j < KC / 32; j++) {
-                const int64_t l = base + lane + 32 * j;
-                v[j] = l < k ? ld1_hint(X + l, pol) : 0.0;
-            }
-        }
-        uint64_t mb = 0;
+    // CU chunks per warp and step (c, c + nwarps, ...): all their loads are in
+    // flight before the first reduction.  The chunk maximum comes from the high
+    // words of |x| (exponent field; >= 0x7ff00000 flags Inf/NaN); a chunk whose
+    // maximum is subnormal or zero takes the full 64-bit patterns (warp-uniform)
+    constexpr int CU = 2, VP = KC / 32;
+    for (int c0 = warp; c0 < nch; c0 += CU * nwarps) {
+        double v[CU][VP];
         #pragma unroll
-        for (int j = 0; j < KC / 32; j++) {
-            const uint64_t b = (uint64_t)__double_as_longlong(v[j]) & ABS_MASK;
-            mb = b > mb ? b : mb;
-        }
-        mb = warp_max64(mb);
-        int Ec = INT32_MIN;
-        double S = 0.0;
-        if (mb >= INF_BITS) {
-            if (lane == 0) sm.misc[0] = 1;
-        } else if (mb != 0) {
-            Ec = ilogb_bits(mb);
-            if (MODE == 0) {
-                double s1, s2;
-                u_scale(Ec, s1, s2);
+        for (int u = 0; u < CU; u++) {
+            const int c = c0 + u * nwarps;
+            const int64_t base = (int64_t)c * KC;
+            if (c < nch && vec && base + KC <= k) {
                 #pragma unroll
-                for (int j = 0; j < KC / 32; j++) S += u_sq(v[j], s1, s2);
-                S = warp_sumd(S);
+                for (int j = 0; j < VP / 2; j++) {
+                    const double2 p = ld2_hint(X + base + 2 * lane + 64 * j, pol);
+                    v[u][2 * j] = p.x; v[u][2 * j + 1] = p.y;
+                }
+            } else {
+                #pragma unroll
+                for (int j = 0; j < VP; j++) {
+                    const int64_t l = base + lane + 32 * j;
+                    v[u][j] = (c < nch && l < k) ? ld1_hint(X + l, pol) : 0.0;
+                }
             }
         }
-        if (lane == 0) { sm.Ec[c] = Ec; sm.Sc[c] = (unsigned long long)S; }
+        uint32_t mh[CU];
+        #pragma unroll
+        for (int u = 0; u < CU; u++) {
+            mh[u] = 0;
+            #pragma unroll
+            for (int j = 0; j < VP; j++) mh[u] = max(mh[u], (uint32_t)__double2hiint(v[u][j]) & 0x7fffffffu);
+        }
+        #pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            #pragma unroll
+            for (int u = 0; u < CU; u++) mh[u] = max(mh[u], __shfl_xor_sync(0xffffffffu, mh[u], o));
+        }
+        int Ec[CU];
+        double S[CU];
+        #pragma unroll
+        for (int u = 0; u < CU; u++) {
+            S[u] = 0.0;
+            if (mh[u] >= (uint32_t)(INF_BITS >> 32)) {
+                Ec[u] = INT32_MIN;
+                if (lane == 0 && c0 + u * nwarps < nch) sm.misc[0] = 1;
+            } else if (mh[u] >= 0x00100000u) {
+                Ec[u] = (int)(mh[u] >> 20) - 1023;
+            } else {
+                uint64_t mb = 0;
+                #pragma unroll
+                for (int j = 0; j < VP; j++) {
+                    const uint64_t b = (uint64_t)__double_as_longlong(v[u][j]) & ABS_MASK;
+                    mb = b > mb ? b : mb;
+                }
+                mb = warp_max64(mb);
+                Ec[u] = mb != 0 ? ilogb_bits(mb) : INT32_MIN;
+            }
+            if (MODE == 0 && Ec[u] != INT32_MIN) {
+                double s1, s2;
+                u_scale(Ec[u], s1, s2);
+                if (s2 == 1.0) {                              // warp-uniform (one chunk per warp)
+                    #pragma unroll
+                    for (int j = 0; j < VP; j++) S[u] += u_sq1(v[u][j], s1);
+                } else {
+                    #pragma unroll
+                    for (int j = 0; j < VP; j++) S[u] += u_sq(v[u][j], s1, s2);
+                }
+            }
+        }
+        if (MODE == 0) {
+            #pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                #pragma unroll
+                for (int u = 0; u < CU; u++) S[u] += __shfl_xor_sync(0xffffffffu, S[u], o);
+            }
+        }
+        #pragma unroll
+        for (int u = 0; u < CU; u++) {
+            const int c = c0 + u * nwarps;
+            if (lane == 0 && c < nch) { sm.Ec[c] = Ec[u]; sm.Sc[c] = (unsigned long long)S[u]; }
+        }
     }
     __syncthreads();
 }
@@ -366,45 +414,82 @@ __global__ void trunc_rows_kernel(const double* __restrict__ A, int64_t m, int64
 // ---------------------------------------------------------------------------
 // Column kernels (B: k x n, row-major, ldb)
 // ---------------------------------------------------------------------------
-// chunk statistics: block = 32 columns x one KC chunk; 16 warps x 16 rows
+// chunk statistics: block = 32 columns x one KC chunk; 16 warps x 16 rows.
+// The chunk maximum is taken over the high words of |x| (one 32-bit max per
+// element): they order like |x| and carry the exponent field, so they give E_c
+// and the Inf/NaN flag directly; only a column chunk whose maximum is subnormal
+// (or zero) needs the full 64-bit patterns (ilogb of a subnormal depends on its
+// leading mantissa bit), which a second, block-uniform pass supplies.
 constexpr int CS_WARPS = 16;
+constexpr int CS_RPT = KC / CS_WARPS;
 template <int MODE>
 __global__ void __launch_bounds__(32 * CS_WARPS)
 cols_stats_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t ldb,
                   int32_t* __restrict__ Ec_out, unsigned long long* __restrict__ Sc_out,
                   int32_t* __restrict__ bad_out) {
+    __shared__ uint32_t sHi[CS_WARPS][32];
     __shared__ unsigned long long sMax[CS_WARPS][32];
     __shared__ double sS[CS_WARPS][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t j = (int64_t)blockIdx.x * 32 + lane;
     const int64_t c = blockIdx.y;
-    const int64_t r0 = c * KC + warp * (KC / CS_WARPS);
+    const int64_t r0 = c * KC + warp * CS_RPT;
     const uint64_t pol = l2_evict_first();
-    double v[KC / CS_WARPS];
-    #pragma unroll
-    for (int q = 0; q < KC / CS_WARPS; q++) {
-        const int64_t l = r0 + q;
-        v[q] = (j < n && l < k) ? ld1_hint(B + l * ldb + j, pol) : 0.0;
-    }
-    uint64_t mb = 0;
-    #pragma unroll
-    for (int q = 0; q < KC / CS_WARPS; q++) {
-        const uint64_t b = (uint64_t)__double_as_longlong(v[q]) & ABS_MASK;
-        mb = b > mb ? b : mb;
-    }
-    sMax[warp][lane] = mb;
-    __syncthreads();
-    uint64_t cm = 0;
-    #pragma unroll
-    for (int w = 0; w < CS_WARPS; w++) cm = sMax[w][lane] > cm ? sMax[w][lane] : cm;
-    double S = 0.0;
-    const bool finite_nz = cm != 0 && cm < INF_BITS;
-    const int Ec = finite_nz ? ilogb_bits(cm) : INT32_MIN;
-    if (MODE == 0 && finite_nz) {
-        double s1, s2;
-        u_scale(Ec, s1, s2);
+    const double* src = B + r0 * ldb + j;
+    double v[CS_RPT];
+    if (j < n && r0 + CS_RPT <= k) {
         #pragma unroll
-        for (int q = 0; q < KC / CS_WARPS; q++) S += u_sq(v[q], s1, s2);
+        for (int q = 0; q < CS_RPT; q++) v[q] = ld1_hint(src + q * ldb, pol);
+    } else {
+        #pragma unroll
+        for (int q = 0; q < CS_RPT; q++) v[q] = (j < n && r0 + q < k) ? ld1_hint(src + q * ldb, pol) : 0.0;
+    }
+    uint32_t mh = 0;
+    #pragma unroll
+    for (int q = 0; q < CS_RPT; q++) mh = max(mh, (uint32_t)__double2hiint(v[q]) & 0x7fffffffu);
+    sHi[warp][lane] = mh;
+    __syncthreads();
+    uint32_t ch = 0;
+    #pragma unroll
+    for (int w = 0; w < CS_WARPS; w++) ch = max(ch, sHi[w][lane]);
+    int Ec;
+    bool bad = false;
+    if (ch >= (uint32_t)(INF_BITS >> 32)) {
+        bad = true; Ec = INT32_MIN;
+    } else if (ch >= 0x00100000u) {
+        Ec = (int)(ch >> 20) - 1023;                          // normal maximum
+    } else {
+        Ec = INT32_MIN;                                       // zero or subnormal: below
+    }
+    // block-uniform: some column's chunk maximum is subnormal (or the chunk is zero)
+    if (__syncthreads_or(ch < 0x00100000u)) {
+        uint64_t mb = 0;
+        #pragma unroll
+        for (int q = 0; q < CS_RPT; q++) {
+            const uint64_t b = (uint64_t)__double_as_longlong(v[q]) & ABS_MASK;
+            mb = b > mb ? b : mb;
+        }
+        sMax[warp][lane] = mb;
+        __syncthreads();
+        if (ch < 0x00100000u) {
+            uint64_t cm = 0;
+            #pragma unroll
+            for (int w = 0; w < CS_WARPS; w++) cm = sMax[w][lane] > cm ? sMax[w][lane] : cm;
+            Ec = cm != 0 ? ilogb_bits(cm) : INT32_MIN;
+        }
+    }
+    double S = 0.0;
+    double s1 = 1.0, s2 = 1.0;
+    if (Ec != INT32_MIN) u_scale(Ec, s1, s2);
+    const bool one = __all_sync(0xffffffffu, s2 == 1.0);      // every lane votes (zero chunks too)
+    if (MODE == 0 && Ec != INT32_MIN) {
+        if (one) {
+            #pragma unroll
+            for (int q = 0; q < CS_RPT; q++) S += u_sq1(v[q], s1);
+        } else {
+            #pragma unroll
+            for (int q = 0; q < CS_RPT; q++) S += u_sq(v[q], s1, s2);
+        }
     }
     sS[warp][lane] = S;
     __syncthreads();
@@ -414,7 +499,7 @@ cols_stats_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t ld
         for (int w = 0; w < CS_WARPS; w++) St += sS[w][lane];
         Ec_out[c * n + j] = Ec;
         Sc_out[c * n + j] = (unsigned long long)St;
-        if (cm >= INF_BITS) atomicOr(bad_out + j, 1);
+        if (bad) atomicOr(bad_out + j, 1);
     }
 }
 
@@ -447,17 +532,19 @@ __global__ void cols_finalize_kernel(const int32_t* __restrict__ Ec, const unsig
 }
 
 // residues of B columns into K-major planes out[t][j][l].  Block = 32 columns
-// x 64 rows of B: thread (warp w, lane) converts column j0+lane, rows
-// l0+8w .. l0+8w+7 (coalesced 256-byte row loads across the warp); the residue
-// bytes are transposed through shared memory so that every 64-byte plane row
-// segment is written by 16 lanes of one warp store (full sectors, no
-// partial-sector read-modify-write in L2).
-constexpr int CR_ROWS = 64;
-template <int NM, int WORDS>
+// x CR_ROWS = 128 rows of B: thread (warp w, lane) converts column j0+lane,
+// rows l0+16w .. l0+16w+15 (coalesced 256-byte row loads across the warp, 16
+// independent loads in flight per thread); its 16 residue bytes per modulus go
+// to shared memory as one 16-byte store ([t][col][128 bytes of k], 16-byte
+// chunks XOR-swizzled by (col & 7): conflict-free), then every 128-byte plane
+// row segment is written by 8 consecutive threads with 16-byte stores (full
+// sectors, no partial-sector read-modify-write in L2).
+template <int NM, int WORDS, int CR_ROWS>
 __global__ void __launch_bounds__(256)
 cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t ldb,
                      const int32_t* __restrict__ f, int8_t* __restrict__ out, int64_t ldr) {
-    // [t][col][64 bytes of k], 8-byte chunks XOR-swizzled by (col & 7)
+    constexpr int CR_RPT = CR_ROWS / 8;             // rows per thread (8 warps)
+    constexpr int NPC = CR_ROWS / 16;               // 16-byte pieces per (t, col) segment
     extern __shared__ __align__(16) uint8_t sres[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t j0 = (int64_t)blockIdx.x * 32;
@@ -469,42 +556,49 @@ cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t
         const bool live = j < n && e != OZ2_EXP_NONFINITE_DEV;     // sentinel column: x = 0
         double s1, s2;
         pow2_factors(e, s1, s2);
-        uint32_t w[8][3];
-        #pragma unroll
-        for (int q = 0; q < 8; q++) {
-            const int64_t l = l0 + warp * 8 + q;
-            const double a = (live && l < k) ? ld1_hint(B + l * ldb + j, pol) : 0.0;
-            to_words<WORDS>(a, s1, s2, w[q]);
+        const int64_t lw = l0 + warp * CR_RPT;
+        const double* src = B + lw * ldb + j;
+        double a[CR_RPT];
+        if (live && lw + CR_RPT <= k) {
+            #pragma unroll
+            for (int q = 0; q < CR_RPT; q++) a[q] = ld1_hint(src + q * ldb, pol);
+        } else {
+            #pragma unroll
+            for (int q = 0; q < CR_RPT; q++) a[q] = (live && lw + q < k) ? ld1_hint(src + q * ldb, pol) : 0.0;
         }
-        const int chunk = warp ^ (lane & 7);                 // swizzled 8-byte chunk within the 64 B row
+        uint32_t w[CR_RPT][3];
+        #pragma unroll
+        for (int q = 0; q < CR_RPT; q++) to_words<WORDS>(a[q], s1, s2, w[q]);
+        // 16-byte chunks XOR-swizzled within the segment (conflict-free stores and loads)
         #pragma unroll
         for (int t = 0; t < NM; t++) {
-            uint32_t r[8];
+            uint32_t r[CR_RPT];
             #pragma unroll
-            for (int q = 0; q < 8; q++) r[q] = t == 0 ? w[q][0] : residue_odd<NM, WORDS>(t, w[q]);
-            *reinterpret_cast<uint2*>(sres + ((size_t)(t * 32 + lane) * 64) + chunk * 8) =
-                make_uint2(pack_lo_bytes(r[0], r[1], r[2], r[3]), pack_lo_bytes(r[4], r[5], r[6], r[7]));
+            for (int q = 0; q < CR_RPT; q++) r[q] = t == 0 ? w[q][0] : residue_odd<NM, WORDS>(t, w[q]);
+            uint8_t* seg = sres + (size_t)(t * 32 + lane) * CR_ROWS;
+            if constexpr (CR_RPT == 16) {
+                *reinterpret_cast<uint4*>(seg + ((warp ^ (lane & 7)) * 16)) =
+                    make_uint4(pack_lo_bytes(r[0], r[1], r[2], r[3]), pack_lo_bytes(r[4], r[5], r[6], r[7]),
+                               pack_lo_bytes(r[8], r[9], r[10], r[11]), pack_lo_bytes(r[12], r[13], r[14], r[15]));
+            } else {                                   // 8 bytes: half of piece (warp >> 1)
+                const int pc = (warp >> 1) ^ (lane & 3);
+                *reinterpret_cast<uint2*>(seg + pc * 16 + (warp & 1) * 8) =
+                    make_uint2(pack_lo_bytes(r[0], r[1], r[2], r[3]), pack_lo_bytes(r[4], r[5], r[6], r[7]));
+            }
         }
     }
     __syncthreads();
-    // write out: 4 threads per (t, col) row segment of 64 bytes, 16 bytes each
-    // (64 segments per pass of the block); the two 8-byte chunks of a 16-byte
-    // piece sit side by side in smem (XOR swizzle keeps pairs), swapped when
-    // (col & 7) is odd
-    const int piece = threadIdx.x & 3;
-    for (int rowi = threadIdx.x >> 2; rowi < NM * 32; rowi += 64) {
+    // write out: NPC threads per (t, col) row segment of CR_ROWS bytes, 16 bytes each
+    const int piece = threadIdx.x % NPC;
+    const int64_t l = l0 + 16 * piece;
+    if (l >= ldr) return;                                    // ldr % 16 == 0: pieces are whole
+    const int swz = NPC - 1;
+    #pragma unroll 2
+    for (int rowi = threadIdx.x / NPC; rowi < NM * 32; rowi += 256 / NPC) {
         const int t = rowi >> 5, col = rowi & 31;
         if (j0 + col >= n) continue;
-        const int sw = col & 7;
-        const uint4 v = *reinterpret_cast<const uint4*>(sres + (size_t)rowi * 64 + (((2 * piece) ^ sw) >> 1) * 16);
-        const uint4 o = (sw & 1) ? make_uint4(v.z, v.w, v.x, v.y) : v;
-        const int64_t l = l0 + 16 * piece;
-        int8_t* dst = out + (int64_t)t * n * ldr + (j0 + col) * ldr + l;
-        if (l + 16 <= ldr) {
-            *reinterpret_cast<uint4*>(dst) = o;
-        } else if (l < ldr) {                                // ldr % 16 == 0: never partial
-            *reinterpret_cast<uint2*>(dst) = make_uint2(o.x, o.y);
-        }
+        const uint4 v = *reinterpret_cast<const uint4*>(sres + (size_t)rowi * CR_ROWS + ((piece ^ (col & swz)) * 16));
+        *reinterpret_cast<uint4*>(out + (int64_t)t * n * ldr + (j0 + col) * ldr + l) = v;
     }
 }
 
@@ -543,20 +637,29 @@ static void launch_rows_nm(const double* A, int64_t m, int64_t k, int64_t lda, i
     kern<<<grid, block, smem, st>>>(A, m, k, lda, what, kstar, e, res, ldr);
 }
 
-template <int NM>
-static void launch_cols_res_nm(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
-                               int8_t* res, int64_t ldr, cudaStream_t st) {
-    dim3 grid((unsigned)((n + 31) / 32), (unsigned)((k + CR_ROWS - 1) / CR_ROWS)), block(256);
+template <int NM, int ROWS>
+static void launch_cols_res_rows(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
+                                 int8_t* res, int64_t ldr, cudaStream_t st) {
+    dim3 grid((unsigned)((n + 31) / 32), (unsigned)((k + ROWS - 1) / ROWS)), block(256);
     constexpr int W = NM <= 16 ? 2 : 3;
-    const size_t smem = (size_t)NM * 32 * CR_ROWS;
+    const size_t smem = (size_t)NM * 32 * ROWS;
     static bool attr_done[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !attr_done[dev]) {
-        cudaFuncSetAttribute(cols_residues_kernel<NM, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(cols_residues_kernel<NM, W, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_done[dev] = true;
     }
-    cols_residues_kernel<NM, W><<<grid, block, smem, st>>>(B, k, n, ldb, f, res, ldr);
+    cols_residues_kernel<NM, W, ROWS><<<grid, block, smem, st>>>(B, k, n, ldb, f, res, ldr);
+}
+
+// rows of B per CTA: 64 (8 per thread) or 128 (16 per thread; OZ2_CR_ROWS=128)
+template <int NM>
+static void launch_cols_res_nm(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
+                               int8_t* res, int64_t ldr, cudaStream_t st) {
+    static const int rows = [] { const char* v = getenv("OZ2_CR_ROWS"); return v && atoi(v) == 128 ? 128 : 64; }();
+    if (rows == 128) launch_cols_res_rows<NM, 128>(B, k, n, ldb, f, res, ldr, st);
+    else launch_cols_res_rows<NM, 64>(B, k, n, ldb, f, res, ldr, st);
 }
 
 #define OZ2_DISPATCH_N(N, FN, ...)                                                   \
