@@ -169,14 +169,19 @@ __device__ __forceinline__ void u_scale(int Ec, double& s1, double& s2) {
     if (sh <= 1000) { s1 = __longlong_as_double((long long)(sh + 1023) << 52); s2 = 1.0; }
     else { s1 = 0x1p1000; s2 = __longlong_as_double((long long)(sh - 1000 + 1023) << 52); }
 }
-__device__ __forceinline__ double u_sq(double x, double s1, double s2) {
-    const double u = fmax(1.0, ceil(fabs(x) * s1 * s2));
-    return x != 0.0 ? u * u : 0.0;
+// u^2 as an exact integer: u = ceil(|x| 2^(15-E_c)) with the product rounded
+// UPWARD (exact whenever it is >= 2^-1022; a nonzero product that underflows
+// stays > 0), then ceil to an integer in one conversion (cvt.rpi.u32.f64): so
+// u >= 1 for every x != 0 and u = 0 for x = 0, which is the rule's
+// max(1, ceil(.)) without a compare; u <= 2^16, u^2 <= 2^32 in 64-bit integers
+__device__ __forceinline__ uint64_t u_sq(double x, double s1, double s2) {
+    const uint32_t u = __double2uint_ru(__dmul_ru(__dmul_ru(fabs(x), s1), s2));
+    return (uint64_t)u * u;
 }
 // the same for s2 = 1 (every chunk whose maximum is a normal number >= 2^-1008)
-__device__ __forceinline__ double u_sq1(double x, double s1) {
-    const double u = fmax(1.0, ceil(fabs(x) * s1));
-    return x != 0.0 ? u * u : 0.0;
+__device__ __forceinline__ uint64_t u_sq1(double x, double s1) {
+    const uint32_t u = __double2uint_ru(__dmul_ru(fabs(x), s1));
+    return (uint64_t)u * u;
 }
 
 // per-row chunk statistics in dynamic shared memory: Sc[nch], Ec[nch], then bad, e
@@ -262,10 +267,10 @@ __device__ void row_chunk_stats(const double* __restrict__ X, int64_t k, RowSmem
             for (int u = 0; u < CU; u++) mh[u] = max(mh[u], __shfl_xor_sync(0xffffffffu, mh[u], o));
         }
         int Ec[CU];
-        double S[CU];
+        uint64_t S[CU];
         #pragma unroll
         for (int u = 0; u < CU; u++) {
-            S[u] = 0.0;
+            S[u] = 0;
             if (mh[u] >= (uint32_t)(INF_BITS >> 32)) {
                 Ec[u] = INT32_MIN;
                 if (lane == 0 && c0 + u * nwarps < nch) sm.misc[0] = 1;
@@ -303,7 +308,7 @@ __device__ void row_chunk_stats(const double* __restrict__ X, int64_t k, RowSmem
         #pragma unroll
         for (int u = 0; u < CU; u++) {
             const int c = c0 + u * nwarps;
-            if (lane == 0 && c < nch) { sm.Ec[c] = Ec[u]; sm.Sc[c] = (unsigned long long)S[u]; }
+            if (lane == 0 && c < nch) { sm.Ec[c] = Ec[u]; sm.Sc[c] = S[u]; }
         }
     }
     __syncthreads();
@@ -429,7 +434,7 @@ cols_stats_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t ld
                   int32_t* __restrict__ bad_out) {
     __shared__ uint32_t sHi[CS_WARPS][32];
     __shared__ unsigned long long sMax[CS_WARPS][32];
-    __shared__ double sS[CS_WARPS][32];
+    __shared__ unsigned long long sS[CS_WARPS][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t j = (int64_t)blockIdx.x * 32 + lane;
     const int64_t c = blockIdx.y;
@@ -478,7 +483,7 @@ cols_stats_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t ld
             Ec = cm != 0 ? ilogb_bits(cm) : INT32_MIN;
         }
     }
-    double S = 0.0;
+    uint64_t S = 0;
     double s1 = 1.0, s2 = 1.0;
     if (Ec != INT32_MIN) u_scale(Ec, s1, s2);
     const bool one = __all_sync(0xffffffffu, s2 == 1.0);      // every lane votes (zero chunks too)
@@ -494,11 +499,11 @@ cols_stats_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t ld
     sS[warp][lane] = S;
     __syncthreads();
     if (warp == 0 && j < n) {
-        double St = 0.0;
+        uint64_t St = 0;
         #pragma unroll
         for (int w = 0; w < CS_WARPS; w++) St += sS[w][lane];
         Ec_out[c * n + j] = Ec;
-        Sc_out[c * n + j] = (unsigned long long)St;
+        Sc_out[c * n + j] = St;
         if (bad) atomicOr(bad_out + j, 1);
     }
 }
