@@ -566,14 +566,19 @@ cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t
         double a[CR_RPT];
         if (live && lw + CR_RPT <= k) {
             #pragma unroll
-            for (int q = 0; q < CR_RPT; q++) a[q] = ld1_hint(src + q * ldb, pol);
+            for (int q = 0; q < CR_RPT; q++) { a[q] = ld1_hint(src, pol); src += ldb; }
         } else {
             #pragma unroll
             for (int q = 0; q < CR_RPT; q++) a[q] = (live && lw + q < k) ? ld1_hint(src + q * ldb, pol) : 0.0;
         }
         uint32_t w[CR_RPT][3];
-        #pragma unroll
-        for (int q = 0; q < CR_RPT; q++) to_words<WORDS>(a[q], s1, s2, w[q]);
+        if (__all_sync(0xffffffffu, s2 == 1.0)) {           // one multiplication (normal scales)
+            #pragma unroll
+            for (int q = 0; q < CR_RPT; q++) to_words<WORDS>(a[q], s1, 1.0, w[q]);
+        } else {
+            #pragma unroll
+            for (int q = 0; q < CR_RPT; q++) to_words<WORDS>(a[q], s1, s2, w[q]);
+        }
         // 16-byte chunks XOR-swizzled within the segment (conflict-free stores and loads)
         #pragma unroll
         for (int t = 0; t < NM; t++) {
@@ -593,17 +598,22 @@ cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t
         }
     }
     __syncthreads();
-    // write out: NPC threads per (t, col) row segment of CR_ROWS bytes, 16 bytes each
+    // write out: NPC threads per (t, col) row segment of CR_ROWS bytes, 16 bytes
+    // each; a thread keeps its column and piece and walks t in steps of TSTEP
+    constexpr int TSTEP = 256 / NPC / 32;
     const int piece = threadIdx.x % NPC;
+    const int col = (threadIdx.x / NPC) & 31;
+    const int t0 = (threadIdx.x / NPC) >> 5;
     const int64_t l = l0 + 16 * piece;
-    if (l >= ldr) return;                                    // ldr % 16 == 0: pieces are whole
-    const int swz = NPC - 1;
-    #pragma unroll 2
-    for (int rowi = threadIdx.x / NPC; rowi < NM * 32; rowi += 256 / NPC) {
-        const int t = rowi >> 5, col = rowi & 31;
-        if (j0 + col >= n) continue;
-        const uint4 v = *reinterpret_cast<const uint4*>(sres + (size_t)rowi * CR_ROWS + ((piece ^ (col & swz)) * 16));
-        *reinterpret_cast<uint4*>(out + (int64_t)t * n * ldr + (j0 + col) * ldr + l) = v;
+    if (l >= ldr || j0 + col >= n) return;                   // ldr % 16 == 0: pieces are whole
+    const uint8_t* sp = sres + (size_t)(t0 * 32 + col) * CR_ROWS + ((piece ^ (col & (NPC - 1))) * 16);
+    int8_t* gp = out + (int64_t)t0 * n * ldr + (j0 + col) * ldr + l;
+    const int64_t gstep = (int64_t)TSTEP * n * ldr;
+    #pragma unroll 4
+    for (int t = t0; t < NM; t += TSTEP) {
+        *reinterpret_cast<uint4*>(gp) = *reinterpret_cast<const uint4*>(sp);
+        sp += TSTEP * 32 * CR_ROWS;
+        gp += gstep;
     }
 }
 
