@@ -132,6 +132,34 @@ def test_edge_shapes_and_values(oz2, oracle):
     _stages(oz2, oracle, A, B, 18, "fast")
 
 
+def test_extreme_range_within_chunk(oz2, oracle):
+    # FAST statistics (reading R4) where |x| 2^(15 - E_c) underflows: a chunk that
+    # holds 2^1000 next to subnormals must still count u = 1 for every nonzero
+    # element; chunks whose maximum is subnormal take the 64-bit ilogb path; a
+    # ragged last chunk (k = 600 = 2 * 256 + 88)
+    m, n, k = 40, 48, 600
+    A = phi_matrix_np(m, k, 1.0, seed=31)
+    B = phi_matrix_np(k, n, 1.0, seed=32)
+    A[0, 0] = 2.0 ** 1000
+    A[0, 1:200:3] = 2.0 ** -1070                 # underflows against 2^(15-1000)
+    A[0, 5] = -5e-324
+    A[1, 260] = 2.0 ** 1000
+    A[1, 301:512] *= 2.0 ** -1060                # mixed normal / subnormal in one chunk
+    A[2, :256] = 2.0 ** -1050                    # a chunk whose maximum is subnormal
+    A[2, 256:] *= 2.0 ** -1100
+    A[3, 520:600] = 3e-320                       # subnormal tail chunk, zeros before
+    A[3, :520] = 0.0
+    B[0, 0] = -2.0 ** 10
+    B[1:250:7, 0] = 2.0 ** -1074
+    B[256:512, 1] *= 2.0 ** -1060
+    B[300, 1] = 2.0 ** 990
+    B[:, 2] = 1e-315                             # subnormal column
+    B[512:, 3] = 2.0 ** -1040
+    B[:512, 3] = 0.0
+    for N in (14, 20):
+        _stages(oz2, oracle, A, B, N, "fast")
+
+
 def test_int32_boundary_k(oz2, oracle):
     # k = 2^17 - 1 with all residues -128 gives 2^31 - 16384
     k = 2**17 - 1
