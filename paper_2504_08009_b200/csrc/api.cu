@@ -200,10 +200,11 @@ int get_workspace(oz2_handle_t h, size_t bytes, uint8_t** ws) {
 }
 
 // 3-D tensor map over residue planes [N][rows][ldr] (int8), box 128 x box_rows x 1, 128B swizzle
+// (pstride > 0: bytes between planes, for a row range of larger planes)
 int make_plane_map(CUtensorMap* tm, const int8_t* base, int64_t rows, int64_t k, int64_t ldr, int N,
-                   int box_rows) {
+                   int box_rows, int64_t pstride = 0) {
     cuuint64_t dims[3] = {(cuuint64_t)k, (cuuint64_t)rows, (cuuint64_t)N};
-    cuuint64_t strides[2] = {(cuuint64_t)ldr, (cuuint64_t)(ldr * rows)};
+    cuuint64_t strides[2] = {(cuuint64_t)ldr, (cuuint64_t)(pstride > 0 ? pstride : ldr * rows)};
     cuuint32_t box[3] = {128, (cuuint32_t)box_rows, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, estr,
@@ -661,22 +662,40 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     return cuda_status();
 }
 
-// 2-D host pipeline (FAST / EQ17, large m and n): the H2D stream interleaves
-// column panels of B and row blocks of A (B0, A0, B1, A1, ..., then the rest
-// of A); every panel and block is converted once when it lands, and each
-// (block, panel) product runs as soon as both sides are on the device, its C
-// tile going back on the D2H stream at once.  Compute starts after the first
-// panel and block instead of after all of B; bit-identical to one call (e_i
-// depends on row i only, f_j on column j only).
+// 2-D host pipeline (FAST / EQ17, large m and n).  Row blocks of A and column
+// panels of B go over the H2D stream interleaved so that the fractions of A and
+// of B on the device stay level (B slightly ahead), each converted once when it
+// lands into plane-major residues ([N][m][ldr], [N][n][ldr]).  A block that
+// lands is multiplied at once with ALL panels already present, and a panel that
+// lands with ALL blocks already present: one GEMM launch per arrival (the
+// arrived blocks / panels are a contiguous row / column range of the planes),
+// so every (block, panel) pair runs exactly once, in launches of many tiles.
+// The last blocks of A shrink (512, 256, 256 rows) so the GEMM and the C
+// copy-back after the final arrival are short.  Each product's C block leaves
+// on the D2H stream as soon as it is written.  Bit-identical to one call: e_i
+// depends on row i only, f_j on column j only.
 int dgemm_host_2d(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
                   const double* B, int64_t ldb, double* C, int64_t ldc, int N, int kstar) {
-    const int64_t P = 4, R = std::max<int64_t>(4, std::min<int64_t>(16, m / 2048));
-    const int64_t nb = round_up((n + P - 1) / P, 512), mb = round_up((m + R - 1) / R, 256);
-    std::vector<int64_t> c0s, ncs, r0s, nrs;
-    for (int64_t c = 0; c < n; c += nb) { c0s.push_back(c); ncs.push_back(std::min(nb, n - c)); }
-    for (int64_t r = 0; r < m; r += mb) { r0s.push_back(r); nrs.push_back(std::min(mb, m - r)); }
+    const int64_t pa = round_up(std::max<int64_t>(256, env_flag("OZ2_HOST_BLOCK", 1024)), 256);
+    const int64_t pb = round_up(std::max<int64_t>(512, env_flag("OZ2_HOST_PANEL", 1024)), 512);
+    std::vector<int64_t> r0s, nrs, c0s, ncs;
+    {
+        // A: blocks of pa rows, the last pa rows as pa/2, pa/4, pa/4 (multiples of 256)
+        const int64_t tail = m > 2 * pa ? pa : 0;
+        int64_t r = 0;
+        for (; r + pa <= m - tail; r += pa) { r0s.push_back(r); nrs.push_back(pa); }
+        if (r < m - tail) { r0s.push_back(r); nrs.push_back(m - tail - r); r = m - tail; }
+        if (tail) {
+            const int64_t t1 = round_up(tail / 2, 256), t2 = std::max<int64_t>(256, round_up(tail / 4, 256));
+            for (int64_t sz : {t1, t2}) {
+                if (r < m) { const int64_t rows = std::min(sz, m - r); r0s.push_back(r); nrs.push_back(rows); r += rows; }
+            }
+            if (r < m) { r0s.push_back(r); nrs.push_back(m - r); }
+        }
+        for (int64_t c = 0; c < n; c += pb) { c0s.push_back(c); ncs.push_back(std::min(pb, n - c)); }
+    }
     const int64_t np = (int64_t)c0s.size(), nr = (int64_t)r0s.size();
-    Layout L = layout_for(m, n, k, N, gemm_sms(h), nb);
+    Layout L = layout_for(m, n, k, N, gemm_sms(h), pb);
     const size_t bytesA = sizeof(double) * (size_t)m * (size_t)k;
     const size_t bytesB = sizeof(double) * (size_t)k * (size_t)n;
     const size_t offA = (size_t)round_up((int64_t)L.total, 256);
@@ -690,60 +709,61 @@ int dgemm_host_2d(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double*
     double* dC = (double*)(ws + offC);
     if (!h->s_h2d && cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking) != cudaSuccess) return OZ2_ERR_CUDA;
     if (!h->s_d2h && cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking) != cudaSuccess) return OZ2_ERR_CUDA;
-    const size_t nev = (size_t)(np + nr + nr * np + 1);
+    const size_t nev = (size_t)(1 + 2 * (np + nr));
     while (h->pipe_ev.size() < nev) {
         cudaEvent_t ev;
         if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return OZ2_ERR_CUDA;
         h->pipe_ev.push_back(ev);
     }
     cudaEvent_t evStart = h->pipe_ev[0];
-    cudaEvent_t* evB = &h->pipe_ev[1];
-    cudaEvent_t* evA = &h->pipe_ev[1 + np];
-    cudaEvent_t* evP = &h->pipe_ev[1 + np + nr];
+    cudaEvent_t* evIn = &h->pipe_ev[1];                          // per piece: landed on the device
+    cudaEvent_t* evOut = &h->pipe_ev[1 + np + nr];               // per piece: its product written
     if (cudaEventRecord(evStart, h->stream) != cudaSuccess) return OZ2_ERR_CUDA;
     cudaStreamWaitEvent(h->s_h2d, evStart, 0);
     cudaStreamWaitEvent(h->s_d2h, evStart, 0);
-    // transfer order: B0, A0, B1, A1, ..., then the remaining blocks of A
+    // transfer order: keep the landed fraction of B at or just above that of A
     std::vector<std::pair<int, int64_t>> order;                  // (0 = panel of B, 1 = block of A, index)
-    for (int64_t x = 0; x < std::max(np, nr); x++) {
-        if (x < np) order.push_back({0, x});
-        if (x < nr) order.push_back({1, x});
+    {
+        int64_t ia = 0, ib = 0, rows_sent = 0, cols_sent = 0;
+        while (ia < nr || ib < np) {
+            const bool sendB = ib < np && (ia >= nr || (double)cols_sent / n <= (double)rows_sent / m + 1e-12);
+            if (sendB) { order.push_back({0, ib}); cols_sent += ncs[ib]; ib++; }
+            else { order.push_back({1, ia}); rows_sent += nrs[ia]; ia++; }
+        }
     }
-    for (auto& o : order) {
+    for (size_t q = 0; q < order.size(); q++) {
+        const auto& o = order[q];
         cudaError_t ce;
         if (o.first == 0) {
             const int64_t c0 = c0s[o.second], nc = ncs[o.second];
             ce = cudaMemcpy2DAsync(dB + c0, sizeof(double) * n, B + c0, sizeof(double) * ldb, sizeof(double) * nc, k,
                                    cudaMemcpyHostToDevice, h->s_h2d);
-            if (ce == cudaSuccess) ce = cudaEventRecord(evB[o.second], h->s_h2d);
         } else {
             const int64_t r0 = r0s[o.second], rows = nrs[o.second];
             ce = cudaMemcpy2DAsync(dA + r0 * k, sizeof(double) * k, A + r0 * lda, sizeof(double) * lda,
                                    sizeof(double) * k, rows, cudaMemcpyHostToDevice, h->s_h2d);
-            if (ce == cudaSuccess) ce = cudaEventRecord(evA[o.second], h->s_h2d);
         }
+        if (ce == cudaSuccess) ce = cudaEventRecord(evIn[q], h->s_h2d);
         if (ce != cudaSuccess) return OZ2_ERR_CUDA;
     }
-    int8_t* Ares = (int8_t*)(ws + L.off_Ares);                 // block-major: block i at N * r0 * ldr
-    int8_t* Bres = (int8_t*)(ws + L.off_Bres);                 // panel-major: panel j at N * c0 * ldr
+    int8_t* Ares = (int8_t*)(ws + L.off_Ares);                 // plane-major [N][m][ldr]
+    int8_t* Bres = (int8_t*)(ws + L.off_Bres);                 // plane-major [N][n][ldr]
     int32_t* e = (int32_t*)(ws + L.off_e);
     int32_t* f = (int32_t*)(ws + L.off_f);
-    std::vector<char> haveA(nr, 0), haveB(np, 0);
+    const int64_t psA = m * L.ldr, psB = n * L.ldr;
     mark(h);
     mark(h);
     mark(h);
     mark(h);                                                   // conversions are timed inside the GEMM stage
-    auto product = [&](int64_t i, int64_t j) -> int {
-        const int64_t r0 = r0s[i], rows = nrs[i], c0 = c0s[j], nc = ncs[j];
+    // rows [r0, r0 + rows) x columns [c0, c0 + nc): one fused GEMM launch, then its C block goes back
+    auto product = [&](int64_t r0, int64_t rows, int64_t c0, int64_t nc, cudaEvent_t ev) -> int {
         CUtensorMap tA, tB;
         int rr;
-        if ((rr = make_plane_map(&tA, Ares + (size_t)N * r0 * L.ldr, rows, k, L.ldr, N, 128))) return rr;
-        if ((rr = make_plane_map(&tB, Bres + (size_t)N * c0 * L.ldr, nc, k, L.ldr, N, 256 / oz2::gemm_cta_group())))
-            return rr;
+        if ((rr = make_plane_map(&tA, Ares + r0 * L.ldr, rows, k, L.ldr, N, 128, psA))) return rr;
+        if ((rr = make_plane_map(&tB, Bres + c0 * L.ldr, nc, k, L.ldr, N, 256 / oz2::gemm_cta_group(), psB))) return rr;
         if (oz2::launch_modmul_fused(&tA, &tB, rows, nc, k, N, ws + L.off_scratch, e + r0, f + c0, dC + r0 * n + c0, n,
                                      (uint32_t*)(ws + L.off_sync), gemm_sms(h), h->stream))
             return OZ2_ERR_CUDA;
-        cudaEvent_t ev = evP[i * np + j];
         cudaEventRecord(ev, h->stream);
         cudaStreamWaitEvent(h->s_d2h, ev, 0);
         if (cudaMemcpy2DAsync(C + r0 * ldc + c0, sizeof(double) * ldc, dC + r0 * n + c0, sizeof(double) * n,
@@ -751,22 +771,22 @@ int dgemm_host_2d(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double*
             return OZ2_ERR_CUDA;
         return OZ2_OK;
     };
-    for (auto& o : order) {
-        const int64_t x = o.second;
-        if (o.first == 0) {
+    int64_t rows_in = 0, cols_in = 0;                          // landed prefixes of A's rows / B's columns
+    for (size_t q = 0; q < order.size(); q++) {
+        const int64_t x = order[q].second;
+        cudaStreamWaitEvent(h->stream, evIn[q], 0);
+        if (order[q].first == 0) {
             const int64_t c0 = c0s[x], nc = ncs[x];
-            cudaStreamWaitEvent(h->stream, evB[x], 0);
             oz2::launch_cols_exponents(dB + c0, k, nc, n, N, h->mode, kstar, f + c0, ws + L.off_stats, h->stream);
-            oz2::launch_cols_residues(dB + c0, k, nc, n, f + c0, N, Bres + (size_t)N * c0 * L.ldr, L.ldr, h->stream);
-            haveB[x] = 1;
-            for (int64_t i = 0; i < nr; i++) if (haveA[i] && (rc = product(i, x))) return rc;
+            oz2::launch_cols_residues(dB + c0, k, nc, n, f + c0, N, Bres + c0 * L.ldr, L.ldr, h->stream, psB);
+            cols_in = c0 + nc;
+            if (rows_in > 0 && (rc = product(0, rows_in, c0, nc, evOut[q]))) return rc;
         } else {
             const int64_t r0 = r0s[x], rows = nrs[x];
-            cudaStreamWaitEvent(h->stream, evA[x], 0);
-            oz2::launch_rows(dA + r0 * k, rows, k, k, N, 3, h->mode, kstar, e + r0, Ares + (size_t)N * r0 * L.ldr,
-                             L.ldr, h->stream);
-            haveA[x] = 1;
-            for (int64_t j = 0; j < np; j++) if (haveB[j] && (rc = product(x, j))) return rc;
+            oz2::launch_rows(dA + r0 * k, rows, k, k, N, 3, h->mode, kstar, e + r0, Ares + r0 * L.ldr, L.ldr,
+                             h->stream, psA);
+            rows_in = r0 + rows;
+            if (cols_in > 0 && (rc = product(r0, rows, 0, cols_in, evOut[q]))) return rc;
         }
     }
     mark(h);

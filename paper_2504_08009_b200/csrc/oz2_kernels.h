@@ -22,15 +22,17 @@ int host_L(int N);   // floor(log2(M/2 - 1))
 
 // scale.cu -- Alg. 1 lines 1-5
 // what: 1 = exponents e, 2 = residues (given e), 3 = both (one pass per row)
+// pstride: bytes between residue planes (default m * ldr)
 void launch_rows(const double* A, int64_t m, int64_t k, int64_t lda, int N, int what, int mode,
-                 int kstar, int32_t* e, int8_t* res, int64_t ldr, cudaStream_t st);
+                 int kstar, int32_t* e, int8_t* res, int64_t ldr, cudaStream_t st, int64_t pstride = 0);
 void launch_trunc_rows(const double* A, int64_t m, int64_t k, int64_t lda, const int32_t* e,
                        double* out, cudaStream_t st);
 size_t cols_stats_bytes(int64_t k, int64_t n);
 void launch_cols_exponents(const double* B, int64_t k, int64_t n, int64_t ldb, int N, int mode,
                            int kstar, int32_t* f, void* scratch, cudaStream_t st);
+// pstride: bytes between residue planes (default n * ldr)
 void launch_cols_residues(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f, int N,
-                          int8_t* res, int64_t ldr, cudaStream_t st);
+                          int8_t* res, int64_t ldr, cudaStream_t st, int64_t pstride = 0);
 void launch_trunc_cols(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
                        double* out, cudaStream_t st);
 

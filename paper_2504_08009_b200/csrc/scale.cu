@@ -384,7 +384,7 @@ __device__ void row_residues(const double* __restrict__ X, int64_t k, int e, int
 template <int NM, int WORDS, int MODE, int THREADS>
 __global__ void __launch_bounds__(THREADS)
 rows_kernel(const double* __restrict__ A, int64_t m, int64_t k, int64_t lda, int what, int kstar,
-            int32_t* __restrict__ e_io, int8_t* __restrict__ res, int64_t ldr) {
+            int32_t* __restrict__ e_io, int8_t* __restrict__ res, int64_t ldr, int64_t pstride) {
     extern __shared__ __align__(16) unsigned char row_smem[];
     const int64_t nch = (k + KC - 1) / KC;
     RowSmem sm;
@@ -402,7 +402,7 @@ rows_kernel(const double* __restrict__ A, int64_t m, int64_t k, int64_t lda, int
         } else {
             e = e_io[i];
         }
-        if (what & 2) row_residues<NM, WORDS>(X, k, e, res + i * ldr, m * ldr);
+        if (what & 2) row_residues<NM, WORDS>(X, k, e, res + i * ldr, pstride);
     }
 }
 
@@ -547,7 +547,7 @@ __global__ void cols_finalize_kernel(const int32_t* __restrict__ Ec, const unsig
 template <int NM, int WORDS, int CR_ROWS>
 __global__ void __launch_bounds__(256)
 cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t ldb,
-                     const int32_t* __restrict__ f, int8_t* __restrict__ out, int64_t ldr) {
+                     const int32_t* __restrict__ f, int8_t* __restrict__ out, int64_t ldr, int64_t pstride) {
     constexpr int CR_RPT = CR_ROWS / 8;             // rows per thread (8 warps)
     constexpr int NPC = CR_ROWS / 16;               // 16-byte pieces per (t, col) segment
     extern __shared__ __align__(16) uint8_t sres[];
@@ -607,8 +607,8 @@ cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t
     const int64_t l = l0 + 16 * piece;
     if (l >= ldr || j0 + col >= n) return;                   // ldr % 16 == 0: pieces are whole
     const uint8_t* sp = sres + (size_t)(t0 * 32 + col) * CR_ROWS + ((piece ^ (col & (NPC - 1))) * 16);
-    int8_t* gp = out + (int64_t)t0 * n * ldr + (j0 + col) * ldr + l;
-    const int64_t gstep = (int64_t)TSTEP * n * ldr;
+    int8_t* gp = out + (int64_t)t0 * pstride + (j0 + col) * ldr + l;
+    const int64_t gstep = (int64_t)TSTEP * pstride;
     #pragma unroll 4
     for (int t = t0; t < NM; t += TSTEP) {
         *reinterpret_cast<uint4*>(gp) = *reinterpret_cast<const uint4*>(sp);
@@ -631,7 +631,7 @@ __global__ void trunc_cols_kernel(const double* __restrict__ B, int64_t k, int64
 // ---------------------------------------------------------------------------
 template <int NM>
 static void launch_rows_nm(const double* A, int64_t m, int64_t k, int64_t lda, int what, int mode,
-                           int kstar, int32_t* e, int8_t* res, int64_t ldr, cudaStream_t st) {
+                           int kstar, int32_t* e, int8_t* res, int64_t ldr, int64_t pstride, cudaStream_t st) {
     constexpr int W = NM <= 16 ? 2 : 3;
     static const int threads = [] { const char* v = getenv("OZ2_ROW_THREADS"); return v && atoi(v) == 512 ? 512 : 256; }();
     // OZ2_ROW_CTAS_PER_SM = R > 0: a persistent grid of R CTAs per SM (rows in
@@ -649,12 +649,12 @@ static void launch_rows_nm(const double* A, int64_t m, int64_t k, int64_t lda, i
     auto kern = threads == 512 ? (mode == 0 ? rows_kernel<NM, W, 0, 512> : rows_kernel<NM, W, 1, 512>)
                                : (mode == 0 ? rows_kernel<NM, W, 0, 256> : rows_kernel<NM, W, 1, 256>);
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, block, smem, st>>>(A, m, k, lda, what, kstar, e, res, ldr);
+    kern<<<grid, block, smem, st>>>(A, m, k, lda, what, kstar, e, res, ldr, pstride);
 }
 
 template <int NM, int ROWS>
 static void launch_cols_res_rows(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
-                                 int8_t* res, int64_t ldr, cudaStream_t st) {
+                                 int8_t* res, int64_t ldr, int64_t pstride, cudaStream_t st) {
     dim3 grid((unsigned)((n + 31) / 32), (unsigned)((k + ROWS - 1) / ROWS)), block(256);
     constexpr int W = NM <= 16 ? 2 : 3;
     const size_t smem = (size_t)NM * 32 * ROWS;
@@ -665,16 +665,16 @@ static void launch_cols_res_rows(const double* B, int64_t k, int64_t n, int64_t 
         cudaFuncSetAttribute(cols_residues_kernel<NM, W, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_done[dev] = true;
     }
-    cols_residues_kernel<NM, W, ROWS><<<grid, block, smem, st>>>(B, k, n, ldb, f, res, ldr);
+    cols_residues_kernel<NM, W, ROWS><<<grid, block, smem, st>>>(B, k, n, ldb, f, res, ldr, pstride);
 }
 
 // rows of B per CTA: 64 (8 per thread) or 128 (16 per thread; OZ2_CR_ROWS=128)
 template <int NM>
 static void launch_cols_res_nm(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
-                               int8_t* res, int64_t ldr, cudaStream_t st) {
+                               int8_t* res, int64_t ldr, int64_t pstride, cudaStream_t st) {
     static const int rows = [] { const char* v = getenv("OZ2_CR_ROWS"); return v && atoi(v) == 128 ? 128 : 64; }();
-    if (rows == 128) launch_cols_res_rows<NM, 128>(B, k, n, ldb, f, res, ldr, st);
-    else launch_cols_res_rows<NM, 64>(B, k, n, ldb, f, res, ldr, st);
+    if (rows == 128) launch_cols_res_rows<NM, 128>(B, k, n, ldb, f, res, ldr, pstride, st);
+    else launch_cols_res_rows<NM, 64>(B, k, n, ldb, f, res, ldr, pstride, st);
 }
 
 #define OZ2_DISPATCH_N(N, FN, ...)                                                   \
@@ -692,9 +692,10 @@ static void launch_cols_res_nm(const double* B, int64_t k, int64_t n, int64_t ld
     }
 
 void launch_rows(const double* A, int64_t m, int64_t k, int64_t lda, int N, int what, int mode,
-                 int kstar, int32_t* e, int8_t* res, int64_t ldr, cudaStream_t st) {
+                 int kstar, int32_t* e, int8_t* res, int64_t ldr, cudaStream_t st, int64_t pstride) {
     if (m == 0) return;
-    OZ2_DISPATCH_N(N, launch_rows_nm, A, m, k, lda, what, mode, kstar, e, res, ldr, st);
+    if (pstride <= 0) pstride = m * ldr;
+    OZ2_DISPATCH_N(N, launch_rows_nm, A, m, k, lda, what, mode, kstar, e, res, ldr, pstride, st);
 }
 
 void launch_trunc_rows(const double* A, int64_t m, int64_t k, int64_t lda, const int32_t* e,
@@ -731,9 +732,10 @@ void launch_cols_exponents(const double* B, int64_t k, int64_t n, int64_t ldb, i
 }
 
 void launch_cols_residues(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f, int N,
-                          int8_t* res, int64_t ldr, cudaStream_t st) {
+                          int8_t* res, int64_t ldr, cudaStream_t st, int64_t pstride) {
     if (n == 0 || k == 0) return;
-    OZ2_DISPATCH_N(N, launch_cols_res_nm, B, k, n, ldb, f, res, ldr, st);
+    if (pstride <= 0) pstride = n * ldr;
+    OZ2_DISPATCH_N(N, launch_cols_res_nm, B, k, n, ldb, f, res, ldr, pstride, st);
 }
 
 void launch_trunc_cols(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
