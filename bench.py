@@ -351,6 +351,20 @@ def main():
 
     if not calls:                              # K-split path: no oz2_dgemm_ex stages to time
         roofline = None
+    # the HBM-bound conversion stages (Alg. 1 lines 1-5), algorithmic bytes per call:
+    # rows_A reads A once and writes N planes; colstats_B reads B; colres_B reads B, writes N planes
+    conv = None
+    if calls and args.mode != "accu" and world == 1:
+        hbm = peaks.get("hbm_gbs")
+        byt = {"rows_A": (8.0 + N) * m * k, "colstats_B": 8.0 * k * n, "colres_B": (8.0 + N) * k * n}
+        conv = {}
+        for st_, b in byt.items():
+            t = stages.get(st_, 0.0) / calls
+            if t > 0:
+                gbs = b / (t * 1e-3) / 1e9
+                conv[st_] = {"bytes": b, "ms": t, "GB/s": gbs, "frac": gbs / hbm if hbm else None}
+        conv["peak_GB/s"] = hbm
+        conv["note"] = "in-step times (the kernels follow a power-capped GEMM at ~1.45 GHz)"
     line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if ksplit else "weak", "vs_baseline": None, "dtype": "int8 (tensor-core s8*s8->s32), f64 in/out",
@@ -358,6 +372,7 @@ def main():
             "max_rel_err": relerr, "compwise_err": compwise, "acc_samples": int(args.acc_samples),
             "stage_ms": {s: v / max(calls, 1) for s, v in stages.items()},
             "roofline": roofline,
+            "conversion_roofline": conv,
             "n_scaled_roofline_frac": value / world / (4500.0 / N),
             # fast / eq17: rows, cols_stats, cols_finalize, cols_residues, modmul; accu adds
             # rows_hat7, cols_stats, cols_finalize, cols_hat7, the bound GEMM and 2 finalizes
