@@ -205,10 +205,11 @@ int make_plane_map(CUtensorMap* tm, const int8_t* base, int64_t rows, int64_t k,
                    int box_rows, int64_t pstride = 0) {
     cuuint64_t dims[3] = {(cuuint64_t)k, (cuuint64_t)rows, (cuuint64_t)N};
     cuuint64_t strides[2] = {(cuuint64_t)ldr, (cuuint64_t)(pstride > 0 ? pstride : ldr * rows)};
-    cuuint32_t box[3] = {128, (cuuint32_t)box_rows, 1};
+    cuuint32_t box[3] = {(cuuint32_t)oz2::gemm_bk(), (cuuint32_t)box_rows, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims, strides, box, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          oz2::gemm_bk() == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? OZ2_OK : OZ2_ERR_CUDA;
 }

@@ -46,7 +46,10 @@ namespace gemm {
 
 constexpr int BM = 128;             // rows of A per CTA (UMMA M per CTA)
 constexpr int BN = 256;             // UMMA N (columns of one accumulator half)
-constexpr int BK = 128;             // bytes = int8 elements per stage (one 128B swizzle row)
+#ifndef OZ2_BK
+#define OZ2_BK 128
+#endif
+constexpr int BK = OZ2_BK;          // bytes = int8 elements per stage: one 128B (or 64B) swizzle row
 constexpr int UK = 32;              // K per tcgen05.mma kind::i8
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 128 + 32 * EPI_WARPS;
@@ -60,7 +63,8 @@ struct Cfg {
     static constexpr int A_BYTES = BM * BK;
     static constexpr int B_HALF_BYTES = B_ROWS * BK;
     static constexpr int B_BYTES = NH * B_HALF_BYTES;
-    static constexpr int STAGES = CG == 2 ? (NH == 2 ? 4 : 6) : 4;
+    // BK = 64: half-size stages, more of them in the same shared memory (9 x 24 KB for the pair tile)
+    static constexpr int STAGES = BK == 64 ? (CG == 2 ? (NH == 2 ? 9 : 12) : 8) : (CG == 2 ? (NH == 2 ? 4 : 6) : 4);
     static constexpr int TILE_M = BM * CG;              // output rows per tile
     static constexpr int TILE_N = BN * NH;              // output columns per tile
     static constexpr int TILE_BYTES = BM * TILE_N;      // one uint8 residue tile (per CTA, per modulus)
@@ -378,8 +382,8 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         #pragma unroll
                         for (int kk = 0; kk < BK / UK; kk++) {
                             const uint32_t accum = (kb != kb0 || kk != 0) ? 1u : 0u;
-                            if (CG == 2) mma_i8_cg2(dh, sw128_desc(a0 + kk * UK), sw128_desc(b0 + kk * UK), idesc, accum);
-                            else mma_i8(dh, sw128_desc(a0 + kk * UK), sw128_desc(b0 + kk * UK), idesc, accum);
+                            if (CG == 2) mma_i8_cg2(dh, sw_desc<BK>(a0 + kk * UK), sw_desc<BK>(b0 + kk * UK), idesc, accum);
+                            else mma_i8(dh, sw_desc<BK>(a0 + kk * UK), sw_desc<BK>(b0 + kk * UK), idesc, accum);
                         }
                     }
                     // the stage is reusable (in both CTAs) when these MMAs finish
@@ -624,6 +628,7 @@ static int env_int(const char* name, int dflt) {
 
 // tuning knobs for experiments (env): OZ2_CG (1 | 2), OZ2_NH (1 | 2, CG = 2 only), OZ2_GROUP_TM, ...
 int gemm_cta_group() { return env_int("OZ2_CG", 2) == 1 ? 1 : 2; }
+int gemm_bk() { return gemm::BK; }
 int gemm_halves() { return gemm_cta_group() == 2 && env_int("OZ2_NH", 2) == 2 ? 2 : 1; }
 static int gemm_shape() { return gemm_cta_group() * 10 + gemm_halves(); }
 
@@ -640,8 +645,9 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
     p.num_tm = (int)((m + tile_m - 1) / tile_m);
     p.num_tn = (int)((n + tile_n - 1) / tile_n);
     p.num_kb = (int)((k + BK - 1) / BK);
-    // K blocking: |C'_t| <= kb_chunk * 128 * 2^14 < 2^31 for kb_chunk <= 1023 (OZ2_KB_CHUNK: tests)
-    p.kb_chunk = std::min(1023, std::max(1, env_int("OZ2_KB_CHUNK", 1023)));
+    // K blocking: |C'_t| <= kb_chunk * BK * 2^14 < 2^31 for kb_chunk * BK <= 1023 * 128 (OZ2_KB_CHUNK: tests)
+    constexpr int KB_MAX = 1023 * 128 / BK;
+    p.kb_chunk = std::min(KB_MAX, std::max(1, env_int("OZ2_KB_CHUNK", KB_MAX)));
     p.nchunk = std::max(1, (p.num_kb + p.kb_chunk - 1) / p.kb_chunk);
     p.group_tm = std::max(1, env_int("OZ2_GROUP_TM", GROUP_TM));
     p.epi_nop = env_int("OZ2_EPI_NOP", 0);
@@ -650,7 +656,7 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
     const int tiles = p.num_tm * p.num_tn;
     const int nclusters = num_sms / cg;
     const int ncl = tiles < nclusters ? tiles : nclusters;
-    p.sync_kb = env_int("OZ2_SYNC_KB", 32 / nh);
+    p.sync_kb = env_int("OZ2_SYNC_KB", 32 / nh * (128 / BK));
     p.sync_lag = env_int("OZ2_SYNC_LAG", 0);
     {
         // busiest CTA: its tiles x N moduli x num_kb k-blocks, in sync_kb steps

@@ -170,6 +170,22 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     d |= (uint64_t)2 << 61;                              // SWIZZLE_128B   [61,64)
     return d;
 }
+// K-major operand with a BK-byte swizzled row: 128B (SBO 1024) or 64B (SBO 512, layout type 4)
+template <int BKB>
+__device__ __forceinline__ uint64_t sw_desc(uint32_t saddr) {
+    if constexpr (BKB == 128) {
+        return sw128_desc(saddr);
+    } else {
+        static_assert(BKB == 64, "BK is 128 or 64");
+        uint64_t d = 0;
+        d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);      // start address
+        d |= (uint64_t)1 << 16;                          // LBO (unused for swizzled K-major)
+        d |= (uint64_t)(512 >> 4) << 32;                 // SBO: 8 rows x 64 B
+        d |= (uint64_t)1 << 46;                          // version = 1
+        d |= (uint64_t)4 << 61;                          // SWIZZLE_64B
+        return d;
+    }
+}
 // instruction descriptor, kind::i8: s8 x s8 -> s32, both K-major, M x N
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool is_signed = true) {
     return (2u << 4)                 // c_format = S32

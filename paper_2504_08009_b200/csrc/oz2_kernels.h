@@ -38,6 +38,7 @@ void launch_trunc_cols(const double* B, int64_t k, int64_t n, int64_t ldb, const
 
 // gemm.cu -- Alg. 1 line 6 on tcgen05 (kind::i8)
 int gemm_cta_group();   // 1 or 2 (CTA pairs, cta_group::2)
+int gemm_bk();          // bytes of K per shared-memory stage (128, or 64 when built with -DOZ2_BK=64)
 int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                   int N, int32_t* cprod, uint32_t* sync_ctr, int num_sms, cudaStream_t st);
 // + Alg. 1 lines 7-10 fused into the epilogue (uint8 residue scratch, exact CRT)

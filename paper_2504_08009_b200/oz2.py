@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liboz2.so")
+# OZ2_LIB: an alternative in-tree build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("OZ2_LIB") or os.path.join(_HERE, "liboz2.so")
 
 OK = 0
 MODE_FAST = 0
