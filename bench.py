@@ -331,7 +331,10 @@ def main():
     t_gemm = stages["gemm"] / max(calls, 1)
     int8_ops = 2.0 * m * n * k * N
     achieved = int8_ops / (t_gemm * 1e-3) / 1e12 if calls else 0.0
-    peak = 2.0 * peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    bf16 = peaks.get("bf16_tflops_sustained") or peaks.get("bf16_tflops")
+    if not bf16:                               # unexpected file contents: the guide's fallback
+        bf16, peak_src = 1400.0, "fallback (unreadable)"
+    peak = 2.0 * float(bf16)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(prof):
