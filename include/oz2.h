@@ -108,6 +108,21 @@ int oz2_dgemm_ex(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* 
 int oz2_dgemm_op(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, int64_t k,
                  double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
                  double beta, double* C, int64_t ldc, int num_moduli);
+/* SYRK-structured product ("GEMM, TRMM, or SYRK"; BLAS
+ * DSYRK semantics, reading R19), row-major:
+ *   trans = OZ2_OP_N: C := alpha A A^T + beta C, A stored n x k (lda >= k);
+ *   trans = OZ2_OP_T: C := alpha A^T A + beta C, A stored k x n (lda >= n);
+ *   uplo = OZ2_LOWER / OZ2_UPPER: only that triangle of C (n x n, ldc >= n,
+ *   diagonal included) is read or written; the other is left untouched.
+ * Every written entry is bit-identical to the same entry of oz2_dgemm_op(A,
+ * A^T): op(A)^T's column exponents are op(A)'s row exponents, so A is converted
+ * once (one set of residue planes serves both operands) and only the output
+ * tiles that meet the triangle are multiplied (about half the GEMM work).
+ * Errors as oz2_dgemm_op; uplo / trans out of range: OZ2_ERR_INVALID_ARG. */
+#define OZ2_LOWER 1
+#define OZ2_UPPER 2
+int oz2_dsyrk(oz2_handle_t h, int uplo, int trans, int64_t n, int64_t k, double alpha,
+              const double* A, int64_t lda, double beta, double* C, int64_t ldc, int num_moduli);
 /* Alg. 1 lines 2-10 with caller-supplied line-1 exponents e[m], f[n] (device
  * int32, OZ2_EXP_NONFINITE allowed): C = D^-1 X E^-1.  For sharded line-1 rules
  * (e.g. OS II-accu across row blocks, where f is a MIN all-reduce of the

@@ -274,6 +274,22 @@ def gemm(A, B, N: int, alpha: float = 1.0, beta: float = 0.0, C=None, transA: bo
     return out
 
 
+def syrk(A, N: int, uplo: str = "L", trans: bool = False, alpha: float = 1.0, beta: float = 0.0, C=None,
+         mode: int = MODE_FAST) -> np.ndarray:
+    """DSYRK (reading R19): the `uplo` triangle (diagonal
+    included) of gemm(op(A), op(A)^T, alpha, beta, C); the other triangle of C
+    is returned unchanged (zeros when C is None)."""
+    A = np.asarray(A, np.float64)
+    Aop = A.T if trans else A
+    n = Aop.shape[0]
+    Cold = np.zeros((n, n)) if C is None else np.array(C, dtype=np.float64)
+    full = gemm(Aop, Aop.T, N, alpha, beta, Cold, mode=mode)
+    mask = np.tril(np.ones((n, n), bool)) if uplo.upper() == "L" else np.triu(np.ones((n, n), bool))
+    out = Cold.copy()
+    out[mask] = full[mask]
+    return out
+
+
 def int_product(Ap, BpT) -> list:
     """Exact integer A' B' as a nested list of Python ints."""
     Ap = _as_f64(Ap)

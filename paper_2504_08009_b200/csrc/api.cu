@@ -136,11 +136,12 @@ struct Layout {
     size_t off_Ares, off_Bres, off_e, off_f, off_stats, off_scratch, off_sync;
     size_t off_E, off_F, off_pr, off_pc;     // accu line 1: max exponents, row / column maxima of P
     size_t off_R;                            // small problems: uint8 c''_t planes [N][m][n]
+    size_t off_tiles;                        // SYRK: the triangle's tile list
     size_t total;
 };
 
 Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms, int64_t stats_cols = -1,
-                  bool with_B = true) {
+                  bool with_B = true, size_t ntiles = 0) {
     Layout L;
     L.ldr = round_up(k > 0 ? k : 1, 16);
     size_t off = 0;
@@ -157,6 +158,7 @@ Layout layout_for(int64_t m, int64_t n, int64_t k, int N, int num_sms, int64_t s
     L.off_pr = take(sizeof(uint32_t) * (size_t)(m > 0 ? m : 1));
     L.off_pc = take(sizeof(uint32_t) * (size_t)(n > 0 ? n : 1));
     L.off_R = take(oz2::gemm_unit_parallel(m, n, num_sms) ? (size_t)N * (size_t)m * (size_t)n : 0);
+    L.off_tiles = take(sizeof(uint32_t) * ntiles);
     L.total = off;
     return L;
 }
@@ -568,9 +570,12 @@ int accu_line1(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
 // of the stored matrix, so the column kernels produce e and the K-major planes;
 // likewise op(B) = B^T (stored n x k) goes through the row kernel.
 // e_given / f_given (both or neither): caller-supplied line-1 exponents (lines 2-10 only).
+// tri = 1 / 2 (SYRK, B is A with the other transpose, m == n): op(B) = op(A)^T
+// shares op(A)'s exponents and residue planes, only the output tiles that meet
+// the lower / upper triangle run, and only that triangle of C is read or written.
 int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int N,
-               const int32_t* e_given = nullptr, const int32_t* f_given = nullptr) {
+               const int32_t* e_given = nullptr, const int32_t* f_given = nullptr, int tri = 0) {
     if (m == 0 || n == 0) return OZ2_OK;
     const bool given = e_given && f_given;
     int rc, kstar = 0;
@@ -578,16 +583,22 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     DevGuard g(h->device);
     if (k == 0 || alpha == 0.0) {                     // no product: C = beta C (0 if beta == 0)
         if (beta == 1.0) return OZ2_OK;
-        oz2::launch_scale_c(C, m, n, ldc, beta, h->stream);
+        oz2::launch_scale_c(C, m, n, ldc, beta, h->stream, tri);
         return cuda_status();
     }
-    Layout L = layout_for(m, n, k, N, gemm_sms(h), ta == OZ2_OP_T ? std::max(m, n) : n);
+    const std::vector<uint32_t> tiles = tri ? oz2::tri_tile_list(m, n, tri, gemm_sms(h)) : std::vector<uint32_t>();
+    Layout L = layout_for(m, n, k, N, gemm_sms(h), ta == OZ2_OP_T ? std::max(m, n) : n, !tri, tiles.size());
+    if (tri) L.off_Bres = L.off_Ares;                 // one set of planes (accu: B-hat = A-hat, same bytes)
     uint8_t* ws;
     if ((rc = get_workspace(h, L.total, &ws))) return rc;
     int8_t* Ares = (int8_t*)(ws + L.off_Ares);
-    int8_t* Bres = (int8_t*)(ws + L.off_Bres);
+    int8_t* Bres = tri ? Ares : (int8_t*)(ws + L.off_Bres);
     int32_t* e = given ? const_cast<int32_t*>(e_given) : (int32_t*)(ws + L.off_e);
     int32_t* f = given ? const_cast<int32_t*>(f_given) : (int32_t*)(ws + L.off_f);
+    if (tri && !tiles.empty() &&
+        cudaMemcpyAsync(ws + L.off_tiles, tiles.data(), sizeof(uint32_t) * tiles.size(), cudaMemcpyHostToDevice,
+                        h->stream) != cudaSuccess)
+        return OZ2_ERR_CUDA;
     uint8_t* scratch = ws + L.off_scratch;
     CUtensorMap tA, tB;
     if ((rc = make_plane_map(&tA, Ares, m, k, L.ldr, N, 128))) return rc;
@@ -607,10 +618,12 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
         }
     };
     auto convert_B_stats = [&](cudaStream_t st) {
+        if (tri) return;                              // SYRK: op(B) = op(A)^T shares e and the planes
         if (tb == OZ2_OP_N && !skip_line1)
             oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, ws + L.off_stats, st);
     };
     auto convert_B_res = [&](cudaStream_t st) {
+        if (tri) return;
         if (tb == OZ2_OP_N) oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, st);
         else oz2::launch_rows(B, n, k, ldb, N, what, h->mode, kstar, f, Bres, L.ldr, st);
     };
@@ -620,7 +633,7 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     // stream concurrently with A's (stage ROWS then times both, the column stages
     // read 0).  Default off: measured no gain, both passes are issue-bound.  (Not
     // with op(A) = A^T, whose column statistics share B's scratch.)
-    const bool overlap = env_flag("OZ2_CONV_OVERLAP", 0) && ta == OZ2_OP_N && !skip_line1;
+    const bool overlap = env_flag("OZ2_CONV_OVERLAP", 0) && ta == OZ2_OP_N && !skip_line1 && !tri;
     if (overlap) {
         if ((rc = ensure_aux(h))) return rc;
         cudaEventRecord(h->ev_fork, h->stream);
@@ -640,6 +653,16 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
         mark(h);
         convert_B_res(h->stream);
         mark(h);
+    }
+    if (tri) {
+        // SYRK: the triangle's tiles only, f = e (the columns of op(A)^T are the rows of op(A))
+        if (oz2::launch_modmul_fused(&tA, &tB, m, n, k, N, scratch, e, e, C, ldc, (uint32_t*)(ws + L.off_sync),
+                                     gemm_sms(h), h->stream, alpha, beta, tri, (const uint32_t*)(ws + L.off_tiles),
+                                     (int)tiles.size()))
+            return OZ2_ERR_CUDA;
+        mark(h);
+        mark(h);
+        return cuda_status();
     }
     if (oz2::gemm_unit_parallel(m, n, gemm_sms(h)) && alpha == 1.0 && beta == 0.0) {
         // small problem (fewer output tiles than CTA pairs): the (tile, modulus)
@@ -816,6 +839,18 @@ int oz2_dgemm_op(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, i
     int rc = check_op_args(transA, transB, m, n, k, A, lda, B, ldb, C, ldc, N);
     if (rc) return rc;
     return dgemm_core(h, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, N);
+}
+
+int oz2_dsyrk(oz2_handle_t h, int uplo, int trans, int64_t n, int64_t k, double alpha, const double* A,
+              int64_t lda, double beta, double* C, int64_t ldc, int N) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    if (uplo != OZ2_LOWER && uplo != OZ2_UPPER) return OZ2_ERR_INVALID_ARG;
+    if (trans != OZ2_OP_N && trans != OZ2_OP_T) return OZ2_ERR_INVALID_ARG;
+    // C := alpha op(A) op(A)^T + beta C: op(B) = op(A)^T is A itself with the other transpose
+    const int tb = trans == OZ2_OP_N ? OZ2_OP_T : OZ2_OP_N;
+    int rc = check_op_args(trans, tb, n, n, k, A, lda, A, lda, C, ldc, N);
+    if (rc) return rc;
+    return dgemm_core(h, trans, tb, n, n, k, alpha, A, lda, A, lda, beta, C, ldc, N, nullptr, nullptr, uplo);
 }
 
 int oz2_prepare_b(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb, int N) {

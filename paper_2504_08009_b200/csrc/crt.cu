@@ -225,17 +225,20 @@ __device__ __forceinline__ double crt_element(const int32_t (&cp)[NM], int ei, i
 }
 
 // C = beta C, or C = 0 when beta == 0 (C not read: BLAS semantics)
-__global__ void scale_c_kernel(double* __restrict__ C, int64_t m, int64_t n, int64_t ldc, double beta) {
+// C := beta C (0 if beta == 0); tri = 1 / 2: only the lower / upper triangle (SYRK)
+__global__ void scale_c_kernel(double* __restrict__ C, int64_t m, int64_t n, int64_t ldc, double beta, int tri) {
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= m * n) return;
-    double* c = C + (idx / n) * ldc + idx % n;
+    const int64_t i = idx / n, j = idx % n;
+    if ((tri == 1 && j > i) || (tri == 2 && j < i)) return;
+    double* c = C + i * ldc + j;
     *c = beta == 0.0 ? 0.0 : beta * *c;
 }
 
-void launch_scale_c(double* C, int64_t m, int64_t n, int64_t ldc, double beta, cudaStream_t st) {
+void launch_scale_c(double* C, int64_t m, int64_t n, int64_t ldc, double beta, cudaStream_t st, int tri) {
     const int64_t tot = m * n;
     if (tot <= 0) return;
-    scale_c_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(C, m, n, ldc, beta);
+    scale_c_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(C, m, n, ldc, beta, tri);
 }
 
 template <int NM>

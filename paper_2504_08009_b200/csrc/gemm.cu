@@ -104,6 +104,9 @@ struct Params {
     double alpha, beta;
     const int32_t* e;
     const int32_t* f;
+    int tri;                        // SYRK: 1 = write only col <= row, 2 = only col >= row (0: all)
+    const uint32_t* tiles;          // SYRK: the tiles to visit, (tm << 16) | tn in schedule order (or NULL)
+    int ntiles;
     uint32_t* sync_ctr;             // global progress counter (zeroed before launch), or NULL
     int sync_kb;                    // k-blocks per progress step
     int sync_lag;                   // steps a CTA may run ahead of the slowest
@@ -114,6 +117,11 @@ struct Params {
 // order: tiles j = cid, cid + ncl, ... (raster groups of group_tm tile rows so
 // concurrent tiles share A and B panels in L2), all N moduli of a tile back to back.
 __device__ __forceinline__ void tile_coords(const Params& p, int j, int& tm, int& tn) {
+    if (p.tiles) {                                   // SYRK: an explicit list (triangle tiles)
+        const uint32_t v = __ldg(p.tiles + j);
+        tm = (int)(v >> 16); tn = (int)(v & 0xffffu);
+        return;
+    }
     const int gsz = p.group_tm * p.num_tn;
     const int g0 = (j / gsz) * p.group_tm;
     const int gtm = min(p.group_tm, p.num_tm - g0);
@@ -128,7 +136,7 @@ __device__ __forceinline__ void for_each_unit(const Params& p, int cid, int ncl,
     // themselves are spread over the clusters.  One call site of fn: the
     // epilogue body must stay inlined (a second call site made it a function
     // with a 600-byte stack frame)
-    const int tiles = p.num_tm * p.num_tn;
+    const int tiles = p.tiles ? p.ntiles : p.num_tm * p.num_tn;
     const int total = p.unit_parallel ? tiles * p.N : tiles;
     for (int j = cid; j < total; j += ncl) {
         const int tile = p.unit_parallel ? j / p.N : j;
@@ -214,19 +222,26 @@ __device__ __forceinline__ void crt_slice(const Params& p, const uint8_t* tile_s
                 const int fj = col < p.n ? __ldg(p.f + col) : 0;
                 o[jj] = crt_from_packed<NM>(P[2 * pr + jj], ei, fj);
             }
+            // SYRK (p.tri): only the requested triangle of C is read or written
+            bool keep[2];
+            #pragma unroll
+            for (int jj = 0; jj < 2; jj++) {
+                const int col = col0 + j + jj;
+                keep[jj] = j + jj < ncol && (p.tri == 0 || (p.tri == 1 ? col <= row : col >= row));
+            }
             if (p.axpby) {
                 // BLAS semantics (reading R19): RN(alpha c + RN(beta c_old)); C not read if beta == 0
                 #pragma unroll
                 for (int jj = 0; jj < 2; jj++) {
-                    if (j + jj < ncol)
+                    if (keep[jj])
                         o[jj] = p.beta == 0.0 ? p.alpha * o[jj] : fma(p.alpha, o[jj], p.beta * crow[j + jj]);
                 }
             }
-            if (vec) {
+            if (vec && keep[0] && keep[1]) {
                 *reinterpret_cast<double2*>(crow + j) = make_double2(o[0], o[1]);
             } else {
-                if (j < ncol) crow[j] = o[0];
-                if (j + 1 < ncol) crow[j + 1] = o[1];
+                if (keep[0]) crow[j] = o[0];
+                if (keep[1]) crow[j + 1] = o[1];
             }
         }
     }
@@ -293,7 +308,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             int step = 0, kb_in_step = 0;          // progress steps issued by this CTA
             const uint32_t nctas = gridDim.x;
             // L2 prefetch cursor, pf_dist k-blocks ahead in this CTA's load sequence
-            const int tiles = p.num_tm * p.num_tn;
+            const int tiles = p.tiles ? p.ntiles : p.num_tm * p.num_tn;
             int pj = cid, pt = 0, pkb = 0;
             auto prefetch_next = [&]() {
                 if (pj >= tiles) return;
@@ -740,14 +755,43 @@ int launch_bound_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m,
     return gemm::launch_shape<-1>(gemm_shape(), tmA, tmB, p, grid, st);
 }
 
+std::vector<uint32_t> tri_tile_list(int64_t m, int64_t n, int tri, int num_sms) {
+    using namespace gemm;
+    int grid;
+    const int cg = gemm_cta_group(), nh = gemm_halves();
+    Params p = make_params(m, n, 1, 2, num_sms, cg, nh, &grid);
+    const int tile_m = BM * cg, tile_n = BN * nh, tiles = p.num_tm * p.num_tn;
+    std::vector<uint32_t> out;
+    for (int j = 0; j < tiles; j++) {
+        // host copy of tile_coords (raster groups of group_tm tile rows)
+        const int gsz = p.group_tm * p.num_tn, g0 = (j / gsz) * p.group_tm;
+        const int gtm = std::min(p.group_tm, p.num_tm - g0), jj = j % gsz;
+        const int tm = g0 + jj % gtm, tn = jj / gtm;
+        const int64_t r0 = (int64_t)tm * tile_m, r1 = std::min<int64_t>(m, r0 + tile_m) - 1;
+        const int64_t c0 = (int64_t)tn * tile_n, c1 = std::min<int64_t>(n, c0 + tile_n) - 1;
+        if ((tri == 1 && c0 <= r1) || (tri == 2 && c1 >= r0)) out.push_back(((uint32_t)tm << 16) | (uint32_t)tn);
+    }
+    return out;
+}
+
 int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                         int N, uint8_t* scratch, const int32_t* e, const int32_t* f, double* C, int64_t ldc,
-                        uint32_t* sync_ctr, int num_sms, cudaStream_t st, double alpha, double beta) {
+                        uint32_t* sync_ctr, int num_sms, cudaStream_t st, double alpha, double beta,
+                        int tri, const uint32_t* tiles, int ntiles) {
     int grid;
     gemm::Params p = make_params(m, n, k, N, num_sms, gemm_cta_group(), gemm_halves(), &grid);
     p.scratch = scratch; p.e = e; p.f = f; p.C = C; p.ldc = ldc;
     p.axpby = (alpha != 1.0 || beta != 0.0) ? 1 : 0;
     p.alpha = alpha; p.beta = beta;
+    if (tri && tiles) {
+        if (ntiles <= 0) return 0;
+        p.tri = tri; p.tiles = tiles; p.ntiles = ntiles;
+        const int cg = gemm_cta_group();
+        const int ncl = std::min(ntiles, num_sms / cg);
+        grid = ncl * cg;
+        const int64_t kbs = (int64_t)((ntiles + ncl - 1) / ncl) * N * p.num_kb;
+        p.sync_steps_max = p.sync_kb > 0 ? (int)((kbs + p.sync_kb - 1) / p.sync_kb) + 1 : 0;
+    }
     p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
     if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
     static unsigned long long* dbg = nullptr;

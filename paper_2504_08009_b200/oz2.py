@@ -33,7 +33,7 @@ SYMBOLS = [
     "oz2_set_profiling", "oz2_stage_times", "oz2_dgemm_op", "oz2_dgemm_strided_batched",
     "oz2_scale_accu", "oz2_dgemm_scaled", "oz2_prepare_b", "oz2_dgemm_prepared", "oz2_release_b",
     "oz2_set_sm_limit", "oz2_kslice_stats_rows", "oz2_kslice_stats_cols", "oz2_exponents_from_stats",
-    "oz2_modmul_residues", "oz2_crt_sum",
+    "oz2_modmul_residues", "oz2_crt_sum", "oz2_dsyrk",
 ]
 OP_N, OP_T = 0, 1
 # stage 0 times A's conversion (and B's too with OZ2_CONV_OVERLAP=1; the two column
@@ -75,6 +75,7 @@ def lib() -> ctypes.CDLL:
                 L.oz2_dgemm_host.argtypes = [P, i64, i64, i64, P, i64, P, i64, P, i64, i32]
                 d = ctypes.c_double
                 L.oz2_dgemm_op.argtypes = [P, i32, i32, i64, i64, i64, d, P, i64, P, i64, d, P, i64, i32]
+                L.oz2_dsyrk.argtypes = [P, i32, i32, i64, i64, d, P, i64, d, P, i64, i32]
                 L.oz2_dgemm_strided_batched.argtypes = [P, i32, i32, i64, i64, i64, d, P, i64, i64, P, i64, i64,
                                                         d, P, i64, i64, i64, i32]
                 L.oz2_scale_rows.argtypes = [P, i64, i64, P, i64, i32, P]
@@ -406,6 +407,28 @@ def gemm(A, B, num_moduli: int = 14, alpha: float = 1.0, beta: float = 0.0, C=No
     _check(lib().oz2_dgemm_op(h.ptr, OP_T if transA else OP_N, OP_T if transB else OP_N, m, n, k,
                               float(alpha), _vp(A), _ld(A), _vp(B), _ld(B), float(beta), _vp(C), _ld(C),
                               num_moduli), "oz2_dgemm_op")
+    return C
+
+
+LOWER, UPPER = 1, 2
+
+
+def syrk(A, num_moduli: int = 14, uplo: str = "L", trans: bool = False, alpha: float = 1.0,
+         beta: float = 0.0, C=None, mode="fast"):
+    """C := alpha op(A) op(A)^T + beta C on the `uplo` triangle only (BLAS DSYRK
+    semantics, row-major) through oz2_dsyrk; op(A) = A.T if trans.  The other
+    triangle of C is left as it was (zeros when C is None)."""
+    import torch
+
+    A = _rowmajor(A, torch.float64)
+    n, k = (A.shape[1], A.shape[0]) if trans else A.shape
+    if C is None:
+        C = torch.zeros((n, n), dtype=torch.float64, device=A.device)
+    assert C.is_cuda and C.dtype == torch.float64 and C.shape == (n, n) and C.stride(1) == 1
+    h = handle(A.device.index)
+    h.prepare(mode, workspace_bytes(n, n, k, num_moduli))
+    _check(lib().oz2_dsyrk(h.ptr, LOWER if uplo.upper() == "L" else UPPER, OP_T if trans else OP_N, n, k,
+                           float(alpha), _vp(A), _ld(A), float(beta), _vp(C), _ld(C), num_moduli), "oz2_dsyrk")
     return C
 
 
