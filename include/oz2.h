@@ -123,6 +123,24 @@ int oz2_dgemm_op(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, i
 #define OZ2_UPPER 2
 int oz2_dsyrk(oz2_handle_t h, int uplo, int trans, int64_t n, int64_t k, double alpha,
               const double* A, int64_t lda, double beta, double* C, int64_t ldc, int num_moduli);
+/* TRMM-structured product (BLAS DTRMM semantics, reading
+ * R19), row-major, in place:
+ *   side = OZ2_LEFT:  B := alpha op(A) B, A m x m (lda >= m);
+ *   side = OZ2_RIGHT: B := alpha B op(A), A n x n (lda >= n);  B m x n (ldb >= n);
+ *   uplo: which triangle of A is referenced; diag = OZ2_UNIT: its diagonal is
+ *   taken as 1 (not read), OZ2_NON_UNIT: read.
+ * The product is Algorithm 1 on T = tri(A) (zeros outside the triangle), so
+ * every entry is bit-identical to oz2_dgemm_op(T, B) scaled by alpha; the GEMM
+ * skips, per output tile, the k-blocks where op(T) is zero (about half the
+ * work).  The masked copy T lives in handle-owned memory (grown on demand).
+ * Errors as oz2_dgemm_op; side / uplo / transA / diag out of range:
+ * OZ2_ERR_INVALID_ARG. */
+#define OZ2_LEFT 0
+#define OZ2_RIGHT 1
+#define OZ2_NON_UNIT 0
+#define OZ2_UNIT 1
+int oz2_dtrmm(oz2_handle_t h, int side, int uplo, int transA, int diag, int64_t m, int64_t n,
+              double alpha, const double* A, int64_t lda, double* B, int64_t ldb, int num_moduli);
 /* Alg. 1 lines 2-10 with caller-supplied line-1 exponents e[m], f[n] (device
  * int32, OZ2_EXP_NONFINITE allowed): C = D^-1 X E^-1.  For sharded line-1 rules
  * (e.g. OS II-accu across row blocks, where f is a MIN all-reduce of the

@@ -290,6 +290,19 @@ def syrk(A, N: int, uplo: str = "L", trans: bool = False, alpha: float = 1.0, be
     return out
 
 
+def trmm(A, B, N: int, side: str = "L", uplo: str = "L", transA: bool = False, unit: bool = False,
+         alpha: float = 1.0, mode: int = MODE_FAST) -> np.ndarray:
+    """DTRMM (reading R19): alpha op(T) B or alpha B op(T)
+    with T = the uplo triangle of A (zeros elsewhere; ones on a unit diagonal)."""
+    A = np.asarray(A, np.float64)
+    T = np.tril(A) if uplo.upper() == "L" else np.triu(A)
+    if unit:
+        np.fill_diagonal(T, 1.0)
+    if side.upper() == "L":
+        return gemm(T, B, N, alpha, 0.0, None, transA=transA, mode=mode)
+    return gemm(B, T, N, alpha, 0.0, None, transB=transA, mode=mode)
+
+
 def int_product(Ap, BpT) -> list:
     """Exact integer A' B' as a nested list of Python ints."""
     Ap = _as_f64(Ap)

@@ -100,6 +100,9 @@ struct oz2_context {
     size_t bprep_bytes;
     int bprep_valid, bprep_N, bprep_mode;
     int64_t bprep_k, bprep_n, bprep_ldr;
+    // TRMM: the masked triangular operand (handle-owned, grown on demand)
+    void* tbuf;
+    size_t tbuf_bytes;
 };
 
 namespace {
@@ -321,6 +324,7 @@ int oz2_destroy(oz2_handle_t h) {
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->ws_own) cudaFree(h->ws_own);
     if (h->bprep) cudaFree(h->bprep);
+    if (h->tbuf) cudaFree(h->tbuf);
     delete h;
     return OZ2_OK;
 }
@@ -575,7 +579,7 @@ int accu_line1(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
 // the lower / upper triangle run, and only that triangle of C is read or written.
 int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int N,
-               const int32_t* e_given = nullptr, const int32_t* f_given = nullptr, int tri = 0) {
+               const int32_t* e_given = nullptr, const int32_t* f_given = nullptr, int tri = 0, int kskip = 0) {
     if (m == 0 || n == 0) return OZ2_OK;
     const bool given = e_given && f_given;
     int rc, kstar = 0;
@@ -664,7 +668,7 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
         mark(h);
         return cuda_status();
     }
-    if (oz2::gemm_unit_parallel(m, n, gemm_sms(h)) && alpha == 1.0 && beta == 0.0) {
+    if (oz2::gemm_unit_parallel(m, n, gemm_sms(h)) && alpha == 1.0 && beta == 0.0 && !kskip) {
         // small problem (fewer output tiles than CTA pairs): the (tile, modulus)
         // units spread over all SMs (line 6-7 into uint8 planes), then lines 8-10
         // in a separate elementwise kernel
@@ -679,7 +683,7 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     }
     // Part 2-b (line 6) with Parts 2-c, 3, 4 (lines 7-10) fused into the epilogue
     if (oz2::launch_modmul_fused(&tA, &tB, m, n, k, N, scratch, e, f, C, ldc, (uint32_t*)(ws + L.off_sync),
-                                 gemm_sms(h), h->stream, alpha, beta))
+                                 gemm_sms(h), h->stream, alpha, beta, 0, nullptr, 0, kskip))
         return OZ2_ERR_CUDA;
     mark(h);
     mark(h);                                          // (no separate CRT stage)
@@ -839,6 +843,39 @@ int oz2_dgemm_op(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, i
     int rc = check_op_args(transA, transB, m, n, k, A, lda, B, ldb, C, ldc, N);
     if (rc) return rc;
     return dgemm_core(h, transA, transB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, N);
+}
+
+int oz2_dtrmm(oz2_handle_t h, int side, int uplo, int transA, int diag, int64_t m, int64_t n, double alpha,
+              const double* A, int64_t lda, double* B, int64_t ldb, int N) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    if ((side != OZ2_LEFT && side != OZ2_RIGHT) || (uplo != OZ2_LOWER && uplo != OZ2_UPPER) ||
+        (transA != OZ2_OP_N && transA != OZ2_OP_T) || (diag != OZ2_NON_UNIT && diag != OZ2_UNIT))
+        return OZ2_ERR_INVALID_ARG;
+    const int64_t na = side == OZ2_LEFT ? m : n;       // A is na x na
+    int rc = check_common(m, n, na, N);
+    if (rc) return rc;
+    if (lda < (na > 0 ? na : 1) || ldb < (n > 0 ? n : 1)) return OZ2_ERR_INVALID_ARG;
+    if (m == 0 || n == 0) return OZ2_OK;
+    if (!A || !B) return OZ2_ERR_INVALID_ARG;
+    DevGuard g(h->device);
+    // T = tri(A) (zeros outside the triangle, ones on a unit diagonal), then the
+    // product with B written over B: the GEMM reads only the residue planes,
+    // which are complete before its first store, so C may alias B (beta = 0)
+    const size_t tb = sizeof(double) * (size_t)na * (size_t)na;
+    if (h->tbuf_bytes < tb) {
+        if (h->tbuf) { cudaStreamSynchronize(h->stream); cudaFree(h->tbuf); h->tbuf = nullptr; h->tbuf_bytes = 0; }
+        if (cudaMalloc(&h->tbuf, tb) != cudaSuccess) return OZ2_ERR_CUDA;
+        h->tbuf_bytes = tb;
+    }
+    double* T = (double*)h->tbuf;
+    oz2::launch_tri_copy(A, na, lda, uplo, diag == OZ2_UNIT, T, h->stream);
+    // op(A) lower iff (lower, N) or (upper, T); its zero K blocks are skipped per output tile
+    const bool low = (uplo == OZ2_LOWER) == (transA == OZ2_OP_N);
+    if (side == OZ2_LEFT)
+        return dgemm_core(h, transA, OZ2_OP_N, m, n, m, alpha, T, m, B, ldb, 0.0, B, ldb, N, nullptr, nullptr, 0,
+                          low ? 1 : 2);
+    return dgemm_core(h, OZ2_OP_N, transA, m, n, n, alpha, B, ldb, T, n, 0.0, B, ldb, N, nullptr, nullptr, 0,
+                      low ? 3 : 4);
 }
 
 int oz2_dsyrk(oz2_handle_t h, int uplo, int trans, int64_t n, int64_t k, double alpha, const double* A,

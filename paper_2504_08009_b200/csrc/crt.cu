@@ -241,6 +241,25 @@ void launch_scale_c(double* C, int64_t m, int64_t n, int64_t ldc, double beta, c
     scale_c_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(C, m, n, ldc, beta, tri);
 }
 
+// TRMM operand: T = the uplo triangle of the n x n matrix A (1 = lower, 2 =
+// upper), zeros elsewhere, ones on the diagonal when unit != 0 (BLAS diag = 'U')
+__global__ void tri_copy_kernel(const double* __restrict__ A, int64_t n, int64_t lda, int uplo, int unit,
+                                double* __restrict__ T) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= n * n) return;
+    const int64_t i = idx / n, j = idx % n;
+    double v = 0.0;
+    if (i == j) v = unit ? 1.0 : A[i * lda + j];
+    else if (uplo == 1 ? j < i : j > i) v = A[i * lda + j];
+    T[idx] = v;
+}
+
+void launch_tri_copy(const double* A, int64_t n, int64_t lda, int uplo, int unit, double* T, cudaStream_t st) {
+    const int64_t tot = n * n;
+    if (tot <= 0) return;
+    tri_copy_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A, n, lda, uplo, unit, T);
+}
+
 template <int NM>
 __global__ void __launch_bounds__(256)
 crt_kernel(const int32_t* __restrict__ cprod, int64_t m, int64_t n, const int32_t* __restrict__ e,

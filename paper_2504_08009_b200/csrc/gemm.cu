@@ -105,6 +105,9 @@ struct Params {
     const int32_t* e;
     const int32_t* f;
     int tri;                        // SYRK: 1 = write only col <= row, 2 = only col >= row (0: all)
+    int unit_fence;                 // progress fence counted in (tile, modulus) units instead of k-blocks
+    int kskip;                      // TRMM: the triangular operand's zero K blocks are skipped per tile:
+                                    //   1: k < (tm+1) TILE_M   2: k >= tm TILE_M   3: k >= tn TILE_N   4: k < (tn+1) TILE_N
     const uint32_t* tiles;          // SYRK: the tiles to visit, (tm << 16) | tn in schedule order (or NULL)
     int ntiles;
     uint32_t* sync_ctr;             // global progress counter (zeroed before launch), or NULL
@@ -148,14 +151,27 @@ __device__ __forceinline__ void for_each_unit(const Params& p, int cid, int ncl,
     }
 }
 
-// the same sequence split into K chunks (tm, tn, t, ch, [kb0, kb1)): each chunk
-// is one int32 accumulation in TMEM; the epilogue adds the chunks' residues mod m_t
-template <typename F>
+// the k-blocks [lo, hi) a tile multiplies: all of them, or (TRMM, p.kskip) only
+// those where the triangular operand can be nonzero (the rest hold residues of 0)
+template <int TILE_M, int TILE_N>
+__device__ __forceinline__ void tile_kb_range(const Params& p, int tm, int tn, int& lo, int& hi) {
+    lo = 0; hi = p.num_kb;
+    if (p.kskip == 1) hi = min(p.num_kb, ((tm + 1) * TILE_M + BK - 1) / BK);
+    else if (p.kskip == 2) lo = min(p.num_kb - 1, (tm * TILE_M) / BK);
+    else if (p.kskip == 3) lo = min(p.num_kb - 1, (tn * TILE_N) / BK);
+    else if (p.kskip == 4) hi = min(p.num_kb, ((tn + 1) * TILE_N + BK - 1) / BK);
+}
+
+// the same sequence split into K chunks (tm, tn, t, ch, [kb0, kb1), last): each
+// chunk is one int32 accumulation in TMEM; the epilogue adds the chunks' residues mod m_t
+template <int TILE_M, int TILE_N, typename F>
 __device__ __forceinline__ void for_each_subunit(const Params& p, int cid, int ncl, F&& fn) {
     for_each_unit(p, cid, ncl, [&](int tm, int tn, int t) {
-        for (int ch = 0; ch < p.nchunk; ch++) {
-            const int kb0 = ch * p.kb_chunk;
-            fn(tm, tn, t, ch, kb0, min(p.num_kb, kb0 + p.kb_chunk));
+        int lo, hi;
+        tile_kb_range<TILE_M, TILE_N>(p, tm, tn, lo, hi);
+        for (int kb0 = lo, ch = 0; kb0 < hi; kb0 += p.kb_chunk, ch++) {
+            const int kb1 = min(hi, kb0 + p.kb_chunk);
+            fn(tm, tn, t, ch, kb0, kb1, kb1 == hi);
         }
     });
 }
@@ -324,8 +340,15 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             for_each_unit(p, cid, ncl, [&](int tm, int tn, int t) {
                 const int arow = tm * C_::TILE_M + (int)rank * BM;
                 const int brow = tn * C_::TILE_N + (int)rank * C_::B_ROWS;
-                for (int kb = 0; kb < p.num_kb; kb++) {
-                    if (p.sync_ctr && kb_in_step == 0 && step > p.sync_lag) {
+                int kb_lo, kb_hi;
+                tile_kb_range<C_::TILE_M, C_::TILE_N>(p, tm, tn, kb_lo, kb_hi);
+                if (p.sync_ctr && p.unit_fence && step > p.sync_lag) {
+                    // units of different lengths (TRMM): keep the CTAs within sync_lag units
+                    const uint32_t need = (uint32_t)(step - p.sync_lag) * nctas;
+                    while (ld_acquire_gpu(p.sync_ctr) < need) __nanosleep(64);
+                }
+                for (int kb = kb_lo; kb < kb_hi; kb++) {
+                    if (p.sync_ctr && !p.unit_fence && kb_in_step == 0 && step > p.sync_lag) {
                         // stay within sync_lag steps of the slowest CTA: the grid then
                         // streams each (wave, modulus) K-slab through L2 roughly once
                         const uint32_t need = (uint32_t)(step - p.sync_lag) * nctas;
@@ -353,11 +376,15 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     }
                     if (++stage == C_::STAGES) { stage = 0; ph ^= 1; }
                     if (p.pf_dist) prefetch_next();
-                    if (p.sync_ctr && ++kb_in_step == p.sync_kb) {
+                    if (p.sync_ctr && !p.unit_fence && ++kb_in_step == p.sync_kb) {
                         kb_in_step = 0;
                         step++;
                         red_add_release_gpu(p.sync_ctr, 1);
                     }
+                }
+                if (p.sync_ctr && p.unit_fence) {
+                    step++;
+                    red_add_release_gpu(p.sync_ctr, 1);
                 }
             });
             if (p.sync_ctr && step < p.sync_steps_max)            // retire: never hold others back
@@ -369,7 +396,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             const uint32_t idesc = idesc_i8(C_::TILE_M, BN, !BOUND);
             int stage = 0; uint32_t ph = 0;
             int acc = 0; uint32_t aph = 0;     // NH = 1: buffer and its phase; NH = 2: phase of the halves
-            for_each_subunit(p, cid, ncl, [&](int, int, int, int, int kb0, int kb1) {
+            for_each_subunit<C_::TILE_M, C_::TILE_N>(p, cid, ncl, [&](int, int, int, int, int kb0, int kb1, bool) {
                 if (NH == 1) {
                     const long long t0 = p.dbg ? clock64() : 0;
                     mbar_wait(smem_u32(&s.tempty[acc]), aph ^ 1);
@@ -446,7 +473,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             }
           }
         };
-        for_each_subunit(p, cid, ncl, [&](int tm, int tn, int t, int ch, int, int) {
+        for_each_subunit<C_::TILE_M, C_::TILE_N>(p, cid, ncl, [&](int tm, int tn, int t, int ch, int, int, bool last) {
             mbar_wait(smem_u32(&s.tfull[acc]), aph);
             tc_fence_after();
             const int row = tm * C_::TILE_M + (int)rank * BM + r;
@@ -540,7 +567,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     }
                 }
                 release();
-                if (ch == p.nchunk - 1 && p.res_out) {           // K-split: c''_t out, no CRT here
+                if (last && p.res_out) {                          // K-split: c''_t out, no CRT here
                     if (row < p.m) {
                         const int64_t blk = row / p.res_rpb;
                         uint8_t* orow = p.res_out + ((blk * p.N + t) * p.res_rpb + (row - blk * p.res_rpb)) * p.n;
@@ -562,7 +589,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             }
                         }
                     }
-                } else if (ch == p.nchunk - 1) {                  // the last K chunk of (tile, t)
+                } else if (last) {                                // the last K chunk of (tile, t)
                     // lines 8-10 of the previous tile, SLICES slices of 8 columns spread
                     // over this tile's N units (no burst that would hold TMEM back)
                     if (pend) {
@@ -777,9 +804,11 @@ std::vector<uint32_t> tri_tile_list(int64_t m, int64_t n, int tri, int num_sms) 
 int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                         int N, uint8_t* scratch, const int32_t* e, const int32_t* f, double* C, int64_t ldc,
                         uint32_t* sync_ctr, int num_sms, cudaStream_t st, double alpha, double beta,
-                        int tri, const uint32_t* tiles, int ntiles) {
+                        int tri, const uint32_t* tiles, int ntiles, int kskip) {
     int grid;
     gemm::Params p = make_params(m, n, k, N, num_sms, gemm_cta_group(), gemm_halves(), &grid);
+    p.kskip = kskip;                                  // (sync_steps_max stays the full-K bound: CTAs retire early)
+    if (kskip) p.group_tm = std::max(1, env_int("OZ2_KSKIP_GROUP", p.group_tm));   // raster (measured: 16 > 1)
     p.scratch = scratch; p.e = e; p.f = f; p.C = C; p.ldc = ldc;
     p.axpby = (alpha != 1.0 || beta != 0.0) ? 1 : 0;
     p.alpha = alpha; p.beta = beta;
@@ -793,6 +822,19 @@ int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t 
         p.sync_steps_max = p.sync_kb > 0 ? (int)((kbs + p.sync_kb - 1) / p.sync_kb) + 1 : 0;
     }
     p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
+    // TRMM: units of different lengths break the k-block fence's lockstep (every
+    // step some CTA sits at a unit boundary: 42.7 ms at 16384^3, 35.5 without a
+    // fence); OZ2_KSKIP_FENCE = 0 none, 1 k-blocks, 2 (default) one step per unit
+    if (kskip) {
+        const int kf = env_int("OZ2_KSKIP_FENCE", 2);
+        if (kf == 0) p.sync_ctr = nullptr;
+        if (kf == 2) {
+            p.unit_fence = 1;
+            const int cg = gemm_cta_group();
+            const int ncl = grid / cg, tiles = p.num_tm * p.num_tn;
+            p.sync_steps_max = ((tiles + ncl - 1) / ncl) * N + 1;
+        }
+    }
     if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
     static unsigned long long* dbg = nullptr;
     const bool want_dbg = env_int("OZ2_GEMM_DEBUG", 0) != 0;

@@ -51,12 +51,14 @@ bool gemm_unit_parallel(int64_t m, int64_t n, int num_sms);
 int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
                         int N, uint8_t* scratch, const int32_t* e, const int32_t* f, double* C, int64_t ldc,
                         uint32_t* sync_ctr, int num_sms, cudaStream_t st, double alpha = 1.0,
-                        double beta = 0.0, int tri = 0, const uint32_t* tiles = nullptr, int ntiles = 0);
+                        double beta = 0.0, int tri = 0, const uint32_t* tiles = nullptr, int ntiles = 0,
+                        int kskip = 0);
 // SYRK (tri = 1 lower, 2 upper; m = n): the output tiles of the fused GEMM that
 // meet the triangle, in the GEMM's raster order, packed (tm << 16) | tn
 std::vector<uint32_t> tri_tile_list(int64_t m, int64_t n, int tri, int num_sms);
 // C = beta C (beta != 0) or 0: the alpha = 0 / k = 0 cases of the DGEMM surface
 void launch_scale_c(double* C, int64_t m, int64_t n, int64_t ldc, double beta, cudaStream_t st, int tri = 0);
+void launch_tri_copy(const double* A, int64_t n, int64_t lda, int uplo, int unit, double* T, cudaStream_t st);
 
 // accu.cu -- Alg. 1 line 1 by the OS II-accu rule (reading R18)
 void launch_rows_hat7(const double* X, int64_t rows, int64_t k, int64_t ld, int32_t* E, uint8_t* hat, int64_t ldr,

@@ -33,7 +33,7 @@ SYMBOLS = [
     "oz2_set_profiling", "oz2_stage_times", "oz2_dgemm_op", "oz2_dgemm_strided_batched",
     "oz2_scale_accu", "oz2_dgemm_scaled", "oz2_prepare_b", "oz2_dgemm_prepared", "oz2_release_b",
     "oz2_set_sm_limit", "oz2_kslice_stats_rows", "oz2_kslice_stats_cols", "oz2_exponents_from_stats",
-    "oz2_modmul_residues", "oz2_crt_sum", "oz2_dsyrk",
+    "oz2_modmul_residues", "oz2_crt_sum", "oz2_dsyrk", "oz2_dtrmm",
 ]
 OP_N, OP_T = 0, 1
 # stage 0 times A's conversion (and B's too with OZ2_CONV_OVERLAP=1; the two column
@@ -76,6 +76,7 @@ def lib() -> ctypes.CDLL:
                 d = ctypes.c_double
                 L.oz2_dgemm_op.argtypes = [P, i32, i32, i64, i64, i64, d, P, i64, P, i64, d, P, i64, i32]
                 L.oz2_dsyrk.argtypes = [P, i32, i32, i64, i64, d, P, i64, d, P, i64, i32]
+                L.oz2_dtrmm.argtypes = [P, i32, i32, i32, i32, i64, i64, d, P, i64, P, i64, i32]
                 L.oz2_dgemm_strided_batched.argtypes = [P, i32, i32, i64, i64, i64, d, P, i64, i64, P, i64, i64,
                                                         d, P, i64, i64, i64, i32]
                 L.oz2_scale_rows.argtypes = [P, i64, i64, P, i64, i32, P]
@@ -430,6 +431,25 @@ def syrk(A, num_moduli: int = 14, uplo: str = "L", trans: bool = False, alpha: f
     _check(lib().oz2_dsyrk(h.ptr, LOWER if uplo.upper() == "L" else UPPER, OP_T if trans else OP_N, n, k,
                            float(alpha), _vp(A), _ld(A), float(beta), _vp(C), _ld(C), num_moduli), "oz2_dsyrk")
     return C
+
+
+def trmm(A, B, num_moduli: int = 14, side: str = "L", uplo: str = "L", transA: bool = False,
+         unit: bool = False, alpha: float = 1.0, mode="fast"):
+    """B := alpha op(tri(A)) B (side "L") or alpha B op(tri(A)) (side "R"), in
+    place on the CUDA tensor B (BLAS DTRMM semantics, row-major) through oz2_dtrmm."""
+    import torch
+
+    A = _rowmajor(A, torch.float64)
+    assert B.is_cuda and B.dtype == torch.float64 and B.dim() == 2 and B.stride(1) == 1
+    m, n = B.shape
+    na = m if side.upper() == "L" else n
+    assert A.shape == (na, na)
+    h = handle(A.device.index)
+    h.prepare(mode, workspace_bytes(m, n, na, num_moduli))
+    _check(lib().oz2_dtrmm(h.ptr, 0 if side.upper() == "L" else 1, LOWER if uplo.upper() == "L" else UPPER,
+                           OP_T if transA else OP_N, 1 if unit else 0, m, n, float(alpha), _vp(A), _ld(A),
+                           _vp(B), _ld(B), num_moduli), "oz2_dtrmm")
+    return B
 
 
 def gemm_strided_batched(A, B, num_moduli: int = 14, alpha: float = 1.0, beta: float = 0.0, C=None,

@@ -61,3 +61,33 @@ def test_syrk_many_tiles(oz2, oracle):
     # n = 2100: 9 x 5 tiles, about half of them skipped
     A = phi_matrix_np(2100, 200, 1.0, seed=16)
     _check(oz2, oracle, A, 14, "L", False)
+
+
+@pytest.mark.parametrize("side", ["L", "R"])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+@pytest.mark.parametrize("transA", [False, True])
+def test_trmm(oz2, oracle, side, uplo, transA):
+    # 600 x 700 B: several tiles, ragged edges; the per-tile K skipping of the zero
+    # triangle must not change a bit against the oracle (which multiplies the zeros)
+    m, n = 600, 700
+    na = m if side == "L" else n
+    A = phi_matrix_np(na, na, 1.0, seed=31)
+    B = phi_matrix_np(m, n, 1.0, seed=32)
+    for unit, alpha in ((False, 1.0), (True, -0.75)):
+        Bd = torch.from_numpy(B.copy()).to(DEV)
+        got = oz2.trmm(torch.from_numpy(A).to(DEV), Bd, 14, side, uplo, transA, unit, alpha).cpu().numpy()
+        ref = oracle.trmm(A, B, 14, side, uplo, transA, unit, alpha)
+        bad = int((got.view(np.int64) != ref.view(np.int64)).sum())
+        assert bad == 0, f"trmm side={side} uplo={uplo} transA={transA} unit={unit}: {bad} entries differ"
+
+
+def test_trmm_k_blocking_and_N20(oz2, oracle, monkeypatch):
+    # forced K chunks (2 k-blocks each) inside the per-tile K ranges, and the 96-bit residue path
+    monkeypatch.setenv("OZ2_KB_CHUNK", "2")
+    A = phi_matrix_np(900, 900, 0.5, seed=33)
+    B = phi_matrix_np(900, 300, 0.5, seed=34)
+    for N in (14, 20):
+        Bd = torch.from_numpy(B.copy()).to(DEV)
+        got = oz2.trmm(torch.from_numpy(A).to(DEV), Bd, N, "L", "U").cpu().numpy()
+        ref = oracle.trmm(A, B, N, "L", "U")
+        assert int((got.view(np.int64) != ref.view(np.int64)).sum()) == 0, f"N={N}"

@@ -46,3 +46,26 @@ def test_syrk_integer_closed_form(oracle):
     exact = A @ A.T                                     # integers < 2^53: exact in FP64
     tri = np.triu(np.ones((12, 12), bool))
     assert np.array_equal(out[tri], exact[tri]) and (out[~tri] == 0).all()
+
+
+@pytest.mark.parametrize("side", ["L", "R"])
+@pytest.mark.parametrize("uplo", ["L", "U"])
+def test_trmm_oracle_closed_forms(oracle, side, uplo):
+    """DTRMM oracle: with a unit diagonal and a zero strict triangle, op(T) = I and
+    (for a B that needs no truncation: small integers) the result is alpha B
+    exactly; with integer entries it is the exact triangular product."""
+    n, m = 9, 7
+    rng0 = np.random.Generator(np.random.PCG64(21))
+    B = rng0.integers(-1000, 1000, size=(m, n) if side == "R" else (n, m)).astype(np.float64)
+    na = n
+    Z = np.zeros((na, na))
+    out = oracle.trmm(Z, B, 14, side, uplo, unit=True, alpha=-0.5)
+    assert np.array_equal(out, -0.5 * B)
+    rng = np.random.Generator(np.random.PCG64(22))
+    A = rng.integers(-50, 50, size=(na, na)).astype(np.float64)
+    Bi = rng.integers(-50, 50, size=B.shape).astype(np.float64)
+    T = np.tril(A) if uplo == "L" else np.triu(A)
+    for transA in (False, True):
+        Top = T.T if transA else T
+        exact = Top @ Bi if side == "L" else Bi @ Top
+        assert np.array_equal(oracle.trmm(A, Bi, 14, side, uplo, transA), exact)

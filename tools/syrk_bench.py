@@ -42,3 +42,20 @@ fl = k * n * (n + 1)
 print(f"n={n} k={k} N={a.N}: syrk {t_syrk:.2f} ms ({fl / t_syrk / 1e9:.1f} TFLOPS, k n (n+1) flops), "
       f"gemm A A^T {t_gemm:.2f} ms ({2 * n * n * k / t_gemm / 1e9:.1f} TFLOPS); speed-up {t_gemm / t_syrk:.2f}x; "
       f"triangle bitwise equal: {same}")
+
+# TRMM: B := op(tri(A)) B at m = n = k, against the full product with the masked matrix
+from paper_2504_08009_b200.inputs import SEED_B
+B = phi_matrix_torch(n, n, 1.0, SEED_B, device="cuda")
+An = phi_matrix_torch(n, n, 1.0, SEED_A, device="cuda")
+T = An.tril()
+Bw = B.clone()
+t_trmm = timed(lambda: (Bw.copy_(B), oz2.trmm(An, Bw, a.N, "L", "L")))
+t_copy = timed(lambda: Bw.copy_(B))
+Bw.copy_(B)
+oz2.trmm(An, Bw, a.N, "L", "L")
+C3 = oz2.gemm(T, B, a.N)
+t_g = timed(lambda: oz2.gemm(T, B, a.N, C=C3))
+same = torch.equal(Bw.view(torch.int64), C3.view(torch.int64))
+t_trmm -= t_copy
+print(f"n={n} N={a.N}: trmm {t_trmm:.2f} ms ({n * n * n / t_trmm / 1e9:.1f} TFLOPS, n^3 flops), "
+      f"gemm tri(A) B {t_g:.2f} ms; speed-up {t_g / t_trmm:.2f}x; bitwise equal: {same}")
