@@ -91,6 +91,8 @@ struct Params {
     unsigned long long* dbg;        // experiment only: per-CTA wait-cycle counters (or NULL)
     int pf_dist;                    // k-blocks of L2 prefetch ahead of the TMA loads
     int exp_skip_b1;                // experiment only (wrong results): skip the second B half's load
+    int exp_no_crt;                 // experiment only (wrong results): skip lines 8-10 (the CRT slices)
+    int crt_prefetch;               // L2 prefetch of the next unit's CRT slice inputs
     int32_t* cprod;                 // RAW: [N][m][n]
     uint8_t* scratch;               // FUSED: [grid][2 slots][N][BM*BN] uint8 residues
     double* C;                      // FUSED
@@ -473,6 +475,17 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             }
           }
         };
+        // L2 prefetch of a slice's N residue rows (written a tile earlier, likely evicted to HBM)
+        auto prefetch_slice = [&](int sl) {
+          if constexpr (FUSED) {
+            const int c = half * CH + (sl >> 2), hh = sl & 3;
+            const uint8_t* pscr = p.scratch + (((size_t)blockIdx.x * 2 + pslot) * NM) * TB
+                                  + ((size_t)(c * BM + r)) * 32 + hh * 8;
+            #pragma unroll
+            for (int tt = 0; tt < NM; tt++)
+                asm volatile("prefetch.global.L2 [%0];" :: "l"(pscr + (size_t)tt * TB));
+          }
+        };
         for_each_subunit<C_::TILE_M, C_::TILE_N>(p, cid, ncl, [&](int tm, int tn, int t, int ch, int, int, bool last) {
             mbar_wait(smem_u32(&s.tfull[acc]), aph);
             tc_fence_after();
@@ -592,8 +605,12 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 } else if (last) {                                // the last K chunk of (tile, t)
                     // lines 8-10 of the previous tile, SLICES slices of 8 columns spread
                     // over this tile's N units (no burst that would hold TMEM back)
-                    if (pend) {
+                    if (pend && !p.exp_no_crt) {
                         const int s0 = (t * SLICES) / NM, s1 = ((t + 1) * SLICES) / NM;
+                        if (p.crt_prefetch && t + 1 < NM) {       // the next unit's slices, one unit ahead
+                            const int n1 = ((t + 2) * SLICES) / NM;
+                            for (int sl = s1; sl < n1; sl++) prefetch_slice(sl);
+                        }
                         for (int sl = s0; sl < s1; sl++) run_slice(sl);
                     }
                     if (t == NM - 1) {
@@ -695,6 +712,8 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
     p.epi_nop = env_int("OZ2_EPI_NOP", 0);
     p.pf_dist = env_int("OZ2_PF_DIST", 0);       // measured: L2 prefetch slows the GEMM (TMA contention)
     p.exp_skip_b1 = env_int("OZ2_EXP_SKIP_B1", 0);
+    p.exp_no_crt = env_int("OZ2_EXP_NO_CRT", 0);
+    p.crt_prefetch = env_int("OZ2_CRT_PREFETCH", 0);   // measured: no gain (the slices are issue-latency-bound, not HBM-bound)
     const int tiles = p.num_tm * p.num_tn;
     const int nclusters = num_sms / cg;
     const int ncl = tiles < nclusters ? tiles : nclusters;
