@@ -724,7 +724,7 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
     const int tiles = p.num_tm * p.num_tn;
     const int nclusters = num_sms / cg;
     const int ncl = tiles < nclusters ? tiles : nclusters;
-    p.sync_kb = env_int("OZ2_SYNC_KB", 64 / nh * (128 / BK));   // measured (4 x 3 A/B): 32 k-blocks per step +1 % over 16
+    p.sync_kb = env_int("OZ2_SYNC_KB", 96 / nh * (128 / BK));   // measured A/B at 16384^3: 48 k-blocks per step ~190.5, 32: 189.6, 16: 187.8 TFLOPS
     p.sync_lag = env_int("OZ2_SYNC_LAG", 0);
     {
         // busiest CTA: its tiles x N moduli x num_kb k-blocks, in sync_kb steps
