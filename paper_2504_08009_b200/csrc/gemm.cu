@@ -49,6 +49,9 @@ constexpr int BN = 256;             // UMMA N (columns of one accumulator half)
 #ifndef OZ2_BK
 #define OZ2_BK 128
 #endif
+#ifndef OZ2_EARLY_RELEASE
+#define OZ2_EARLY_RELEASE 1         // free a TMEM half before reducing its last chunk (A/B: +0.3 %, 86 GPU tests pass)
+#endif
 #ifndef OZ2_CRT_UNROLL
 #define OZ2_CRT_UNROLL 2            // both column pairs of a CRT slice inline (measured: 16384^3 -1 %, k = 256 -12 %, 4096^3 +3 %; 1: one after the other)
 #endif
@@ -560,6 +563,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const int ch_valid = min(CH, max(0, (p.n - tn * C_::TILE_N - half * CH * 32 + 31) / 32));
                 const bool quad_live = tm * C_::TILE_M + (int)rank * BM + q * 32 < p.m;
                 uint32_t va[32], vb[32];
+                bool released = false;
                 if (quad_live && ch_valid == CH) {
                 tmem_ld_32x32b_x32(tbase + (uint32_t)(half * CH * 32), va);
                 #pragma unroll
@@ -572,6 +576,9 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     store_residues<NM>(reinterpret_cast<uint4*>(tile_scr + ((size_t)(c * BM + r)) * 32), w, ch, t);
                     tmem_ld_wait_regs(vb);
                     if (cc + 2 < CH) tmem_ld_32x32b_x32(tbase + (uint32_t)((c + 2) * 32), va);
+#if OZ2_EARLY_RELEASE
+                    else { release(); released = true; }   // every TMEM read of this unit is done
+#endif
                     reduce32<NM>(vb, t, w);
                     store_residues<NM>(reinterpret_cast<uint4*>(tile_scr + ((size_t)((c + 1) * BM + r)) * 32), w, ch, t);
                 }
@@ -586,7 +593,7 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         store_residues<NM>(reinterpret_cast<uint4*>(tile_scr + ((size_t)(c * BM + r)) * 32), w, ch, t);
                     }
                 }
-                release();
+                if (!released) release();
                 if (last && p.res_out) {                          // K-split: c''_t out, no CRT here
                     if (row < p.m) {
                         const int64_t blk = row / p.res_rpb;
