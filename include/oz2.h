@@ -54,6 +54,8 @@ extern "C" {
 #define OZ2_ERR_CUDA 5          /* a CUDA runtime / driver call failed */
 #define OZ2_ERR_NO_DEVICE 6     /* no sm_100 device */
 #define OZ2_ERR_WORKSPACE 7     /* caller workspace too small */
+#define OZ2_ERR_NOT_UNIQUE 8    /* condition (13), 2 c_max < M, not certified for
+                                   caller-supplied exponents: C was set to NaN (see oz2_certify) */
 
 #define OZ2_MODE_FAST 0   /* OS II-fast: Cauchy-Schwarz bound, reading R4 */
 #define OZ2_MODE_EQ17 1   /* Eqs. (15)-(17): k_A = k_B = floor(log2((M/2-1)/q)/2) */
@@ -144,24 +146,54 @@ int oz2_dtrmm(oz2_handle_t h, int side, int uplo, int transA, int diag, int64_t 
 /* Alg. 1 lines 2-10 with caller-supplied line-1 exponents e[m], f[n] (device
  * int32, OZ2_EXP_NONFINITE allowed): C = D^-1 X E^-1.  For sharded line-1 rules
  * (e.g. OS II-accu across row blocks, where f is a MIN all-reduce of the
- * ranks' partial f).  The caller guarantees condition (13);
- * otherwise X is not unique and C is undefined. */
+ * ranks' partial f).  Condition (13) is certified on the
+ * device (oz2_certify; one statistics pass over A and B) unless disabled with
+ * oz2_set_certify(h, 0): if the certificate fails, every entry of C is set to
+ * NaN and the handle's status records OZ2_ERR_NOT_UNIQUE (read it with
+ * oz2_status -- the call itself does not synchronise). */
 int oz2_dgemm_scaled(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A,
                      int64_t lda, const double* B, int64_t ldb, const int32_t* e,
                      const int32_t* f, double* C, int64_t ldc, int num_moduli);
-/* B-stationary products: oz2_prepare_b converts B (k x n) once into
- * handle-owned device memory (Alg. 1 lines 1, 3, 5 for B: f and the residue
- * planes); each oz2_dgemm_prepared(m, A, C) then runs lines 1, 2, 4 for A and
- * 6-10 against it -- bit-identical to oz2_dgemm_ex(A, B), since e_i depends on
- * row i of A only and f_j on column j of B only (FAST / EQ17; ACCU couples the
- * operands and is rejected).  Used by the row-block pipelines (one B, many row
- * blocks of A).  Valid until the next oz2_prepare_b or oz2_release_b; the
- * handle's mode must not change in between. */
+/* ---- condition (13) certificates (Eq. 13: 2 c_max < M) ----
+ * oz2_certify writes to the device int32 *beta a bound c_max <= 2^beta for the
+ * product A B under caller-supplied exponents e[m], f[n]:
+ *   beta = max_i (e_i - e^F_i) + max_j (f_j - f^F_j) + 2T,
+ * where e^F, f^F are the OS II-fast exponents (reading R4), which guarantee
+ * ||2^(e^F_i) a_i||_2 <= 2^T; by Cauchy-Schwarz (|A'||B'|)_ij <= 2^beta.  Rows /
+ * columns that are zero, hold Inf/NaN, or carry the OZ2_EXP_NONFINITE exponent do
+ * not take part; INT32_MIN if nothing does.  beta <= L (oz2_tables) certifies
+ * uniqueness; it is a sufficient condition (Cauchy-Schwarz may overestimate).
+ * The certified stage calls (oz2_crt, oz2_crt_sum with a non-NULL beta, and
+ * oz2_dgemm_scaled) refuse when beta > L: C := NaN and the handle's sticky
+ * status becomes OZ2_ERR_NOT_UNIQUE -- no host synchronisation.
+ * oz2_status synchronises the handle's stream and returns (and clears) it. */
+int oz2_certify(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                const double* B, int64_t ldb, const int32_t* e, const int32_t* f, int num_moduli,
+                int32_t* beta);
+int oz2_set_certify(oz2_handle_t h, int enable);
+int oz2_status(oz2_handle_t h);
+/* Prepared operands: oz2_prepare_a converts A (m x k) and oz2_prepare_b converts
+ * B (k x n) once (Alg. 1 lines 1-5 for that operand: its exponents and its N
+ * residue planes) into device memory owned by the returned object (freed by
+ * oz2_release, which waits for the device).  Since e_i depends on row i of A
+ * only and f_j on column j of B only (FAST / EQ17; ACCU couples the operands
+ * and is rejected), the products are bit-identical to oz2_dgemm_ex(A, B):
+ *   oz2_dgemm_prepared(h, pb, m, A, C): lines 1, 2, 4 for A, then 6-10 against pb;
+ *   oz2_dgemm_prep2(h, pa, pb, C):      lines 6-10 only (pa->k == pb->k, same N).
+ * Used by the row-block and column-panel pipelines (one B, many row blocks of
+ * A; one A, many column panels of B).  The handle's mode must equal the mode
+ * the objects were prepared with; the objects are read-only afterwards and may
+ * be used by several handles of the same device (stream ordering is the
+ * caller's). */
+typedef struct oz2_prepared* oz2_prep_t;
+int oz2_prepare_a(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda,
+                  int num_moduli, oz2_prep_t* out);
 int oz2_prepare_b(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb,
-                  int num_moduli);
-int oz2_dgemm_prepared(oz2_handle_t h, int64_t m, const double* A, int64_t lda, double* C,
-                       int64_t ldc);
-int oz2_release_b(oz2_handle_t h);
+                  int num_moduli, oz2_prep_t* out);
+int oz2_dgemm_prepared(oz2_handle_t h, oz2_prep_t pb, int64_t m, const double* A, int64_t lda,
+                       double* C, int64_t ldc);
+int oz2_dgemm_prep2(oz2_handle_t h, oz2_prep_t pa, oz2_prep_t pb, double* C, int64_t ldc);
+int oz2_release(oz2_prep_t p);
 /* Limit the persistent GEMM to `sms` SMs (0 = all; rounded down to even), e.g.
  * to leave SMs to NCCL kernels that overlap it.  Results do not depend on it. */
 int oz2_set_sm_limit(oz2_handle_t h, int sms);
@@ -180,7 +212,8 @@ int oz2_set_sm_limit(oz2_handle_t h, int sms);
  * R = C'_t mod m_t in [0, m_t) as uint8, layout [m/rpb][N][rpb][n]
  * (rows_per_block rpb; 0 = m), ready for an all-to-all to row-block owners.
  * oz2_crt_sum: c''_t = (sum over the parts g of R + g * part_stride) mod m_t
- * (linearity of mod), then lines 8-10: C = D^-1 X E^-1 for the local rows.
+ * (linearity of mod), then lines 8-10: C = D^-1 X E^-1 for the local rows
+ * (beta: as oz2_crt).
  * All device pointers; asynchronous on the handle's stream. */
 int oz2_kslice_stats_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda,
                           const int32_t* E_global, int32_t* E_out, uint64_t* S_out);
@@ -193,7 +226,7 @@ int oz2_modmul_residues(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const i
                         int64_t rows_per_block);
 int oz2_crt_sum(oz2_handle_t h, int parts, int64_t m, int64_t n, const uint8_t* R,
                 int64_t part_stride, const int32_t* e, const int32_t* f, int num_moduli,
-                double* C, int64_t ldc);
+                double* C, int64_t ldc, const int32_t* beta);
 /* batch independent products: A + b*strideA, B + b*strideB, C + b*strideC
  * (elements), b = 0..batch-1, in stream order on one workspace. */
 int oz2_dgemm_strided_batched(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n,
@@ -254,9 +287,11 @@ int oz2_residues_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int
 int oz2_modmul(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const int8_t* Ares,
                const int8_t* Bres, int64_t ld_res, int num_moduli, int32_t* Cprod);
 /* Alg. 1 lines 7-10: c''_t = Cprod_t mod m_t in [0, m_t), X = (sum_t c''_t
- * M y_t / m_t) mod M (Eq. 1), C[i][j] = 2^-(e[i]+f[j]) RN(X)  (reading R10). */
+ * M y_t / m_t) mod M (Eq. 1), C[i][j] = 2^-(e[i]+f[j]) RN(X)  (reading R10).
+ * beta (device int32 from oz2_certify, or NULL = not certified): beta > L
+ * refuses (C := NaN, status OZ2_ERR_NOT_UNIQUE; see oz2_certify). */
 int oz2_crt(oz2_handle_t h, int64_t m, int64_t n, const int32_t* Cprod, const int32_t* e,
-            const int32_t* f, int num_moduli, double* C, int64_t ldc);
+            const int32_t* f, int num_moduli, double* C, int64_t ldc, const int32_t* beta);
 
 /* ---- constants (host memory, no device needed) ----------------------------
  * moduli[N], y[N] (M_t y_t == 1 mod m_t, least positive), w_words[5*N] with

@@ -70,8 +70,6 @@ def lib():
         L.oz2o_modmul.argtypes = [i64, i64, i64, P, P, i32, P]
         L.oz2o_crt.argtypes = [i64, i64, i32, P, P, P, P, i64, P]
         L.oz2o_dgemm.argtypes = [i64, i64, i64, P, i64, P, i64, P, i64, i32, i32, P, P]
-        L.oz2o_int_product.argtypes = [i64, i64, i64, P, P, P]
-        L.oz2o_int_product.restype = None
         L.oz2o_exact_entries.argtypes = [i64, P, i64, P, i64, i64, P, P, P, P]
         L.oz2o_exact_entries.restype = None
         L.oz2o_wide_to_double.argtypes = [P]
@@ -301,17 +299,6 @@ def trmm(A, B, N: int, side: str = "L", uplo: str = "L", transA: bool = False, u
     if side.upper() == "L":
         return gemm(T, B, N, alpha, 0.0, None, transA=transA, mode=mode)
     return gemm(B, T, N, alpha, 0.0, None, transB=transA, mode=mode)
-
-
-def int_product(Ap, BpT) -> list:
-    """Exact integer A' B' as a nested list of Python ints."""
-    Ap = _as_f64(Ap)
-    BpT = _as_f64(BpT)
-    m, k = Ap.shape
-    n = BpT.shape[0]
-    out = np.zeros((m, n, 4), np.uint64)
-    lib().oz2o_int_product(m, n, k, _p(Ap), _p(BpT), _p(out))
-    return [[limbs_to_int(out[i, j]) for j in range(n)] for i in range(m)]
 
 
 def limbs_matrix_to_ints(X) -> list:

@@ -591,8 +591,7 @@ int oz2o_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
     oz2o_residues(m, k, Ap, N, Ar);
     oz2o_residues(n, k, Bp, N, Br);
     free(Ap); free(Bp);
-    int bad = 0;
-    #pragma omp parallel for schedule(dynamic, 1) reduction(|:bad)
+    #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t i = 0; i < m; i++) {
         int64_t* cp = (int64_t*)malloc(sizeof(int64_t) * N);
         for (int64_t j = 0; j < n; j++) {
@@ -610,22 +609,7 @@ int oz2o_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
     if (e_out) memcpy(e_out, e, sizeof(int32_t) * m);
     if (f_out) memcpy(f_out, f, sizeof(int32_t) * n);
     free(e); free(f); free(Ar); free(Br);
-    return bad ? OZ2O_ERR_OVERFLOW : OZ2O_OK;
-}
-
-/* The exact integer product X = A' B' (A' m x k, B'^T n x k as FP64 integers),
- * as [m][n][4] limbs: the value the CRT must reconstruct when (13) holds
- * (PAPER.md:361-379).  Independent of every modular step above.               */
-void oz2o_int_product(int64_t m, int64_t n, int64_t k, const double* Ap,
-                      const double* BpT, uint64_t* out) {
-    #pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < m; i++)
-        for (int64_t j = 0; j < n; j++) {
-            wide_t s = w_from_i64(0);
-            for (int64_t l = 0; l < k; l++)
-                s = w_add(s, w_mul(w_from_double(Ap[i * k + l]), w_from_double(BpT[j * k + l])));
-            for (int q = 0; q < WL; q++) out[(i * n + j) * WL + q] = s.l[q];
-        }
+    return OZ2O_OK;
 }
 
 /* ------------------------------------------------------------------------- */

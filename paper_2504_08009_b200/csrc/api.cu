@@ -57,6 +57,7 @@ int ensure_device(int dev) {
         if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) { cudaSetDevice(cur); return OZ2_ERR_NO_DEVICE; }
         if (prop.major != 10) { cudaSetDevice(cur); return OZ2_ERR_NO_DEVICE; }
         cudaError_t e = cudaMemcpyToSymbol(c_tab, g_tabs, sizeof(g_tabs));
+        if (e == cudaSuccess) e = oz2::upload_tables_gemm(g_tabs, sizeof(g_tabs));
         cudaSetDevice(cur);
         if (e != cudaSuccess) return OZ2_ERR_CUDA;
         g_dev_uploaded[dev] = true;
@@ -95,14 +96,13 @@ struct oz2_context {
     cudaStream_t s_aux;
     cudaEvent_t ev_fork, ev_join;
     int sm_limit;                      // 0 = all SMs; else the persistent GEMM's SM budget
-    // B-stationary products (oz2_prepare_b): f and B's residue planes, owned here
-    void* bprep;
-    size_t bprep_bytes;
-    int bprep_valid, bprep_N, bprep_mode;
-    int64_t bprep_k, bprep_n, bprep_ldr;
     // TRMM: the masked triangular operand (handle-owned, grown on demand)
     void* tbuf;
     size_t tbuf_bytes;
+    // condition (13) certificates: device words [0] sticky refusal status,
+    // [1..2] partial maxima, [3] beta of oz2_dgemm_scaled (allocated on first use)
+    int* cert;
+    int certify;                       // oz2_dgemm_scaled certifies (default 1)
 };
 
 namespace {
@@ -241,6 +241,13 @@ int check_op_args(int ta, int tb, int64_t m, int64_t n, int64_t k, const double*
 int accu_line1(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
                const double* B, int64_t ldb, int N, uint8_t* ws, const Layout& L, int32_t* e, int32_t* f);
 
+int ensure_cert(oz2_handle_t h) {
+    if (h->cert) return OZ2_OK;
+    if (cudaMalloc(&h->cert, 16 * sizeof(int)) != cudaSuccess) { h->cert = nullptr; return OZ2_ERR_CUDA; }
+    if (cudaMemset(h->cert, 0, 16 * sizeof(int)) != cudaSuccess) return OZ2_ERR_CUDA;
+    return OZ2_OK;
+}
+
 int env_flag(const char* name, int dflt) {
     const char* v = getenv(name);
     return v && *v ? atoi(v) : dflt;
@@ -269,6 +276,7 @@ const char* oz2_strerror(int code) {
         case OZ2_ERR_CUDA: return "CUDA error";
         case OZ2_ERR_NO_DEVICE: return "no sm_100 CUDA device";
         case OZ2_ERR_WORKSPACE: return "workspace too small";
+        case OZ2_ERR_NOT_UNIQUE: return "condition (13) 2 c_max < M not certified for the given exponents (PAPER.md:370-381): C was set to NaN";
         default: return "unknown error";
     }
 }
@@ -308,6 +316,7 @@ int oz2_create(oz2_handle_t* h, int device) {
         return OZ2_ERR_CUDA;
     }
     c->mode = OZ2_MODE_FAST;
+    c->certify = 1;
     *h = c;
     return OZ2_OK;
 }
@@ -323,8 +332,8 @@ int oz2_destroy(oz2_handle_t h) {
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->ws_own) cudaFree(h->ws_own);
-    if (h->bprep) cudaFree(h->bprep);
     if (h->tbuf) cudaFree(h->tbuf);
+    if (h->cert) cudaFree(h->cert);
     delete h;
     return OZ2_OK;
 }
@@ -352,6 +361,40 @@ int oz2_set_sm_limit(oz2_handle_t h, int sms) {
     if (!h || sms < 0) return OZ2_ERR_INVALID_ARG;
     h->sm_limit = sms;
     return OZ2_OK;
+}
+
+int oz2_set_certify(oz2_handle_t h, int enable) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    h->certify = enable ? 1 : 0;
+    return OZ2_OK;
+}
+
+int oz2_status(oz2_handle_t h) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    if (!h->cert) return OZ2_OK;
+    DevGuard g(h->device);
+    int st = 0;
+    if (cudaMemcpyAsync(&st, h->cert, sizeof(int), cudaMemcpyDeviceToHost, h->stream) != cudaSuccess ||
+        cudaStreamSynchronize(h->stream) != cudaSuccess)
+        return OZ2_ERR_CUDA;
+    if (st && cudaMemsetAsync(h->cert, 0, sizeof(int), h->stream) != cudaSuccess) return OZ2_ERR_CUDA;
+    return st ? OZ2_ERR_NOT_UNIQUE : OZ2_OK;
+}
+
+int oz2_certify(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                int64_t ldb, const int32_t* e, const int32_t* f, int N, int32_t* beta) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    int rc = check_common(m, n, k, N);
+    if (rc) return rc;
+    if (!beta || lda < (k > 0 ? k : 1) || ldb < (n > 0 ? n : 1) || (m > 0 && k > 0 && (!A || !e)) ||
+        (n > 0 && k > 0 && (!B || !f)))
+        return OZ2_ERR_INVALID_ARG;
+    DevGuard g(h->device);
+    if ((rc = ensure_cert(h))) return rc;
+    uint8_t* ws;
+    if ((rc = get_workspace(h, oz2::cols_stats_bytes(k, n), &ws))) return rc;
+    oz2::launch_certify(A, m, k, lda, B, n, ldb, e, f, N, h->cert + 1, ws, beta, h->stream);
+    return cuda_status();
 }
 
 int oz2_set_profiling(oz2_handle_t h, int enable) {
@@ -504,13 +547,15 @@ int oz2_modmul(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const int8_t* Ar
 }
 
 int oz2_crt(oz2_handle_t h, int64_t m, int64_t n, const int32_t* Cprod, const int32_t* e, const int32_t* f,
-            int N, double* C, int64_t ldc) {
+            int N, double* C, int64_t ldc, const int32_t* beta) {
     if (!h) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(m, n, 0, N);
     if (rc) return rc;
     if (ldc < (n > 0 ? n : 1)) return OZ2_ERR_INVALID_ARG;
     DevGuard g(h->device);
+    if (beta && (rc = ensure_cert(h))) return rc;
     oz2::launch_crt(Cprod, m, n, e, f, N, C, ldc, h->stream);
+    if (beta) oz2::launch_refuse(beta, N, C, m, n, ldc, h->cert, h->stream);
     return cuda_status();
 }
 
@@ -890,45 +935,90 @@ int oz2_dsyrk(oz2_handle_t h, int uplo, int trans, int64_t n, int64_t k, double 
     return dgemm_core(h, trans, tb, n, n, k, alpha, A, lda, A, lda, beta, C, ldc, N, nullptr, nullptr, uplo);
 }
 
-int oz2_prepare_b(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb, int N) {
-    if (!h) return OZ2_ERR_INVALID_ARG;
-    int rc = check_common(1, n, k, N);
+// Prepared operands (oz2_prepare_a / oz2_prepare_b): exponents and residue
+// planes of one operand, in memory owned by the object (one cudaMalloc each)
+struct oz2_prepared {
+    int device, side, N, mode;           // side: OZ2_LEFT (A, rows x k) or OZ2_RIGHT (B, k x rows)
+    int64_t rows, k, ldr;
+    void* mem;
+    int32_t* exps;                       // e[rows] (A) or f[rows] (B)
+    int8_t* planes;                      // [N][rows][ldr], K-major
+};
+
+namespace {
+int prepare_common(oz2_handle_t h, int side, int64_t rows, int64_t k, const double* X, int64_t ld, int N,
+                   oz2_prep_t* out) {
+    if (!h || !out) return OZ2_ERR_INVALID_ARG;
+    *out = nullptr;
+    int rc = check_common(rows, rows, k, N);
     if (rc) return rc;
     if (h->mode == OZ2_MODE_ACCU) return OZ2_ERR_INVALID_ARG;        // accu couples A and B
-    if (ldb < (n > 0 ? n : 1) || (k > 0 && n > 0 && !B)) return OZ2_ERR_INVALID_ARG;
+    const int64_t need_ld = side == OZ2_LEFT ? (k > 0 ? k : 1) : (rows > 0 ? rows : 1);
+    if (ld < need_ld || (k > 0 && rows > 0 && !X)) return OZ2_ERR_INVALID_ARG;
     int kstar = 0;
     if (k > 0 && (rc = kstar_for(h, N, k, &kstar))) return rc;
     DevGuard g(h->device);
-    const int64_t ldr = round_up(k > 0 ? k : 1, 16);
-    const size_t off_planes = (size_t)round_up((int64_t)sizeof(int32_t) * (n > 0 ? n : 1), 256);
-    const size_t off_stats = (size_t)round_up((int64_t)(off_planes + (size_t)N * (size_t)n * (size_t)ldr), 256);
-    const size_t total = off_stats + oz2::cols_stats_bytes(k, n);
-    if (h->bprep_bytes < total) {
-        if (h->bprep) { cudaStreamSynchronize(h->stream); cudaFree(h->bprep); h->bprep = nullptr; h->bprep_bytes = 0; }
-        if (cudaMalloc(&h->bprep, total) != cudaSuccess) return OZ2_ERR_CUDA;
-        h->bprep_bytes = total;
+    oz2_prepared* p = new (std::nothrow) oz2_prepared();
+    if (!p) return OZ2_ERR_INVALID_ARG;
+    p->device = h->device; p->side = side; p->N = N; p->mode = h->mode;
+    p->rows = rows; p->k = k; p->ldr = round_up(k > 0 ? k : 1, 16);
+    const size_t off_planes = (size_t)round_up((int64_t)sizeof(int32_t) * (rows > 0 ? rows : 1), 256);
+    const size_t off_stats = (size_t)round_up((int64_t)(off_planes + (size_t)N * (size_t)rows * (size_t)p->ldr), 256);
+    const size_t total = off_stats + (side == OZ2_RIGHT ? oz2::cols_stats_bytes(k, rows) : 0);
+    if (cudaMalloc(&p->mem, total) != cudaSuccess) { delete p; return OZ2_ERR_CUDA; }
+    uint8_t* base = (uint8_t*)p->mem;
+    p->exps = (int32_t*)base;
+    p->planes = (int8_t*)(base + off_planes);
+    if (k > 0 && rows > 0) {
+        if (side == OZ2_LEFT) {
+            oz2::launch_rows(X, rows, k, ld, N, 3, h->mode, kstar, p->exps, p->planes, p->ldr, h->stream);
+        } else {
+            oz2::launch_cols_exponents(X, k, rows, ld, N, h->mode, kstar, p->exps, base + off_stats, h->stream);
+            oz2::launch_cols_residues(X, k, rows, ld, p->exps, N, p->planes, p->ldr, h->stream);
+        }
     }
-    uint8_t* base = (uint8_t*)h->bprep;
-    int32_t* f = (int32_t*)base;
-    if (k > 0 && n > 0) {
-        oz2::launch_cols_exponents(B, k, n, ldb, N, h->mode, kstar, f, base + off_stats, h->stream);
-        oz2::launch_cols_residues(B, k, n, ldb, f, N, (int8_t*)(base + off_planes), ldr, h->stream);
-    }
-    h->bprep_valid = 1; h->bprep_N = N; h->bprep_mode = h->mode;
-    h->bprep_k = k; h->bprep_n = n; h->bprep_ldr = ldr;
-    return cuda_status();
-}
-
-int oz2_release_b(oz2_handle_t h) {
-    if (!h) return OZ2_ERR_INVALID_ARG;
-    h->bprep_valid = 0;
+    if ((rc = cuda_status())) { cudaFree(p->mem); delete p; return rc; }
+    *out = p;
     return OZ2_OK;
 }
 
-int oz2_dgemm_prepared(oz2_handle_t h, int64_t m, const double* A, int64_t lda, double* C, int64_t ldc) {
-    if (!h || !h->bprep_valid || h->mode != h->bprep_mode) return OZ2_ERR_INVALID_ARG;
-    const int64_t k = h->bprep_k, n = h->bprep_n;
-    const int N = h->bprep_N;
+// lines 6-10 on converted operands: A' planes (ldr_a) x B' planes (ldr_b)
+int prepared_product(oz2_handle_t h, int64_t m, int64_t n, int64_t k, int N, const int8_t* Ares, int64_t ldr_a,
+                     const int32_t* e, const int8_t* Bres, int64_t ldr_b, const int32_t* f, double* C, int64_t ldc,
+                     uint8_t* ws, const Layout& L) {
+    int rc;
+    CUtensorMap tA, tB;
+    if ((rc = make_plane_map(&tA, Ares, m, k, ldr_a, N, 128))) return rc;
+    if ((rc = make_plane_map(&tB, Bres, n, k, ldr_b, N, 256 / oz2::gemm_cta_group()))) return rc;
+    if (oz2::launch_modmul_fused(&tA, &tB, m, n, k, N, ws + L.off_scratch, e, f, C, ldc,
+                                 (uint32_t*)(ws + L.off_sync), gemm_sms(h), h->stream))
+        return OZ2_ERR_CUDA;
+    return cuda_status();
+}
+}  // namespace
+
+int oz2_prepare_a(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda, int N, oz2_prep_t* out) {
+    return prepare_common(h, OZ2_LEFT, m, k, A, lda, N, out);
+}
+
+int oz2_prepare_b(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb, int N, oz2_prep_t* out) {
+    return prepare_common(h, OZ2_RIGHT, n, k, B, ldb, N, out);
+}
+
+int oz2_release(oz2_prep_t p) {
+    if (!p) return OZ2_ERR_INVALID_ARG;
+    DevGuard g(p->device);
+    const cudaError_t e = cudaFree(p->mem);
+    delete p;
+    return e == cudaSuccess ? OZ2_OK : OZ2_ERR_CUDA;
+}
+
+int oz2_dgemm_prepared(oz2_handle_t h, oz2_prep_t pb, int64_t m, const double* A, int64_t lda, double* C,
+                       int64_t ldc) {
+    if (!h || !pb || pb->side != OZ2_RIGHT || pb->device != h->device || h->mode != pb->mode)
+        return OZ2_ERR_INVALID_ARG;
+    const int64_t k = pb->k, n = pb->rows;
+    const int N = pb->N;
     int rc = check_common(m, n, k, N);
     if (rc) return rc;
     if (lda < (k > 0 ? k : 1) || ldc < (n > 0 ? n : 1) || (m > 0 && n > 0 && (!C || (k > 0 && !A))))
@@ -946,23 +1036,37 @@ int oz2_dgemm_prepared(oz2_handle_t h, int64_t m, const double* A, int64_t lda, 
     if ((rc = get_workspace(h, L.total, &ws))) return rc;
     int8_t* Ares = (int8_t*)(ws + L.off_Ares);
     int32_t* e = (int32_t*)(ws + L.off_e);
-    uint8_t* base = (uint8_t*)h->bprep;
-    const int32_t* f = (const int32_t*)base;
-    const int8_t* Bres = (const int8_t*)(base + (size_t)round_up((int64_t)sizeof(int32_t) * n, 256));
-    CUtensorMap tA, tB;
-    if ((rc = make_plane_map(&tA, Ares, m, k, L.ldr, N, 128))) return rc;
-    if ((rc = make_plane_map(&tB, Bres, n, k, h->bprep_ldr, N, 256 / oz2::gemm_cta_group()))) return rc;
     mark(h);
     oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
     mark(h);
     mark(h);
     mark(h);
-    if (oz2::launch_modmul_fused(&tA, &tB, m, n, k, N, ws + L.off_scratch, e, f, C, ldc,
-                                 (uint32_t*)(ws + L.off_sync), gemm_sms(h), h->stream))
-        return OZ2_ERR_CUDA;
+    if ((rc = prepared_product(h, m, n, k, N, Ares, L.ldr, e, pb->planes, pb->ldr, pb->exps, C, ldc, ws, L)))
+        return rc;
     mark(h);
     mark(h);
-    return cuda_status();
+    return OZ2_OK;
+}
+
+int oz2_dgemm_prep2(oz2_handle_t h, oz2_prep_t pa, oz2_prep_t pb, double* C, int64_t ldc) {
+    if (!h || !pa || !pb || pa->side != OZ2_LEFT || pb->side != OZ2_RIGHT || pa->device != h->device ||
+        pb->device != h->device || pa->N != pb->N || pa->k != pb->k || pa->mode != pb->mode)
+        return OZ2_ERR_INVALID_ARG;
+    const int64_t m = pa->rows, n = pb->rows, k = pa->k;
+    const int N = pa->N;
+    int rc = check_common(m, n, k, N);
+    if (rc) return rc;
+    if (ldc < (n > 0 ? n : 1) || (m > 0 && n > 0 && !C)) return OZ2_ERR_INVALID_ARG;
+    if (m == 0 || n == 0) return OZ2_OK;
+    DevGuard g(h->device);
+    if (k == 0) {
+        oz2::launch_scale_c(C, m, n, ldc, 0.0, h->stream);
+        return cuda_status();
+    }
+    Layout L = layout_for(m, n, 0, N, gemm_sms(h), 0, false);     // scratch + sync only (no planes)
+    uint8_t* ws;
+    if ((rc = get_workspace(h, L.total, &ws))) return rc;
+    return prepared_product(h, m, n, k, N, pa->planes, pa->ldr, pa->exps, pb->planes, pb->ldr, pb->exps, C, ldc, ws, L);
 }
 
 // ---------------------------------------------------------------------------
@@ -1027,13 +1131,15 @@ int oz2_modmul_residues(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const i
 }
 
 int oz2_crt_sum(oz2_handle_t h, int parts, int64_t m, int64_t n, const uint8_t* R, int64_t part_stride,
-                const int32_t* e, const int32_t* f, int N, double* C, int64_t ldc) {
+                const int32_t* e, const int32_t* f, int N, double* C, int64_t ldc, const int32_t* beta) {
     if (!h || parts < 1 || parts > (1 << 20)) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(m, n, 0, N);
     if (rc) return rc;
     if (ldc < (n > 0 ? n : 1) || (m > 0 && n > 0 && (!R || !e || !f || !C))) return OZ2_ERR_INVALID_ARG;
     DevGuard g(h->device);
+    if (beta && (rc = ensure_cert(h))) return rc;
     oz2::launch_crt_sum(R, parts, part_stride, m, n, e, f, N, C, ldc, h->stream);
+    if (beta) oz2::launch_refuse(beta, N, C, m, n, ldc, h->cert, h->stream);
     return cuda_status();
 }
 
@@ -1044,7 +1150,19 @@ int oz2_dgemm_scaled(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const doub
     int rc = check_op_args(OZ2_OP_N, OZ2_OP_N, m, n, k, A, lda, B, ldb, C, ldc, N);
     if (rc) return rc;
     if (m > 0 && n > 0 && k > 0 && (!e || !f)) return OZ2_ERR_INVALID_ARG;
-    return dgemm_core(h, OZ2_OP_N, OZ2_OP_N, m, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldc, N, e, f);
+    if (!h->certify || m == 0 || n == 0 || k == 0)
+        return dgemm_core(h, OZ2_OP_N, OZ2_OP_N, m, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldc, N, e, f);
+    // condition (13) certificate (certify.cu), then the product, then the refusal check
+    DevGuard g(h->device);
+    if ((rc = ensure_cert(h))) return rc;
+    uint8_t* ws;
+    if ((rc = get_workspace(h, oz2::cols_stats_bytes(k, n), &ws))) return rc;
+    oz2::launch_certify(A, m, k, lda, B, n, ldb, e, f, N, h->cert + 1, ws, h->cert + 3, h->stream);
+    if ((rc = cuda_status())) return rc;
+    if ((rc = dgemm_core(h, OZ2_OP_N, OZ2_OP_N, m, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldc, N, e, f))) return rc;
+    DevGuard g2(h->device);
+    oz2::launch_refuse(h->cert + 3, N, C, m, n, ldc, h->cert, h->stream);
+    return cuda_status();
 }
 
 int oz2_dgemm_strided_batched(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, int64_t k,

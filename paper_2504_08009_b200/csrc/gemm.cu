@@ -34,8 +34,7 @@
 // Schedule: tile-major (default; all N moduli of a tile back to back, tiles in
 // GROUP_TM-row groups for L2 reuse) or modulus-outer groups.  Either way a
 // tile is finalised by the CTA (and the threads) that wrote its residues.
-#include "oz2_device.cuh"
-#include "oz2_kernels.h"
+#include "crt_device.cuh"
 
 #include <algorithm>
 #include <stdlib.h>
@@ -334,7 +333,22 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (lane == 0) {
             int stage = 0; uint32_t ph = 0;
             int step = 0, kb_in_step = 0;          // progress steps issued by this CTA
-            const uint32_t nctas = gridDim.x;
+            // The progress fence (sync_ctr[0] = steps published, sync_ctr[1] =
+            // CTAs taking part) never waits for a CTA that is not running: a CTA
+            // joins only if no step has been published when it starts, and the
+            // wait threshold counts the CTAs that have joined.  A CTA that starts
+            // late (the grid was not co-resident: another kernel, MPS, a smaller
+            // part) neither waits nor is waited for; among the joined CTAs the
+            // slowest never waits, so the fence cannot deadlock.
+            bool fence = p.sync_ctr != nullptr;
+            if (fence) {
+                if (ld_acquire_gpu(p.sync_ctr) == 0) red_add_release_gpu(p.sync_ctr + 1, 1u);
+                else fence = false;
+            }
+            auto fence_wait = [&](int target) {
+                while (ld_acquire_gpu(p.sync_ctr) < (uint32_t)target * ld_acquire_gpu(p.sync_ctr + 1))
+                    __nanosleep(64);
+            };
             // L2 prefetch cursor, pf_dist k-blocks ahead in this CTA's load sequence
             const int tiles = p.tiles ? p.ntiles : p.num_tm * p.num_tn;
             int pj = cid, pt = 0, pkb = 0;
@@ -354,18 +368,16 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const int brow = tn * C_::TILE_N + (int)rank * C_::B_ROWS;
                 int kb_lo, kb_hi;
                 tile_kb_range<C_::TILE_M, C_::TILE_N>(p, tm, tn, kb_lo, kb_hi);
-                if (p.sync_ctr && p.unit_fence && step > p.sync_lag) {
+                if (fence && p.unit_fence && step > p.sync_lag) {
                     // units of different lengths (TRMM): keep the CTAs within sync_lag units
-                    const uint32_t need = (uint32_t)(step - p.sync_lag) * nctas;
-                    while (ld_acquire_gpu(p.sync_ctr) < need) __nanosleep(64);
+                    fence_wait(step - p.sync_lag);
                 }
                 for (int kb = kb_lo; kb < kb_hi; kb++) {
-                    if (p.sync_ctr && !p.unit_fence && kb_in_step == 0 && step > p.sync_lag) {
+                    if (fence && !p.unit_fence && kb_in_step == 0 && step > p.sync_lag) {
                         // stay within sync_lag steps of the slowest CTA: the grid then
                         // streams each (wave, modulus) K-slab through L2 roughly once
-                        const uint32_t need = (uint32_t)(step - p.sync_lag) * nctas;
                         const long long t0 = p.dbg ? clock64() : 0;
-                        while (ld_acquire_gpu(p.sync_ctr) < need) __nanosleep(64);
+                        fence_wait(step - p.sync_lag);
                         if (p.dbg) dbg_fence += clock64() - t0;
                     }
                     { const long long t0 = p.dbg ? clock64() : 0;
@@ -388,18 +400,18 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     }
                     if (++stage == C_::STAGES) { stage = 0; ph ^= 1; }
                     if (p.pf_dist) prefetch_next();
-                    if (p.sync_ctr && !p.unit_fence && ++kb_in_step == p.sync_kb) {
+                    if (fence && !p.unit_fence && ++kb_in_step == p.sync_kb) {
                         kb_in_step = 0;
                         step++;
                         red_add_release_gpu(p.sync_ctr, 1);
                     }
                 }
-                if (p.sync_ctr && p.unit_fence) {
+                if (fence && p.unit_fence) {
                     step++;
                     red_add_release_gpu(p.sync_ctr, 1);
                 }
             });
-            if (p.sync_ctr && step < p.sync_steps_max)            // retire: never hold others back
+            if (fence && step < p.sync_steps_max)                 // retire: never hold others back
                 red_add_release_gpu(p.sync_ctr, (uint32_t)(p.sync_steps_max - step));
         }
     } else if (warp == 1) {
@@ -694,10 +706,22 @@ static int launch_shape(int shape, const CUtensorMap* tmA, const CUtensorMap* tm
 
 }  // namespace gemm
 
+// Tuning knobs read from the environment.  env_int: schedule/shape choices that
+// never change a result (clamped where a value could stall the kernel).
+// exp_int: timing experiments that produce WRONG results or add host syncs --
+// compiled in only with -DOZ2_EXPERIMENTS (tools/, never the default build).
+// this translation unit's copy of the constant tables (api.cu uploads it)
+cudaError_t upload_tables_gemm(const void* tabs, size_t bytes) { return cudaMemcpyToSymbol(c_tab, tabs, bytes); }
+
 static int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
     return v && *v ? atoi(v) : dflt;
 }
+#ifdef OZ2_EXPERIMENTS
+static int exp_int(const char* name, int dflt) { return env_int(name, dflt); }
+#else
+static int exp_int(const char*, int dflt) { return dflt; }
+#endif
 
 // tuning knobs for experiments (env): OZ2_CG (1 | 2), OZ2_NH (1 | 2, CG = 2 only), OZ2_GROUP_TM, ...
 int gemm_cta_group() { return env_int("OZ2_CG", 2) == 1 ? 1 : 2; }
@@ -708,6 +732,46 @@ static int gemm_shape() { return gemm_cta_group() * 10 + gemm_halves(); }
 // threshold in output tiles below which the unit-parallel path is used
 static int unit_parallel_tiles(int num_sms) {
     return env_int("OZ2_UNIT_PARALLEL", 1) ? env_int("OZ2_UP_TILES", num_sms / gemm_cta_group()) : 0;
+}
+
+// clusters of the persistent GEMM that can be resident at once on this device
+// (cudaOccupancyMaxActiveClusters; every instantiation has the same shared
+// memory and block size, one CTA per SM): the grid never asks for more, so on
+// an idle device all CTAs are co-resident
+template <int CG, int NH>
+static int max_clusters_cfg() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && cache[dev] > 0) return cache[dev];
+    auto kern = gemm::modmul_kernel<2, CG, NH>;
+    const size_t smem = sizeof(gemm::Smem<CG, NH>) + 1024;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CG);
+    cfg.blockDim = dim3(gemm::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
+        cudaGetLastError();                       // clear; fall back to one cluster per CG SMs
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        n = sms / CG;
+    }
+    if (dev < 64) cache[dev] = n;
+    return n;
+}
+static int max_clusters(int cg, int nh) {
+    if (cg == 1) return max_clusters_cfg<1, 1>();
+    return nh == 2 ? max_clusters_cfg<2, 2>() : max_clusters_cfg<2, 1>();
 }
 
 static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_sms, int cg, int nh, int* grid_out) {
@@ -723,16 +787,16 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
     p.kb_chunk = std::min(KB_MAX, std::max(1, env_int("OZ2_KB_CHUNK", KB_MAX)));
     p.nchunk = std::max(1, (p.num_kb + p.kb_chunk - 1) / p.kb_chunk);
     p.group_tm = std::max(1, env_int("OZ2_GROUP_TM", GROUP_TM));
-    p.epi_nop = env_int("OZ2_EPI_NOP", 0);
-    p.pf_dist = env_int("OZ2_PF_DIST", 0);       // measured: L2 prefetch slows the GEMM (TMA contention)
-    p.exp_skip_b1 = env_int("OZ2_EXP_SKIP_B1", 0);
-    p.exp_no_crt = env_int("OZ2_EXP_NO_CRT", 0);
-    p.crt_prefetch = env_int("OZ2_CRT_PREFETCH", 0);   // measured: no gain (the slices are issue-latency-bound, not HBM-bound)
+    p.epi_nop = exp_int("OZ2_EPI_NOP", 0);
+    p.pf_dist = exp_int("OZ2_PF_DIST", 0);       // measured: L2 prefetch slows the GEMM (TMA contention)
+    p.exp_skip_b1 = exp_int("OZ2_EXP_SKIP_B1", 0);
+    p.exp_no_crt = exp_int("OZ2_EXP_NO_CRT", 0);
+    p.crt_prefetch = exp_int("OZ2_CRT_PREFETCH", 0);   // measured: no gain (the slices are issue-latency-bound, not HBM-bound)
     const int tiles = p.num_tm * p.num_tn;
-    const int nclusters = num_sms / cg;
+    const int nclusters = std::max(1, std::min(num_sms / cg, max_clusters(cg, nh)));
     const int ncl = tiles < nclusters ? tiles : nclusters;
-    p.sync_kb = env_int("OZ2_SYNC_KB", 96 / nh * (128 / BK));   // measured A/B at 16384^3: 48 k-blocks per step ~190.5, 32: 189.6, 16: 187.8 TFLOPS
-    p.sync_lag = env_int("OZ2_SYNC_LAG", 0);
+    p.sync_kb = std::max(0, env_int("OZ2_SYNC_KB", 96 / nh * (128 / BK)));   // measured A/B at 16384^3: 48 k-blocks per step ~190.5, 32: 189.6, 16: 187.8 TFLOPS
+    p.sync_lag = std::max(0, env_int("OZ2_SYNC_LAG", 0));
     {
         // busiest CTA: its tiles x N moduli x num_kb k-blocks, in sync_kb steps
         const int64_t kbs = (int64_t)((tiles + ncl - 1) / ncl) * N * p.num_kb;
@@ -746,7 +810,7 @@ size_t fused_scratch_bytes(int64_t m, int64_t n, int N, int num_sms) {
     int grid;
     const int cg = gemm_cta_group(), nh = gemm_halves();
     gemm::Params p = make_params(m, n, 1, N, num_sms, cg, nh, &grid);
-    const int tiles = p.num_tm * p.num_tn, ncl_max = num_sms / cg;
+    const int tiles = p.num_tm * p.num_tn, ncl_max = std::min(num_sms / cg, max_clusters(cg, nh));
     if (tiles < unit_parallel_tiles(num_sms)) grid = std::max(grid, std::min(tiles * N, ncl_max) * cg);   // unit-parallel
     return (size_t)grid * 2 * N * gemm::BM * gemm::BN * nh;
 }
@@ -765,7 +829,7 @@ int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int
     p.kb_chunk = std::max(1, p.num_kb);               // RAW int32 products: one accumulation (k < 2^17)
     p.nchunk = 1;
     p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
-    if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
+    if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, 2 * sizeof(uint32_t), st);
     return gemm::launch_shape<0>(gemm_shape(), tmA, tmB, p, grid, st);
 }
 
@@ -776,7 +840,8 @@ int launch_modmul_residues(const CUtensorMap* tmA, const CUtensorMap* tmB, int64
     gemm::Params p = make_params(m, n, k, N, num_sms, gemm_cta_group(), gemm_halves(), &grid);
     {
         // fewer tiles than clusters: spread the (tile, modulus) units instead
-        const int tiles = p.num_tm * p.num_tn, ncl_max = num_sms / gemm_cta_group();
+        const int tiles = p.num_tm * p.num_tn,
+                  ncl_max = std::min(num_sms / gemm_cta_group(), max_clusters(gemm_cta_group(), gemm_halves()));
         if (tiles < unit_parallel_tiles(num_sms)) {
             p.unit_parallel = 1;
             grid = std::min(tiles * N, ncl_max) * gemm_cta_group();
@@ -789,7 +854,7 @@ int launch_modmul_residues(const CUtensorMap* tmA, const CUtensorMap* tmB, int64
     p.res_out = R;
     p.res_rpb = rows_per_block > 0 ? rows_per_block : m;
     p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
-    if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
+    if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, 2 * sizeof(uint32_t), st);
     const int shape = gemm_shape();
     switch (N) {
 #define OZ2_CASE(NN) case NN: return gemm::launch_shape<NN>(shape, tmA, tmB, p, grid, st);
@@ -809,7 +874,7 @@ int launch_bound_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m,
     p.kb_chunk = std::max(1, p.num_kb);               // one exact int32 accumulation (k < 2^17)
     p.nchunk = 1;
     p.sync_ctr = p.sync_kb > 0 ? sync_ctr : nullptr;
-    if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
+    if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, 2 * sizeof(uint32_t), st);
     cudaMemsetAsync(rowmax, 0, sizeof(uint32_t) * (size_t)m, st);
     cudaMemsetAsync(colmax, 0, sizeof(uint32_t) * (size_t)n, st);
     return gemm::launch_shape<-1>(gemm_shape(), tmA, tmB, p, grid, st);
@@ -849,7 +914,7 @@ int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t 
         if (ntiles <= 0) return 0;
         p.tri = tri; p.tiles = tiles; p.ntiles = ntiles;
         const int cg = gemm_cta_group();
-        const int ncl = std::min(ntiles, num_sms / cg);
+        const int ncl = std::min(ntiles, std::min(num_sms / cg, max_clusters(cg, gemm_halves())));
         grid = ncl * cg;
         const int64_t kbs = (int64_t)((ntiles + ncl - 1) / ncl) * N * p.num_kb;
         p.sync_steps_max = p.sync_kb > 0 ? (int)((kbs + p.sync_kb - 1) / p.sync_kb) + 1 : 0;
@@ -868,9 +933,9 @@ int launch_modmul_fused(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t 
             p.sync_steps_max = ((tiles + ncl - 1) / ncl) * N + 1;
         }
     }
-    if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, sizeof(uint32_t), st);
+    if (p.sync_ctr) cudaMemsetAsync(p.sync_ctr, 0, 2 * sizeof(uint32_t), st);
     static unsigned long long* dbg = nullptr;
-    const bool want_dbg = env_int("OZ2_GEMM_DEBUG", 0) != 0;
+    const bool want_dbg = exp_int("OZ2_GEMM_DEBUG", 0) != 0;
     if (want_dbg) {
         if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 8 * 1024);
         cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 8 * 1024, st);

@@ -11,8 +11,7 @@
 // INT32_MAX an Inf / NaN (MAX propagates it).  The per-modulus products of the
 // slices are reduced mod m_t (Alg. 1 line 7) and summed mod m_t across ranks
 // (linearity of mod) before the CRT: oz2_crt_sum.
-#include "oz2_device.cuh"
-#include "oz2_kernels.h"
+#include "crt_device.cuh"
 
 namespace oz2 {
 

@@ -1,9 +1,11 @@
-// liboz2.cu -- the library is compiled as one translation unit so that the
-// __constant__ tables are shared by every kernel without relocatable device code.
+// liboz2.cu -- translation unit 1 of liboz2.so: conversion, CRT, accu, K-split,
+// certificate kernels and the C ABI.  The persistent GEMM is translation unit 2
+// (liboz2_gemm.cu).  Each unit has its own copy of the __constant__ tables;
+// api.cu uploads both.
 #include "oz2_device.cuh"
 #include "scale.cu"
 #include "crt.cu"
 #include "accu.cu"
 #include "kslice.cu"
-#include "gemm.cu"
+#include "certify.cu"
 #include "api.cu"

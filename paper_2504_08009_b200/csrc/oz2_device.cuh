@@ -11,7 +11,8 @@
 
 // per-N constants, filled once per device by api.cu (the library is one
 // translation unit, liboz2.cu, so this is the single definition)
-__constant__ Oz2Table c_tab[OZ2_MAX_MODULI + 1];
+// one copy per translation unit (static): api.cu uploads every TU's copy
+static __constant__ Oz2Table c_tab[OZ2_MAX_MODULI + 1];
 
 namespace oz2 {
 

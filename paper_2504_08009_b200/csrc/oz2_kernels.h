@@ -39,6 +39,7 @@ void launch_trunc_cols(const double* B, int64_t k, int64_t n, int64_t ldb, const
                        double* out, cudaStream_t st);
 
 // gemm.cu -- Alg. 1 line 6 on tcgen05 (kind::i8)
+cudaError_t upload_tables_gemm(const void* tabs, size_t bytes);   // gemm.cu's copy of c_tab
 int gemm_cta_group();   // 1 or 2 (CTA pairs, cta_group::2)
 int gemm_bk();          // bytes of K per shared-memory stage (128, or 64 when built with -DOZ2_BK=64)
 int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
@@ -85,6 +86,15 @@ void launch_crt_sum(const uint8_t* R, int G, int64_t part_stride, int64_t m, int
 int launch_modmul_residues(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k, int N,
                            uint8_t* scratch, uint8_t* R, int64_t rows_per_block, uint32_t* sync_ctr, int num_sms,
                            cudaStream_t st);
+
+// certify.cu -- condition (13) certificate for caller-supplied exponents
+// dmax2: two device ints (scratch); stats_scratch: cols_stats_bytes(k, n)
+void launch_certify(const double* A, int64_t m, int64_t k, int64_t lda, const double* B, int64_t n, int64_t ldb,
+                    const int32_t* e, const int32_t* f, int N, int* dmax2, void* stats_scratch, int32_t* beta,
+                    cudaStream_t st);
+// beta > L: C := NaN and atomicOr(status, 1)
+void launch_refuse(const int32_t* beta, int N, double* C, int64_t m, int64_t n, int64_t ldc, int* status,
+                   cudaStream_t st);
 
 // crt.cu -- Alg. 1 lines 7-10
 void launch_crt(const int32_t* cprod, int64_t m, int64_t n, const int32_t* e, const int32_t* f,

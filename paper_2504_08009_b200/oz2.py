@@ -22,6 +22,7 @@ MODE_FAST = 0
 MODE_EQ17 = 1
 MODE_ACCU = 2
 EXP_NONFINITE = -(2**31)
+ERR_NOT_UNIQUE = 8
 MAX_K = 2**20          # oz2_modmul (raw int32 products): 2**17
 
 # every symbol include/oz2.h declares (checked by tests/test_abi.py)
@@ -31,7 +32,8 @@ SYMBOLS = [
     "oz2_scale_cols", "oz2_trunc_rows", "oz2_trunc_cols", "oz2_residues_rows", "oz2_residues_cols",
     "oz2_modmul", "oz2_crt", "oz2_tables", "oz2_eq17_k", "oz2_strerror", "oz2_version",
     "oz2_set_profiling", "oz2_stage_times", "oz2_dgemm_op", "oz2_dgemm_strided_batched",
-    "oz2_scale_accu", "oz2_dgemm_scaled", "oz2_prepare_b", "oz2_dgemm_prepared", "oz2_release_b",
+    "oz2_scale_accu", "oz2_dgemm_scaled", "oz2_prepare_a", "oz2_prepare_b", "oz2_dgemm_prepared",
+    "oz2_dgemm_prep2", "oz2_release", "oz2_certify", "oz2_set_certify", "oz2_status",
     "oz2_set_sm_limit", "oz2_kslice_stats_rows", "oz2_kslice_stats_cols", "oz2_exponents_from_stats",
     "oz2_modmul_residues", "oz2_crt_sum", "oz2_dsyrk", "oz2_dtrmm",
 ]
@@ -82,22 +84,27 @@ def lib() -> ctypes.CDLL:
                 L.oz2_scale_rows.argtypes = [P, i64, i64, P, i64, i32, P]
                 L.oz2_scale_cols.argtypes = [P, i64, i64, P, i64, i32, P]
                 L.oz2_scale_accu.argtypes = [P, i64, i64, i64, P, i64, P, i64, i32, P, P]
-                L.oz2_prepare_b.argtypes = [P, i64, i64, P, i64, i32]
-                L.oz2_dgemm_prepared.argtypes = [P, i64, P, i64, P, i64]
-                L.oz2_release_b.argtypes = [P]
+                L.oz2_prepare_a.argtypes = [P, i64, i64, P, i64, i32, ctypes.POINTER(P)]
+                L.oz2_prepare_b.argtypes = [P, i64, i64, P, i64, i32, ctypes.POINTER(P)]
+                L.oz2_dgemm_prepared.argtypes = [P, P, i64, P, i64, P, i64]
+                L.oz2_dgemm_prep2.argtypes = [P, P, P, P, i64]
+                L.oz2_release.argtypes = [P]
+                L.oz2_certify.argtypes = [P, i64, i64, i64, P, i64, P, i64, P, P, i32, P]
+                L.oz2_set_certify.argtypes = [P, i32]
+                L.oz2_status.argtypes = [P]
                 L.oz2_set_sm_limit.argtypes = [P, i32]
                 L.oz2_kslice_stats_rows.argtypes = [P, i64, i64, P, i64, P, P, P]
                 L.oz2_kslice_stats_cols.argtypes = [P, i64, i64, P, i64, P, P, P]
                 L.oz2_exponents_from_stats.argtypes = [P, i64, P, P, i64, i32, P]
                 L.oz2_modmul_residues.argtypes = [P, i64, i64, i64, P, P, i64, i32, P, i64]
-                L.oz2_crt_sum.argtypes = [P, i32, i64, i64, P, i64, P, P, i32, P, i64]
+                L.oz2_crt_sum.argtypes = [P, i32, i64, i64, P, i64, P, P, i32, P, i64, P]
                 L.oz2_dgemm_scaled.argtypes = [P, i64, i64, i64, P, i64, P, i64, P, P, P, i64, i32]
                 L.oz2_trunc_rows.argtypes = [P, i64, i64, P, i64, P, P]
                 L.oz2_trunc_cols.argtypes = [P, i64, i64, P, i64, P, P]
                 L.oz2_residues_rows.argtypes = [P, i64, i64, P, i64, P, i32, P, i64]
                 L.oz2_residues_cols.argtypes = [P, i64, i64, P, i64, P, i32, P, i64]
                 L.oz2_modmul.argtypes = [P, i64, i64, i64, P, P, i64, i32, P]
-                L.oz2_crt.argtypes = [P, i64, i64, P, P, P, i32, P, i64]
+                L.oz2_crt.argtypes = [P, i64, i64, P, P, P, i32, P, i64, P]
                 L.oz2_tables.argtypes = [i32, P, P, P, P, P, P, P]
                 L.oz2_eq17_k.argtypes = [i32, i64]
                 L.oz2_strerror.argtypes = [i32]
@@ -228,6 +235,35 @@ def _ld(x):
     return max(int(x.stride(0)), max(1, int(x.shape[1])))
 
 
+def _same_device(dev, *xs):
+    for x in xs:
+        if x is not None and x.device != dev:
+            raise ValueError(f"tensor on {x.device}, expected {dev}")
+
+
+def _out(out, m: int, n: int, dev):
+    """The output matrix: a new (m, n) float64 tensor, or `out` validated (the
+    library writes m*n doubles with leading dimension out.stride(0))."""
+    import torch
+
+    if out is None:
+        return torch.empty((m, n), dtype=torch.float64, device=dev)
+    if not (out.dtype == torch.float64 and out.device == dev and out.dim() == 2 and tuple(out.shape) == (m, n)
+            and out.stride(1) == 1 and out.stride(0) >= max(1, n)):
+        raise ValueError(f"out must be a row-major float64 ({m}, {n}) tensor on {dev}; got "
+                         f"{out.dtype} {tuple(out.shape)} strides {tuple(out.stride())} on {out.device}")
+    return out
+
+
+def _vec_i32(v, n: int, dev, name: str):
+    import torch
+
+    v = v.to(device=dev, dtype=torch.int32).contiguous()
+    if v.numel() != n:
+        raise ValueError(f"{name}: {v.numel()} entries, expected {n}")
+    return v
+
+
 def ld_res_for(k: int) -> int:
     return max(16, (k + 15) // 16 * 16)
 
@@ -245,8 +281,8 @@ def dgemm(A, B, num_moduli: int = 14, mode="fast", out=None):
     k2, n = B.shape
     if k != k2:
         raise ValueError(f"inner dimensions differ: {A.shape} @ {B.shape}")
-    C = out if out is not None else torch.empty((m, n), dtype=torch.float64, device=A.device)
-    assert C.stride(1) == 1 and C.shape == (m, n)
+    _same_device(A.device, B)
+    C = _out(out, m, n, A.device)
     h = handle(A.device.index)
     h.prepare(mode, workspace_bytes(m, n, k, num_moduli))
     _check(lib().oz2_dgemm_ex(h.ptr, m, n, k, _vp(A), _ld(A), _vp(B), _ld(B), _vp(C), _ld(C),
@@ -254,35 +290,89 @@ def dgemm(A, B, num_moduli: int = 14, mode="fast", out=None):
     return C
 
 
-class PreparedB:
-    """B-stationary products (oz2_prepare_b / oz2_dgemm_prepared): B converted
-    once on this device's handle, then any number of row blocks of A."""
+class Prepared:
+    """A converted operand (oz2_prepare_a / oz2_prepare_b): its exponents and
+    its N residue planes in device memory owned by this object (one object, one
+    allocation; released by release() or garbage collection)."""
 
-    def __init__(self, B, num_moduli: int = 14, mode="fast"):
+    def __init__(self, X, side: str, num_moduli: int = 14, mode="fast"):
         import torch
 
-        self._B = _rowmajor(B, torch.float64)          # kept alive while prepared
-        self.k, self.n = self._B.shape
+        X = _rowmajor(X, torch.float64)
+        self.side = side
         self.N = num_moduli
         self.mode = mode
-        self.h = handle(self._B.device.index)
+        self.device = X.device
+        self.h = handle(X.device.index)
         self.h.prepare(mode)
-        _check(lib().oz2_prepare_b(self.h.ptr, self.k, self.n, _vp(self._B), _ld(self._B), num_moduli),
-               "oz2_prepare_b")
+        self._p = ctypes.c_void_p()
+        if side == "A":
+            self.rows, self.k = X.shape
+            _check(lib().oz2_prepare_a(self.h.ptr, self.rows, self.k, _vp(X), _ld(X), num_moduli,
+                                       ctypes.byref(self._p)), "oz2_prepare_a")
+        else:
+            self.k, self.rows = X.shape
+            _check(lib().oz2_prepare_b(self.h.ptr, self.k, self.rows, _vp(X), _ld(X), num_moduli,
+                                       ctypes.byref(self._p)), "oz2_prepare_b")
+
+    @property
+    def ptr(self):
+        if self._p is None or not self._p.value:
+            raise ValueError("prepared operand already released")
+        return self._p
+
+    def release(self):
+        if self._p is not None and self._p.value:
+            # the object's memory may still be read by queued work: wait first
+            self.h._torch.cuda.current_stream(self.device).synchronize()
+            _check(lib().oz2_release(self._p), "oz2_release")
+        self._p = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+class PreparedB(Prepared):
+    """B-stationary products: B (k x n) converted once, then any number of row
+    blocks of A (oz2_dgemm_prepared), or prepared A blocks (oz2_dgemm_prep2)."""
+
+    def __init__(self, B, num_moduli: int = 14, mode="fast"):
+        super().__init__(B, "B", num_moduli, mode)
+        self.n = self.rows
 
     def dgemm(self, A, out=None):
         import torch
 
         A = _rowmajor(A, torch.float64)
+        _same_device(self.device, A)
         m = A.shape[0]
-        assert A.shape[1] == self.k
-        C = out if out is not None else torch.empty((m, self.n), dtype=torch.float64, device=A.device)
+        if A.shape[1] != self.k:
+            raise ValueError(f"A has {A.shape[1]} columns, B was prepared with k = {self.k}")
+        C = _out(out, m, self.n, self.device)
         self.h.prepare(self.mode, workspace_bytes(m, self.n, self.k, self.N))
-        _check(lib().oz2_dgemm_prepared(self.h.ptr, m, _vp(A), _ld(A), _vp(C), _ld(C)), "oz2_dgemm_prepared")
+        _check(lib().oz2_dgemm_prepared(self.h.ptr, self.ptr, m, _vp(A), _ld(A), _vp(C), _ld(C)),
+               "oz2_dgemm_prepared")
         return C
 
-    def release(self):
-        _check(lib().oz2_release_b(self.h.ptr), "oz2_release_b")
+
+class PreparedA(Prepared):
+    def __init__(self, A, num_moduli: int = 14, mode="fast"):
+        super().__init__(A, "A", num_moduli, mode)
+        self.m = self.rows
+
+
+def dgemm_prep2(pa: PreparedA, pb: PreparedB, out=None):
+    """Lines 6-10 on two prepared operands (oz2_dgemm_prep2)."""
+    if pa.k != pb.k or pa.N != pb.N or pa.device != pb.device:
+        raise ValueError("prepared operands do not match (k, N, device)")
+    C = _out(out, pa.m, pb.n, pa.device)
+    h = pa.h
+    h.prepare(pa.mode, workspace_bytes(pa.m, pb.n, 0, pa.N))
+    _check(lib().oz2_dgemm_prep2(h.ptr, pa.ptr, pb.ptr, _vp(C), _ld(C)), "oz2_dgemm_prep2")
+    return C
 
 
 def set_sm_limit(sms: int, device=None):
@@ -358,29 +448,36 @@ def modmul_residues(Ares, Bres, k: int, rows_per_block: int = 0):
     return R
 
 
-def crt_sum(R, parts: int, part_stride: int, m: int, n: int, e, f, N: int, out=None):
-    """Lines 7-10 over `parts` partial residue planes: C = D^-1 X E^-1."""
+def crt_sum(R, parts: int, part_stride: int, m: int, n: int, e, f, N: int, out=None, beta=None):
+    """Lines 7-10 over `parts` partial residue planes: C = D^-1 X E^-1.
+    beta: a certificate from certify() (refusal: C := NaN, status())."""
     import torch
 
-    C = out if out is not None else torch.empty((m, n), dtype=torch.float64, device=R.device)
+    C = _out(out, m, n, R.device)
+    e = _vec_i32(e, m, R.device, "e")
+    f = _vec_i32(f, n, R.device, "f")
+    _same_device(R.device, beta)
     h = handle(R.device.index)
     h.prepare("fast")
-    _check(lib().oz2_crt_sum(h.ptr, parts, m, n, _vp(R), part_stride, _vp(e.contiguous()), _vp(f.contiguous()), N,
-                             _vp(C), _ld(C)), "oz2_crt_sum")
+    _check(lib().oz2_crt_sum(h.ptr, parts, m, n, _vp(R), part_stride, _vp(e), _vp(f), N,
+                             _vp(C), _ld(C), _vp(beta)), "oz2_crt_sum")
     return C
 
 
 def dgemm_scaled(A, B, e, f, num_moduli: int = 14, out=None):
-    """Alg. 1 lines 2-10 with given exponent vectors e (rows of A), f (columns of B)."""
+    """Alg. 1 lines 2-10 with given exponent vectors e (rows of A), f (columns of B).
+    Condition (13) is certified on the device (oz2_certify): on refusal C is NaN
+    and status() raises OZ2_ERR_NOT_UNIQUE."""
     import torch
 
     A = _rowmajor(A, torch.float64)
     B = _rowmajor(B, torch.float64)
     m, k = A.shape
     n = B.shape[1]
-    e = e.to(device=A.device, dtype=torch.int32).contiguous()
-    f = f.to(device=A.device, dtype=torch.int32).contiguous()
-    C = out if out is not None else torch.empty((m, n), dtype=torch.float64, device=A.device)
+    _same_device(A.device, B)
+    e = _vec_i32(e, m, A.device, "e")
+    f = _vec_i32(f, n, A.device, "f")
+    C = _out(out, m, n, A.device)
     h = handle(A.device.index)
     h.prepare("fast", workspace_bytes(m, n, k, num_moduli))
     _check(lib().oz2_dgemm_scaled(h.ptr, m, n, k, _vp(A), _ld(A), _vp(B), _ld(B), _vp(e), _vp(f), _vp(C), _ld(C),
@@ -607,13 +704,45 @@ def modmul(Ares, Bres, k: int):
     return out
 
 
-def crt(Cprod, e, f, out=None):
-    import torch
-
+def crt(Cprod, e, f, out=None, beta=None):
+    """Lines 7-10 on int32 products; beta: a certificate from certify()."""
     N, m, n = Cprod.shape
-    C = out if out is not None else torch.empty((m, n), dtype=torch.float64, device=Cprod.device)
+    C = _out(out, m, n, Cprod.device)
+    e = _vec_i32(e, m, Cprod.device, "e")
+    f = _vec_i32(f, n, Cprod.device, "f")
+    _same_device(Cprod.device, beta)
     h = handle(Cprod.device.index)
     h.prepare("fast")
-    _check(lib().oz2_crt(h.ptr, m, n, _vp(Cprod.contiguous()), _vp(e.contiguous()), _vp(f.contiguous()), N,
-                         _vp(C), _ld(C)), "oz2_crt")
+    _check(lib().oz2_crt(h.ptr, m, n, _vp(Cprod.contiguous()), _vp(e), _vp(f), N,
+                         _vp(C), _ld(C), _vp(beta)), "oz2_crt")
     return C
+
+
+def certify(A, B, e, f, N: int):
+    """Device int32 tensor [beta]: c_max <= 2^beta for the product A B under the
+    exponents e, f (oz2_certify; beta <= tables(N)["L"] certifies condition (13))."""
+    import torch
+
+    A = _rowmajor(A, torch.float64)
+    B = _rowmajor(B, torch.float64)
+    _same_device(A.device, B)
+    m, k = A.shape
+    n = B.shape[1]
+    e = _vec_i32(e, m, A.device, "e")
+    f = _vec_i32(f, n, A.device, "f")
+    beta = torch.empty(1, dtype=torch.int32, device=A.device)
+    h = handle(A.device.index)
+    h.prepare("fast", 16 * n * ((k + 255) // 256) + 4 * n + 4096)
+    _check(lib().oz2_certify(h.ptr, m, n, k, _vp(A), _ld(A), _vp(B), _ld(B), _vp(e), _vp(f), N, _vp(beta)),
+           "oz2_certify")
+    return beta
+
+
+def status(device=None):
+    """Waits for this device's handle and raises Oz2Error(OZ2_ERR_NOT_UNIQUE) if
+    a certified call refused since the last status() (oz2_status)."""
+    _check(lib().oz2_status(handle(device).ptr), "oz2_status")
+
+
+def set_certify(on: bool, device=None):
+    _check(lib().oz2_set_certify(handle(device).ptr, 1 if on else 0), "oz2_set_certify")

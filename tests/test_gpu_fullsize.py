@@ -28,7 +28,7 @@ def oz2():
     return o
 
 
-def _check(oz2, oracle, m, n, k, N, phi, nrows, ncols, full_rows, mode="fast"):
+def _check(oz2, oracle, m, n, k, N, phi, nrows, ncols, full_rows, mode="fast", full_cols=()):
     A = phi_matrix_torch(m, k, phi, SEED_A, device=DEV)
     B = phi_matrix_torch(k, n, phi, SEED_B, device=DEV)
     C = oz2.dgemm(A, B, N, mode)
@@ -49,13 +49,20 @@ def _check(oz2, oracle, m, n, k, N, phi, nrows, ncols, full_rows, mode="fast"):
             row = C[i].cpu().numpy()
             ref_row = oracle.dgemm(A[i:i + 1].cpu().numpy(), B.cpu().numpy(), N)[0]
             assert np.array_equal(row.view(np.int64), ref_row.view(np.int64)), f"row {i}"
+        for j in full_cols:
+            col = C[:, j].cpu().numpy()
+            ref_col = oracle.dgemm(A.cpu().numpy(), B[:, j:j + 1].cpu().numpy(), N)[:, 0]
+            assert np.array_equal(col.view(np.int64), ref_col.view(np.int64)), f"column {j}"
     ii, jj = np.meshgrid(np.arange(nrows), np.arange(ncols), indexing="ij")
     ab, absab = oracle.exact_entries(Ar, Bc, ii.ravel(), jj.ravel())
     return float(np.max(np.abs(got.ravel() - ab) / absab))
 
 
 def test_config2_headline(oz2, oracle):
-    err = _check(oz2, oracle, 16384, 16384, 16384, 14, 1.0, 32, 32, full_rows=[])
+    # sampled 32 x 32 block + 2 full rows (first / last: ragged-free edge tiles)
+    # and 2 full columns, every entry bitwise
+    err = _check(oz2, oracle, 16384, 16384, 16384, 14, 1.0, 32, 32, full_rows=[0, 16383],
+                 full_cols=[0, 16383])
     assert err < 2.0 ** -48, err                            # N = 14 at phi = 1: ~2^-50 (DESIGN R14)
 
 
