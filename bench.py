@@ -156,16 +156,39 @@ def oracle_sample(A_rows: np.ndarray, B_cols: np.ndarray, N: int, mode: str = "f
     return time.perf_counter() - t0
 
 
+# One oracle sample shape for both the cpu_baseline leg and the reference arm:
+# the first SAMPLE_ROWS rows x SAMPLE_COLS columns of C (the full k), i.e. a
+# block of the same product (the oracle converts only the sampled rows of A and
+# columns of B, so its time scales with the block, not with m, n).
+SAMPLE_ROWS, SAMPLE_COLS = 64, 512
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def sample_desc(k: int, N: int, dt: float, steps: int = 1) -> str:
+    return (f"rows 0..{SAMPLE_ROWS - 1} x cols 0..{SAMPLE_COLS - 1} of C (k={k}, N={N}) per step, "
+            f"{dt:.2f} s per step over {steps} step(s); host: {cpu_model()}")
+
+
 def run_reference(args, cfg):
-    """--impl reference: the oracle (as it stands) on the host cores; each step a
-    bounded sample (rows x cols block) of the same workload."""
+    """--impl reference: the oracle (as it stands) on the host cores; each step the
+    same bounded block of the workload as the cpu_baseline leg."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import oracle
     from paper_2504_08009_b200.inputs import phi_matrix_np
     n, k, N = cfg["n"], cfg["k"], cfg["N"]
-    r, c = 8, 128
+    r, c = SAMPLE_ROWS, SAMPLE_COLS
     # rows/cols of the same phi-distribution (host generator: same recipe)
     A = phi_matrix_np(r, k, args.phi, seed=11)
     B = phi_matrix_np(k, c, args.phi, seed=12)
@@ -182,7 +205,7 @@ def run_reference(args, cfg):
             "scaling": "weak", "vs_baseline": None, "dtype": "int64/wide-int (exact CPU oracle)",
             "data": "synthetic", "config": cfg["config"],
             "cpu_baseline": {"value": value, "unit": "TFLOPS", "cores": cores, "kind": "oracle",
-                             "sample": f"{r} rows x {c} cols of the {cfg['config']['workload']} product per step"},
+                             "sample": sample_desc(k, N, dt, args.steps)},
             "e2e": {"value": value, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -279,6 +302,7 @@ def main():
 
     h.set_profiling(True)
     h.stage_times()
+    launches0 = oz2.kernel_launches()
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -293,6 +317,7 @@ def main():
         if world > 1:
             dist.barrier()
     ms_total = ev0.elapsed_time(ev1)
+    launches = oz2.kernel_launches() - launches0     # liboz2's own launch counter (every launch site)
     stages, calls = h.stage_times()
     h.set_profiling(False)
     if world > 1:
@@ -377,10 +402,8 @@ def main():
             "roofline": roofline,
             "conversion_roofline": conv,
             "n_scaled_roofline_frac": value / world / (4500.0 / N),
-            # fast / eq17: rows, cols_stats, cols_finalize, cols_residues, modmul; accu adds
-            # rows_hat7, cols_stats, cols_finalize, cols_hat7, the bound GEMM and 2 finalizes
-            # multi-GPU (fast): cols_stats, cols_finalize, cols_residues once, rows + GEMM per piece
-            "gpu_launches": (10 if args.mode == "accu" else (5 if world == 1 else 3 + 2 * chunks)) * args.steps,
+            # counted: oz2_kernel_launches() across the timed region (rank 0's library)
+            "gpu_launches": int(launches),
             "clocks": clk.summary()}
 
     # e2e: same metric through the C ABI with host buffers (pinned), copies timed
@@ -443,14 +466,13 @@ def main():
 
     if not args.no_cpu_baseline and world == 1:
         import oracle
-        r, c = 64, 512
+        r, c = SAMPLE_ROWS, SAMPLE_COLS
         Ar = A[:r].cpu().numpy()
         Bc = B[:, :c].cpu().numpy()
         dt = oracle_sample(Ar, Bc, N, args.mode)
         line["cpu_baseline"] = {"value": 2.0 * r * c * k / dt / 1e12, "unit": "TFLOPS",
                                 "cores": oracle.get_threads(), "kind": "oracle",
-                                "sample": f"rows 0..{r - 1} x cols 0..{c - 1} of the same product "
-                                          f"(k={k}, N={N}), {dt:.1f} s"}
+                                "sample": sample_desc(k, N, dt)}
 
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -161,8 +161,12 @@ int oz2_dgemm_scaled(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const doub
  * where e^F, f^F are the OS II-fast exponents (reading R4), which guarantee
  * ||2^(e^F_i) a_i||_2 <= 2^T; by Cauchy-Schwarz (|A'||B'|)_ij <= 2^beta.  Rows /
  * columns that are zero, hold Inf/NaN, or carry the OZ2_EXP_NONFINITE exponent do
- * not take part; INT32_MIN if nothing does.  beta <= L (oz2_tables) certifies
- * uniqueness; it is a sufficient condition (Cauchy-Schwarz may overestimate).
+ * not take part; INT32_MIN if nothing does.  For k < 2^17 the OS II-accu bound
+ * (row / column maxima of the 7-bit bound GEMM, reading R18) is formed as well
+ * and the smaller bound is reported.  Exponents under which some trunc(2^e a)
+ * would not fit the residue kernels' integers (63 bits for N <= 16, 95 bits
+ * otherwise) give beta = INT32_MAX.  beta <= L (oz2_tables) certifies
+ * uniqueness; it is a sufficient condition (the bounds may overestimate).
  * The certified stage calls (oz2_crt, oz2_crt_sum with a non-NULL beta, and
  * oz2_dgemm_scaled) refuse when beta > L: C := NaN and the handle's sticky
  * status becomes OZ2_ERR_NOT_UNIQUE -- no host synchronisation.
@@ -322,6 +326,10 @@ int oz2_stage_times(oz2_handle_t h, double* ms, int64_t* calls);
 const char* oz2_strerror(int code);
 /* 100 * major + minor */
 int oz2_version(void);
+/* Kernels the library has launched since it was loaded (all handles, all
+ * devices): every launch site counts itself, so the difference across a timed
+ * region is the number of liboz2 kernels that ran in it. */
+unsigned long long oz2_kernel_launches(void);
 
 #ifdef __cplusplus
 }

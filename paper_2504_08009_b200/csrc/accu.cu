@@ -132,20 +132,20 @@ __global__ void accu_finalize_kernel(const int32_t* __restrict__ E, const uint32
 void launch_rows_hat7(const double* X, int64_t rows, int64_t k, int64_t ld, int32_t* E, uint8_t* hat, int64_t ldr,
                       cudaStream_t st) {
     if (rows <= 0) return;
-    rows_hat7_kernel<<<(unsigned)rows, 256, 0, st>>>(X, rows, k, ld, E, hat, ldr);
+    (rows_hat7_kernel<<<(unsigned)rows, 256, 0, st>>>(X, rows, k, ld, E, hat, ldr), count_launch());
 }
 
 void launch_cols_hat7(const double* X, int64_t k, int64_t cols, int64_t ld, const int32_t* F, uint8_t* hat,
                       int64_t ldr, cudaStream_t st) {
     if (cols <= 0) return;
     dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((ldr + 63) / 64));
-    cols_hat7_kernel<<<grid, 256, 0, st>>>(X, k, cols, ld, F, hat, ldr);
+    (cols_hat7_kernel<<<grid, 256, 0, st>>>(X, k, cols, ld, F, hat, ldr), count_launch());
 }
 
 void launch_accu_finalize(const int32_t* E, const uint32_t* Pmax, int64_t cnt, int N, int32_t* e, cudaStream_t st) {
     if (cnt <= 0) return;
     const int G = N <= 16 ? 61 : 93;
-    accu_finalize_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(E, Pmax, cnt, host_L(N), G, e);
+    (accu_finalize_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(E, Pmax, cnt, host_L(N), G, e), count_launch());
 }
 
 }  // namespace oz2

@@ -58,6 +58,10 @@ int ensure_device(int dev) {
         if (prop.major != 10) { cudaSetDevice(cur); return OZ2_ERR_NO_DEVICE; }
         cudaError_t e = cudaMemcpyToSymbol(c_tab, g_tabs, sizeof(g_tabs));
         if (e == cudaSuccess) e = oz2::upload_tables_gemm(g_tabs, sizeof(g_tabs));
+        if (e == cudaSuccess) {
+            oz2::launch_init_bfrag(0);
+            e = cudaStreamSynchronize(0);
+        }
         cudaSetDevice(cur);
         if (e != cudaSuccess) return OZ2_ERR_CUDA;
         g_dev_uploaded[dev] = true;
@@ -100,7 +104,8 @@ struct oz2_context {
     void* tbuf;
     size_t tbuf_bytes;
     // condition (13) certificates: device words [0] sticky refusal status,
-    // [1..2] partial maxima, [3] beta of oz2_dgemm_scaled (allocated on first use)
+    // [1] beta of oz2_dgemm_scaled, [4..8] partial maxima and the width flag
+    // (allocated on first use)
     int* cert;
     int certify;                       // oz2_dgemm_scaled certifies (default 1)
 };
@@ -240,6 +245,17 @@ int check_op_args(int ta, int tb, int64_t m, int64_t n, int64_t k, const double*
                   int64_t ldb, const double* C, int64_t ldc, int N);
 int accu_line1(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
                const double* B, int64_t ldb, int N, uint8_t* ws, const Layout& L, int32_t* e, int32_t* f);
+int certify_into(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                 int64_t ldb, const int32_t* e, const int32_t* f, int N, int32_t* beta);
+
+// a bound |trunc(2^e a)| < 2^xbits of the handle's line-1 rule: FAST ||2^e a||_2 <= 2^T
+// (reading R4), EQ17 |2^e a| < 2^k* (reading R5); ACCU (and caller exponents) 64 =
+// the residue kernels' widest integers for N
+int xbits_rule(oz2_handle_t h, int N, int kstar) {
+    if (h->mode == OZ2_MODE_FAST) return oz2::host_T(N) + 1;
+    if (h->mode == OZ2_MODE_EQ17) return kstar;
+    return 64;
+}
 
 int ensure_cert(oz2_handle_t h) {
     if (h->cert) return OZ2_OK;
@@ -262,9 +278,18 @@ int ensure_aux(oz2_handle_t h) {
 
 }  // namespace
 
+namespace oz2 {
+unsigned long long& launch_counter_ref() {
+    static unsigned long long n = 0;
+    return n;
+}
+}  // namespace oz2
+
 extern "C" {
 
-int oz2_version(void) { return 110; }
+int oz2_version(void) { return 200; }
+
+unsigned long long oz2_kernel_launches(void) { return __atomic_load_n(&oz2::launch_counter_ref(), __ATOMIC_RELAXED); }
 
 const char* oz2_strerror(int code) {
     switch (code) {
@@ -390,11 +415,7 @@ int oz2_certify(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A
         (n > 0 && k > 0 && (!B || !f)))
         return OZ2_ERR_INVALID_ARG;
     DevGuard g(h->device);
-    if ((rc = ensure_cert(h))) return rc;
-    uint8_t* ws;
-    if ((rc = get_workspace(h, oz2::cols_stats_bytes(k, n), &ws))) return rc;
-    oz2::launch_certify(A, m, k, lda, B, n, ldb, e, f, N, h->cert + 1, ws, beta, h->stream);
-    return cuda_status();
+    return certify_into(h, m, n, k, A, lda, B, ldb, e, f, N, beta);
 }
 
 int oz2_set_profiling(oz2_handle_t h, int enable) {
@@ -582,8 +603,10 @@ int check_op_args(int ta, int tb, int64_t m, int64_t n, int64_t k, const double*
 // Alg. 1 line 1 by the OS II-accu rule (reading R18): e[m], f[n] from op(A),
 // op(B).  Uses plane 0 of the residue buffers for the 7-bit approximations
 // (overwritten by the residues afterwards).  k < 2^17 (exact int32 bound GEMM).
-int accu_line1(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
-               const double* B, int64_t ldb, int N, uint8_t* ws, const Layout& L, int32_t* e, int32_t* f) {
+// OS II-accu line 1 without the last step: E, F, and the row / column maxima
+// of the bound P = Ahat Bhat^T in the workspace (L.off_E, off_F, off_pr, off_pc)
+int accu_bound(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+               const double* B, int64_t ldb, int N, uint8_t* ws, const Layout& L) {
     if (k >= (int64_t)1 << 17) return OZ2_ERR_K_TOO_LARGE;
     uint8_t* Ah = ws + L.off_Ares;
     uint8_t* Bh = ws + L.off_Bres;
@@ -609,8 +632,33 @@ int accu_line1(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     if ((rc = make_plane_map(&tB, (const int8_t*)Bh, n, k, L.ldr, 1, 256 / oz2::gemm_cta_group()))) return rc;
     if (oz2::launch_bound_gemm(&tA, &tB, m, n, k, pr, pc, (uint32_t*)(ws + L.off_sync), gemm_sms(h), h->stream))
         return OZ2_ERR_CUDA;
-    oz2::launch_accu_finalize(E, pr, m, N, e, h->stream);
-    oz2::launch_accu_finalize(F, pc, n, N, f, h->stream);
+    return cuda_status();
+}
+
+int accu_line1(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+               const double* B, int64_t ldb, int N, uint8_t* ws, const Layout& L, int32_t* e, int32_t* f) {
+    int rc = accu_bound(h, ta, tb, m, n, k, A, lda, B, ldb, N, ws, L);
+    if (rc) return rc;
+    oz2::launch_accu_finalize((int32_t*)(ws + L.off_E), (uint32_t*)(ws + L.off_pr), m, N, e, h->stream);
+    oz2::launch_accu_finalize((int32_t*)(ws + L.off_F), (uint32_t*)(ws + L.off_pc), n, N, f, h->stream);
+    return cuda_status();
+}
+
+// condition (13) certificate of caller exponents into *beta (certify.cu): the
+// Cauchy-Schwarz bound, and for k < 2^17 also the OS II-accu bound
+int certify_into(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                 int64_t ldb, const int32_t* e, const int32_t* f, int N, int32_t* beta) {
+    int rc;
+    if ((rc = ensure_cert(h))) return rc;
+    Layout L = layout_for(m, n, k, 1, gemm_sms(h), std::max(m, n));
+    uint8_t* ws;
+    if ((rc = get_workspace(h, L.total, &ws))) return rc;
+    oz2::AccuBound ab{(const int32_t*)(ws + L.off_E), (const int32_t*)(ws + L.off_F),
+                      (const uint32_t*)(ws + L.off_pr), (const uint32_t*)(ws + L.off_pc)};
+    const bool with_p = k > 0 && k < ((int64_t)1 << 17) && m > 0 && n > 0;
+    if (with_p && (rc = accu_bound(h, OZ2_OP_N, OZ2_OP_N, m, n, k, A, lda, B, ldb, N, ws, L))) return rc;
+    oz2::launch_certify(A, m, k, lda, B, n, ldb, e, f, N, h->cert + 4, ws + L.off_stats, beta, with_p ? &ab : nullptr,
+                        h->stream);
     return cuda_status();
 }
 
@@ -658,12 +706,13 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     const bool accu = h->mode == OZ2_MODE_ACCU && !given;
     const bool skip_line1 = accu || given;              // e, f known before the residue passes
     const int what = skip_line1 ? 2 : 3;
+    const int xb = given ? 64 : xbits_rule(h, N, kstar);
     auto convert_A = [&](cudaStream_t st) {
         if (ta == OZ2_OP_N) {
-            oz2::launch_rows(A, m, k, lda, N, what, h->mode, kstar, e, Ares, L.ldr, st);
+            oz2::launch_rows(A, m, k, lda, N, what, h->mode, kstar, e, Ares, L.ldr, st, 0, xb);
         } else {
             if (!skip_line1) oz2::launch_cols_exponents(A, k, m, lda, N, h->mode, kstar, e, ws + L.off_stats, st);
-            oz2::launch_cols_residues(A, k, m, lda, e, N, Ares, L.ldr, st);
+            oz2::launch_cols_residues(A, k, m, lda, e, N, Ares, L.ldr, st, 0, xb);
         }
     };
     auto convert_B_stats = [&](cudaStream_t st) {
@@ -673,8 +722,8 @@ int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, 
     };
     auto convert_B_res = [&](cudaStream_t st) {
         if (tri) return;
-        if (tb == OZ2_OP_N) oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, st);
-        else oz2::launch_rows(B, n, k, ldb, N, what, h->mode, kstar, f, Bres, L.ldr, st);
+        if (tb == OZ2_OP_N) oz2::launch_cols_residues(B, k, n, ldb, f, N, Bres, L.ldr, st, 0, xb);
+        else oz2::launch_rows(B, n, k, ldb, N, what, h->mode, kstar, f, Bres, L.ldr, st, 0, xb);
     };
     mark(h);
     if (accu && (rc = accu_line1(h, ta, tb, m, n, k, A, lda, B, ldb, N, ws, L, e, f))) return rc;
@@ -851,13 +900,14 @@ int dgemm_host_2d(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double*
         if (order[q].first == 0) {
             const int64_t c0 = c0s[x], nc = ncs[x];
             oz2::launch_cols_exponents(dB + c0, k, nc, n, N, h->mode, kstar, f + c0, ws + L.off_stats, h->stream);
-            oz2::launch_cols_residues(dB + c0, k, nc, n, f + c0, N, Bres + c0 * L.ldr, L.ldr, h->stream, psB);
+            oz2::launch_cols_residues(dB + c0, k, nc, n, f + c0, N, Bres + c0 * L.ldr, L.ldr, h->stream, psB,
+                                      xbits_rule(h, N, kstar));
             cols_in = c0 + nc;
             if (rows_in > 0 && (rc = product(0, rows_in, c0, nc, evOut[q]))) return rc;
         } else {
             const int64_t r0 = r0s[x], rows = nrs[x];
             oz2::launch_rows(dA + r0 * k, rows, k, k, N, 3, h->mode, kstar, e + r0, Ares + r0 * L.ldr, L.ldr,
-                             h->stream, psA);
+                             h->stream, psA, xbits_rule(h, N, kstar));
             rows_in = r0 + rows;
             if (cols_in > 0 && (rc = product(r0, rows, 0, cols_in, evOut[q]))) return rc;
         }
@@ -971,10 +1021,12 @@ int prepare_common(oz2_handle_t h, int side, int64_t rows, int64_t k, const doub
     p->planes = (int8_t*)(base + off_planes);
     if (k > 0 && rows > 0) {
         if (side == OZ2_LEFT) {
-            oz2::launch_rows(X, rows, k, ld, N, 3, h->mode, kstar, p->exps, p->planes, p->ldr, h->stream);
+            oz2::launch_rows(X, rows, k, ld, N, 3, h->mode, kstar, p->exps, p->planes, p->ldr, h->stream, 0,
+                             xbits_rule(h, N, kstar));
         } else {
             oz2::launch_cols_exponents(X, k, rows, ld, N, h->mode, kstar, p->exps, base + off_stats, h->stream);
-            oz2::launch_cols_residues(X, k, rows, ld, p->exps, N, p->planes, p->ldr, h->stream);
+            oz2::launch_cols_residues(X, k, rows, ld, p->exps, N, p->planes, p->ldr, h->stream, 0,
+                                      xbits_rule(h, N, kstar));
         }
     }
     if ((rc = cuda_status())) { cudaFree(p->mem); delete p; return rc; }
@@ -1037,7 +1089,7 @@ int oz2_dgemm_prepared(oz2_handle_t h, oz2_prep_t pb, int64_t m, const double* A
     int8_t* Ares = (int8_t*)(ws + L.off_Ares);
     int32_t* e = (int32_t*)(ws + L.off_e);
     mark(h);
-    oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
+    oz2::launch_rows(A, m, k, lda, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream, 0, xbits_rule(h, N, kstar));
     mark(h);
     mark(h);
     mark(h);
@@ -1155,13 +1207,10 @@ int oz2_dgemm_scaled(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const doub
     // condition (13) certificate (certify.cu), then the product, then the refusal check
     DevGuard g(h->device);
     if ((rc = ensure_cert(h))) return rc;
-    uint8_t* ws;
-    if ((rc = get_workspace(h, oz2::cols_stats_bytes(k, n), &ws))) return rc;
-    oz2::launch_certify(A, m, k, lda, B, n, ldb, e, f, N, h->cert + 1, ws, h->cert + 3, h->stream);
-    if ((rc = cuda_status())) return rc;
+    if ((rc = certify_into(h, m, n, k, A, lda, B, ldb, e, f, N, h->cert + 1))) return rc;
     if ((rc = dgemm_core(h, OZ2_OP_N, OZ2_OP_N, m, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldc, N, e, f))) return rc;
     DevGuard g2(h->device);
-    oz2::launch_refuse(h->cert + 3, N, C, m, n, ldc, h->cert, h->stream);
+    oz2::launch_refuse(h->cert + 1, N, C, m, n, ldc, h->cert, h->stream);
     return cuda_status();
 }
 
@@ -1313,14 +1362,15 @@ int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
     mark(h);                                                  // rows of A are timed inside the GEMM stage here
     oz2::launch_cols_exponents(dB, k, n, n, N, h->mode, kstar, f, ws + L.off_stats, h->stream);
     mark(h);
-    oz2::launch_cols_residues(dB, k, n, n, f, N, Bres, L.ldr, h->stream);
+    oz2::launch_cols_residues(dB, k, n, n, f, N, Bres, L.ldr, h->stream, 0, xbits_rule(h, N, kstar));
     mark(h);
     CUtensorMap tB;
     if ((rc = make_plane_map(&tB, Bres, n, k, L.ldr, N, 256 / oz2::gemm_cta_group()))) return rc;
     for (int64_t b = 0; b < nblk; b++) {
         const int64_t r0 = blk_r0[b], rows = blk_rows[b];
         cudaStreamWaitEvent(h->stream, evA[b], 0);
-        oz2::launch_rows(dA + r0 * k, rows, k, k, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream);
+        oz2::launch_rows(dA + r0 * k, rows, k, k, N, 3, h->mode, kstar, e, Ares, L.ldr, h->stream, 0,
+                         xbits_rule(h, N, kstar));
         CUtensorMap tA;
         if ((rc = make_plane_map(&tA, Ares, rows, k, L.ldr, N, 128))) return rc;
         if (oz2::launch_modmul_fused(&tA, &tB, rows, n, k, N, ws + L.off_scratch, e, f, dC + r0 * n, n,

@@ -9,7 +9,10 @@
 //   (|A'||B'|)_ij <= ||a'_i||_2 ||b'_j||_2 <= 2^{(e_i - e^F_i) + T} 2^{(f_j - f^F_j) + T}
 // by Cauchy-Schwarz.  beta = max_i (e_i - e^F_i) + max_j (f_j - f^F_j) + 2T is
 // therefore a bound c_max <= 2^beta, and beta <= L (2^L <= M/2 - 1) certifies
-// (13).  It is a sufficient condition only.  Rows / columns that are zero or
+// (13).  For k < 2^17 the OS II-accu bound (certify_p_kernel) is formed too and
+// the smaller of the two is reported.  A sufficient condition only.  Exponents
+// under which some |trunc(2^e a)| would not fit the residue kernels' integers
+// (63 bits for N <= 16, 95 bits otherwise) give beta = INT32_MAX (refused).  Rows / columns that are zero or
 // hold Inf/NaN, and rows / columns whose caller exponent is the non-finite
 // sentinel, do not take part (their entries of C are 0 or NaN by construction).
 #include "oz2_device.cuh"
@@ -25,7 +28,7 @@ __device__ __forceinline__ int clamp_i32(long long v) {
 // atomicMax(dmax, e_i - e^F_i) for a row that takes part
 __global__ void __launch_bounds__(256)
 certify_rows_kernel(const double* __restrict__ A, int64_t m, int64_t k, int64_t lda, const int32_t* __restrict__ e,
-                    int Tb, int* __restrict__ dmax) {
+                    int Tb, int width, int* __restrict__ dmax, int* __restrict__ wflag) {
     extern __shared__ __align__(16) unsigned char row_smem[];
     const int64_t i = blockIdx.x;
     if (i >= m) return;
@@ -49,13 +52,15 @@ certify_rows_kernel(const double* __restrict__ A, int64_t m, int64_t k, int64_t 
     if (lane == 0 && ei != OZ2_EXP_NONFINITE_DEV) {
         const long long eF = (long long)Tb + 15 - E - log4_ceil(S);
         atomicMax(dmax, clamp_i32((long long)ei - eF));
+        if ((long long)ei + E + 1 > width) atomicOr(wflag, 1);     // |a'| < 2^(e + E + 1) must fit
     }
 }
 
 // columns: per-chunk statistics from cols_stats_kernel ([nch][n])
 __global__ void certify_cols_kernel(const int32_t* __restrict__ Ec, const unsigned long long* __restrict__ Sc,
                                     const int32_t* __restrict__ bad, int64_t n, int nch,
-                                    const int32_t* __restrict__ f, int Tb, int* __restrict__ dmax) {
+                                    const int32_t* __restrict__ f, int Tb, int width, int* __restrict__ dmax,
+                                    int* __restrict__ wflag) {
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (j >= n) return;
     int E = INT32_MIN;
@@ -68,12 +73,46 @@ __global__ void certify_cols_kernel(const int32_t* __restrict__ Ec, const unsign
     }
     const long long fF = (long long)Tb + 15 - E - log4_ceil(S);
     atomicMax(dmax, clamp_i32((long long)f[j] - fF));
+    if ((long long)f[j] + E + 1 > width) atomicOr(wflag, 1);
 }
 
-// beta = dmax[0] + dmax[1] + 2T, or INT32_MIN if no row or no column takes part
-__global__ void certify_finalize_kernel(const int* __restrict__ dmax, int Tb, int32_t* __restrict__ beta) {
+// the OS II-accu bound (reading R18): with E_i = max ilogb |a_il|, the 7-bit
+// approximations give (|A||B|)_ij <= P_ij 2^(E_i + F_j - 12), P = Ahat Bhat^T, and
+// P_ij <= sqrt(R_i C_j) with the row / column maxima R, C of P; so for g_i =
+// e_i + E_i, h_j = f_j + F_j:
+//   (|A'||B'|)_ij <= 2^((2 g_i - 12 + lambda_i) / 2 + (2 h_j - 12 + mu_j) / 2),
+// lambda = ceil(log2 R), mu = ceil(log2 C).  dmax2[0] = max over the rows of
+// 2 g_i - 12 + lambda_i (dmax2[1]: columns).  The accu rule's own exponents
+// satisfy each term <= L by construction, which the
+// Cauchy-Schwarz bound above does not always certify.
+__global__ void certify_p_kernel(const int32_t* __restrict__ E, const uint32_t* __restrict__ Pmax,
+                                 const int32_t* __restrict__ e, int64_t cnt, int* __restrict__ dmax) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= cnt) return;
+    const int Ei = E[i];
+    const uint32_t p = Pmax[i];
+    if (Ei == OZ2_EXP_NONFINITE_DEV || Ei == OZ2_EXP_ZERO_DEV || p == 0 || e[i] == OZ2_EXP_NONFINITE_DEV) return;
+    const int lam = p <= 1 ? 0 : 32 - __clz((int)(p - 1));              // ceil(log2 p)
+    atomicMax(dmax, clamp_i32(2LL * ((long long)e[i] + Ei) - 12 + lam));
+}
+
+// beta = min(beta_CS, beta_P): beta_CS = dmax[0] + dmax[1] + 2T, beta_P =
+// ceil((dmax[2] + dmax[3]) / 2) (when computed); INT32_MIN if no row or no
+// column takes part.  Either is an upper bound of log2 c_max.
+__global__ void certify_finalize_kernel(const int* __restrict__ dmax, int Tb, int with_p, int32_t* __restrict__ beta) {
+    if (dmax[4]) { *beta = INT32_MAX; return; }            // a scaled entry exceeds the kernels' integers
     const int a = dmax[0], b = dmax[1];
-    *beta = (a == INT32_MIN || b == INT32_MIN) ? INT32_MIN : clamp_i32((long long)a + b + 2LL * Tb);
+    if (a == INT32_MIN || b == INT32_MIN) { *beta = INT32_MIN; return; }
+    long long bt = (long long)a + b + 2LL * Tb;
+    if (with_p) {
+        const int c = dmax[2], d = dmax[3];
+        if (c != INT32_MIN && d != INT32_MIN) {
+            const long long s = (long long)c + d;
+            const long long bp = s >= 0 ? (s + 1) / 2 : -((-s) / 2);     // ceil(s / 2)
+            bt = bp < bt ? bp : bt;
+        }
+    }
+    *beta = clamp_i32(bt);
 }
 
 // refusal (the error behaviour of the certified calls): when beta > L every
@@ -90,16 +129,24 @@ __global__ void refuse_kernel(const int32_t* __restrict__ beta, int L, double* _
         C[(x / n) * ldc + x % n] = nan;
 }
 
+__global__ void certify_init_kernel(int* __restrict__ dmax) {
+    if (threadIdx.x < 4) dmax[threadIdx.x] = INT32_MIN;
+    if (threadIdx.x == 4) dmax[4] = 0;
+}
+
 void launch_certify(const double* A, int64_t m, int64_t k, int64_t lda, const double* B, int64_t n, int64_t ldb,
-                    const int32_t* e, const int32_t* f, int N, int* dmax2, void* stats_scratch, int32_t* beta,
-                    cudaStream_t st) {
+                    const int32_t* e, const int32_t* f, int N, int* dmax4, void* stats_scratch, int32_t* beta,
+                    const AccuBound* ab, cudaStream_t st) {
     const int Tb = host_T(N);
-    static const int init[2] = {INT32_MIN, INT32_MIN};
-    cudaMemcpyAsync(dmax2, init, sizeof(init), cudaMemcpyHostToDevice, st);
+    // the residue kernels hold trunc(2^e a) in 63 (N <= 16) or 95 bits (scale.cu BW_8 / BW_12)
+    const int width = N <= 16 ? 63 : 95;
+    int* dmax2 = dmax4;
+    (certify_init_kernel<<<1, 32, 0, st>>>(dmax4), count_launch());
     if (m > 0 && k > 0) {
         const size_t smem = row_smem_bytes(k);
         if (smem > 48 * 1024) cudaFuncSetAttribute(certify_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        certify_rows_kernel<<<(unsigned)m, 256, smem, st>>>(A, m, k, lda, e, Tb, dmax2);
+        (certify_rows_kernel<<<(unsigned)m, 256, smem, st>>>(A, m, k, lda, e, Tb, width, dmax2, dmax4 + 4),
+         count_launch());
     }
     const int64_t nch = (k + KC - 1) / KC;
     if (n > 0 && nch > 0) {
@@ -108,16 +155,22 @@ void launch_certify(const double* A, int64_t m, int64_t k, int64_t lda, const do
         int32_t* bad = Ec + nch * n;
         cudaMemsetAsync(bad, 0, sizeof(int32_t) * n, st);
         dim3 grid((unsigned)((n + 31) / 32), (unsigned)nch);
-        cols_stats_kernel<0><<<grid, 32 * CS_WARPS, 0, st>>>(B, k, n, ldb, Ec, Sc, bad);
-        certify_cols_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, f, Tb, dmax2 + 1);
+        (cols_stats_kernel<0><<<grid, 32 * CS_WARPS, 0, st>>>(B, k, n, ldb, Ec, Sc, bad), count_launch());
+        (certify_cols_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, f, Tb, width,
+                                                                            dmax2 + 1, dmax4 + 4),
+         count_launch());
     }
-    certify_finalize_kernel<<<1, 1, 0, st>>>(dmax2, Tb, beta);
+    if (ab) {
+        if (m > 0) (certify_p_kernel<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(ab->E, ab->rowmax, e, m, dmax4 + 2), count_launch());
+        if (n > 0) (certify_p_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(ab->F, ab->colmax, f, n, dmax4 + 3), count_launch());
+    }
+    (certify_finalize_kernel<<<1, 1, 0, st>>>(dmax4, Tb, ab ? 1 : 0, beta), count_launch());
 }
 
 void launch_refuse(const int32_t* beta, int N, double* C, int64_t m, int64_t n, int64_t ldc, int* status,
                    cudaStream_t st) {
     if (m * n == 0) return;
-    refuse_kernel<<<148, 256, 0, st>>>(beta, host_L(N), C, m, n, ldc, status);
+    (refuse_kernel<<<148, 256, 0, st>>>(beta, host_L(N), C, m, n, ldc, status), count_launch());
 }
 
 }  // namespace oz2

@@ -19,7 +19,7 @@ __global__ void scale_c_kernel(double* __restrict__ C, int64_t m, int64_t n, int
 void launch_scale_c(double* C, int64_t m, int64_t n, int64_t ldc, double beta, cudaStream_t st, int tri) {
     const int64_t tot = m * n;
     if (tot <= 0) return;
-    scale_c_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(C, m, n, ldc, beta, tri);
+    (scale_c_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(C, m, n, ldc, beta, tri), count_launch());
 }
 
 // TRMM operand: T = the uplo triangle of the n x n matrix A (1 = lower, 2 =
@@ -38,7 +38,7 @@ __global__ void tri_copy_kernel(const double* __restrict__ A, int64_t n, int64_t
 void launch_tri_copy(const double* A, int64_t n, int64_t lda, int uplo, int unit, double* T, cudaStream_t st) {
     const int64_t tot = n * n;
     if (tot <= 0) return;
-    tri_copy_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A, n, lda, uplo, unit, T);
+    (tri_copy_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A, n, lda, uplo, unit, T), count_launch());
 }
 
 template <int NM>
@@ -58,7 +58,7 @@ template <int NM>
 static void launch_crt_nm(const int32_t* cprod, int64_t m, int64_t n, const int32_t* e, const int32_t* f,
                           double* C, int64_t ldc, cudaStream_t st) {
     int64_t tot = m * n;
-    crt_kernel<NM><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(cprod, m, n, e, f, C, ldc);
+    (crt_kernel<NM><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(cprod, m, n, e, f, C, ldc), count_launch());
 }
 
 void launch_crt(const int32_t* cprod, int64_t m, int64_t n, const int32_t* e, const int32_t* f,

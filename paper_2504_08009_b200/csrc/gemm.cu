@@ -690,6 +690,7 @@ static int launch_nm(const CUtensorMap* tmA, const CUtensorMap* tmB, const Param
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    count_launch();
     return (int)cudaLaunchKernelEx(&cfg, kern, *tmA, *tmB, p);
 }
 

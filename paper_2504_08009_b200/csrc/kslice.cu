@@ -145,7 +145,7 @@ void launch_kslice_rows(const double* A, int64_t m, int64_t k, int64_t lda, int 
     const size_t smem = row_smem_bytes(k);
     auto kern = mode == 0 ? kslice_rows_kernel<0> : kslice_rows_kernel<1>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)m, 256, smem, st>>>(A, m, k, lda, Eg, E_out, S_out);
+    (kern<<<(unsigned)m, 256, smem, st>>>(A, m, k, lda, Eg, E_out, S_out), count_launch());
 }
 
 void launch_kslice_cols(const double* B, int64_t k, int64_t n, int64_t ldb, int mode, const int32_t* Eg,
@@ -158,25 +158,25 @@ void launch_kslice_cols(const double* B, int64_t k, int64_t n, int64_t ldb, int 
     cudaMemsetAsync(bad, 0, sizeof(int32_t) * n, st);
     if (nch > 0) {
         dim3 grid((unsigned)((n + 31) / 32), (unsigned)nch);
-        if (mode == 0) cols_stats_kernel<0><<<grid, 32 * CS_WARPS, 0, st>>>(B, k, n, ldb, Ec, Sc, bad);
-        else cols_stats_kernel<1><<<grid, 32 * CS_WARPS, 0, st>>>(B, k, n, ldb, Ec, Sc, bad);
+        if (mode == 0) (cols_stats_kernel<0><<<grid, 32 * CS_WARPS, 0, st>>>(B, k, n, ldb, Ec, Sc, bad), count_launch());
+        else (cols_stats_kernel<1><<<grid, 32 * CS_WARPS, 0, st>>>(B, k, n, ldb, Ec, Sc, bad), count_launch());
     }
-    kslice_cols_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, Eg, E_out, S_out);
+    (kslice_cols_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, Eg, E_out, S_out), count_launch());
 }
 
 void launch_exponents_from_stats(const int32_t* E, const unsigned long long* S, int64_t cnt, int N, int mode,
                                  int kstar, int32_t* e, cudaStream_t st) {
     if (cnt <= 0) return;
     const unsigned g = (unsigned)((cnt + 255) / 256);
-    if (mode == 0) exponents_from_stats_kernel<0><<<g, 256, 0, st>>>(E, S, cnt, host_T(N), kstar, e);
-    else exponents_from_stats_kernel<1><<<g, 256, 0, st>>>(E, S, cnt, host_T(N), kstar, e);
+    if (mode == 0) (exponents_from_stats_kernel<0><<<g, 256, 0, st>>>(E, S, cnt, host_T(N), kstar, e), count_launch());
+    else (exponents_from_stats_kernel<1><<<g, 256, 0, st>>>(E, S, cnt, host_T(N), kstar, e), count_launch());
 }
 
 template <int NM>
 static void launch_crt_sum_nm(const uint8_t* R, int G, int64_t part_stride, int64_t m, int64_t n, const int32_t* e,
                               const int32_t* f, double* C, int64_t ldc, cudaStream_t st) {
     dim3 grid((unsigned)((n + 4 * 64 - 1) / (4 * 64)), (unsigned)(m < 65535 ? m : 65535));
-    crt_sum_kernel<NM><<<grid, 64, 0, st>>>(R, G, part_stride, m, n, e, f, C, ldc);
+    (crt_sum_kernel<NM><<<grid, 64, 0, st>>>(R, G, part_stride, m, n, e, f, C, ldc), count_launch());
 }
 
 void launch_crt_sum(const uint8_t* R, int G, int64_t part_stride, int64_t m, int64_t n, const int32_t* e,

@@ -9,12 +9,17 @@
 #define OZ2_EXP_NONFINITE_DEV INT32_MIN
 #define OZ2_EXP_ZERO_DEV (INT32_MIN + 1)     // accu-internal: max exponent of an all-zero row/column
 
-// per-N constants, filled once per device by api.cu (the library is one
-// translation unit, liboz2.cu, so this is the single definition)
-// one copy per translation unit (static): api.cu uploads every TU's copy
+// per-N constants, filled once per device by api.cu; one copy per translation
+// unit (static): api.cu uploads every TU's copy
 static __constant__ Oz2Table c_tab[OZ2_MAX_MODULI + 1];
 
 namespace oz2 {
+
+// kernel launches issued by the library since load (oz2_kernel_launches):
+// every launch site increments it, so a caller can count the library's own
+// kernels in a timed region (bench.py's gpu_launches)
+unsigned long long& launch_counter_ref();
+inline void count_launch() { __atomic_add_fetch(&launch_counter_ref(), 1ull, __ATOMIC_RELAXED); }
 
 // ---------------------------------------------------------------------------
 // binary64 decomposition: x = mant * 2^ex with integer mant (exact), and
@@ -269,6 +274,21 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
     return d;
 }
+// Legacy warp-level INT8 MMA (IMMA.16832.U8.U8): D = A B + C, A 16 x 32 u8
+// (row), B 32 x 8 u8 (col), int32 C / D, fragment layout per the PTX ISA
+// (groupID g = lane / 4, t = lane % 4): a0 = A[g][4t..4t+3], a1 = A[g+8][4t..],
+// a2 = A[g][16+4t..], a3 = A[g+8][16+4t..]; b0 = B[4t..4t+3][g], b1 =
+// B[16+4t..][g]; c0, c1 = C[g][2t, 2t+1], c2, c3 = C[g+8][2t, 2t+1].
+// Used for the residue byte dot products (scale.cu), not for the GEMM.
+__device__ __forceinline__ void imma_u8(uint32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                        uint32_t b0, uint32_t b1, uint32_t c0, uint32_t c1, uint32_t c2,
+                                        uint32_t c3) {
+    asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%11,%12,%13};"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(c0), "r"(c1), "r"(c2), "r"(c3));
+}
+
 // low bytes of four 32-bit values -> one word (byte i from v_i)
 __device__ __forceinline__ uint32_t pack_lo_bytes(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3) {
     uint32_t a = prmt(v0, v1, 0x0040u);

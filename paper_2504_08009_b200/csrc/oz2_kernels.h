@@ -23,10 +23,14 @@ int host_T(int N);   // floor(L/2) for N moduli (host copy of the table)
 int host_L(int N);   // floor(log2(M/2 - 1))
 
 // scale.cu -- Alg. 1 lines 1-5
+void launch_init_bfrag(cudaStream_t st);   // once per device after the tables: the residue MMAs' B fragments
 // what: 1 = exponents e, 2 = residues (given e), 3 = both (one pass per row)
 // pstride: bytes between residue planes (default m * ldr)
+// xbits: a bound |trunc(2^e a)| < 2^xbits of the line-1 rule in use (selects the
+// residue kernels' integer width; 64 = the widest for N, always valid)
 void launch_rows(const double* A, int64_t m, int64_t k, int64_t lda, int N, int what, int mode,
-                 int kstar, int32_t* e, int8_t* res, int64_t ldr, cudaStream_t st, int64_t pstride = 0);
+                 int kstar, int32_t* e, int8_t* res, int64_t ldr, cudaStream_t st, int64_t pstride = 0,
+                 int xbits = 64);
 void launch_trunc_rows(const double* A, int64_t m, int64_t k, int64_t lda, const int32_t* e,
                        double* out, cudaStream_t st);
 size_t cols_stats_bytes(int64_t k, int64_t n);
@@ -34,7 +38,7 @@ void launch_cols_exponents(const double* B, int64_t k, int64_t n, int64_t ldb, i
                            int kstar, int32_t* f, void* scratch, cudaStream_t st);
 // pstride: bytes between residue planes (default n * ldr)
 void launch_cols_residues(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f, int N,
-                          int8_t* res, int64_t ldr, cudaStream_t st, int64_t pstride = 0);
+                          int8_t* res, int64_t ldr, cudaStream_t st, int64_t pstride = 0, int xbits = 64);
 void launch_trunc_cols(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
                        double* out, cudaStream_t st);
 
@@ -88,10 +92,18 @@ int launch_modmul_residues(const CUtensorMap* tmA, const CUtensorMap* tmB, int64
                            cudaStream_t st);
 
 // certify.cu -- condition (13) certificate for caller-supplied exponents
-// dmax2: two device ints (scratch); stats_scratch: cols_stats_bytes(k, n)
+// dmax4: five device ints (scratch); stats_scratch: cols_stats_bytes(k, n);
+// ab (or NULL): the OS II-accu line-1 bound of the same product (E, F, row /
+// column maxima of P), giving the second, often tighter, bound
+struct AccuBound {
+    const int32_t* E;
+    const int32_t* F;
+    const uint32_t* rowmax;
+    const uint32_t* colmax;
+};
 void launch_certify(const double* A, int64_t m, int64_t k, int64_t lda, const double* B, int64_t n, int64_t ldb,
-                    const int32_t* e, const int32_t* f, int N, int* dmax2, void* stats_scratch, int32_t* beta,
-                    cudaStream_t st);
+                    const int32_t* e, const int32_t* f, int N, int* dmax4, void* stats_scratch, int32_t* beta,
+                    const AccuBound* ab, cudaStream_t st);
 // beta > L: C := NaN and atomicOr(status, 1)
 void launch_refuse(const int32_t* beta, int N, double* C, int64_t m, int64_t n, int64_t ldc, int* status,
                    cudaStream_t st);

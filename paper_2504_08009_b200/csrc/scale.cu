@@ -69,6 +69,139 @@ __device__ __forceinline__ uint32_t residue_odd(int t, const uint32_t (&w)[3]) {
     return q * T.negm[t] + y;                                   // y - q m_t (mod 2^32)
 }
 
+// ---------------------------------------------------------------------------
+// The same residues with the byte dot products on the (otherwise idle) tensor
+// cores: one legacy warp-level IMMA (m16n8k32, u8 x u8 -> s32) computes, for 64
+// elements of a warp (2 per thread) and 2 moduli, y = G_t + sum_b byte_b(U)
+// c_(t,b).  Fragment mapping (imma_u8): thread (g, tq) puts its element E0's
+// words into A row g and E1's into row g + 8, at K slot tq (bytes 0-3 at K =
+// 4 tq.., bytes 4-7 at K = 16 + 4 tq..) -- exactly the a0..a3 registers, no
+// data movement.  Column n = 2 slot + mm of B holds c_(t_mm, b) at the K
+// positions of `slot` and 0 elsewhere, so C[g][2 tq + mm] is y of this
+// thread's own element and modulus t_mm: the accumulator fragment c0..c3 holds
+// (E0, t0), (E0, t1), (E1, t0), (E1, t1).  C (the bias G_t) enters as the MMA's
+// addend.  96-bit inputs (N > 16) chain a second IMMA over bytes 8-11.
+// One IMMA replaces 4 dp4a per thread (8 for 96-bit); the symmetric reduction
+// and the byte packing stay on the integer pipes.
+// ---------------------------------------------------------------------------
+constexpr int MAX_PAIRS = OZ2_MAX_MODULI / 2;
+
+// Integer widths of the residue inputs x = trunc(2^e a) (the launcher picks the
+// narrowest that holds the line-1 rule's bound on |x|):
+//   BW_7:  |x| < 2^55: U = x + 2^55 in bytes 0-6, byte 7 := 1, and B carries the
+//          bias correction (-2^55 mod m_t) at byte 7 -- the MMA's addend is 0, so
+//          no accumulator set-up per MMA (FAST / EQ17 with N <= 14: T <= 54);
+//   BW_8:  |x| < 2^63: U = x + 2^63, the correction G63_t as the MMA's addend;
+//   BW_12: |x| < 2^95: U = x + 2^95 in 12 bytes (two chained MMAs), G95_t.
+constexpr int BW_7 = 7, BW_8 = 8, BW_12 = 12;
+template <int BW> struct BwWords { static constexpr int value = BW == BW_12 ? 3 : 2; };
+
+// B fragments of every (N, width class, modulus pair (t0, t1) = (1 + 2p, 2 + 2p),
+// lane): the same for every warp and CTA, built once per device by
+// init_bfrag_kernel (api.cu, after the tables) and read with one cached 8- or
+// 12-byte load per pair and lane
+static __device__ uint32_t g_bfrag[OZ2_MAX_MODULI + 1][2][MAX_PAIRS][32][3];
+
+__device__ __forceinline__ uint32_t pow2_mod(int e, uint32_t m) {
+    uint32_t r = 1 % m;
+    for (int i = 0; i < e; i++) r = (r * 2u) % m;
+    return r;
+}
+
+__global__ void init_bfrag_kernel() {
+    const int NM = blockIdx.x, b7 = blockIdx.y;
+    if (NM < 2) return;
+    const Oz2Table& T = c_tab[NM];
+    for (int x = threadIdx.x; x < (NM / 2) * 32; x += blockDim.x) {
+        const int p = x >> 5, l = x & 31, g = l >> 2, tq = l & 3;
+        const int t = 1 + 2 * p + (g & 1);
+        const bool sel = tq == (g >> 1) && t < NM;
+        uint32_t v[3] = {0u, 0u, 0u};
+        if (sel) {
+            for (int w = 0; w < 3; w++) v[w] = T.cw[w][t];
+            if (b7) {                                      // BW_7: byte 7 of U is 1, its weight is the bias term
+                const uint32_t m = (uint32_t)T.m[t];
+                const uint32_t g55 = (m - pow2_mod(55, m)) % m;
+                v[1] = (v[1] & 0x00ffffffu) | (g55 << 24);
+            }
+        }
+        for (int w = 0; w < 3; w++) g_bfrag[NM][b7][p][l][w] = v[w];
+    }
+}
+
+void launch_init_bfrag(cudaStream_t st) {
+    (init_bfrag_kernel<<<dim3(OZ2_MAX_MODULI + 1, 2), 128, 0, st>>>(), count_launch());
+}
+
+template <int NM>
+__device__ __forceinline__ uint32_t sym_residue(uint32_t y, int t) {
+    const Oz2Table& T = c_tab[NM];
+    const uint32_t q = (uint32_t)(((uint64_t)y * T.magic[t] + T.hmagic[t]) >> 32);
+    return q * T.negm[t] + y;                                   // y - q m_t (mod 2^32)
+}
+
+// The IMMA A operand of element pair (E0, E1) as one register quad, in the
+// fragment order {bytes 0-3 of E0, of E1, bytes 4-7 of E0, of E1} (plus, for
+// 12-byte inputs, {bytes 8-11 of E0, of E1, 0, 0}): built once by to_quad and
+// reused by every modulus pair.
+template <int BW>
+struct EQuad {
+    uint32_t a[4];
+    uint32_t b[4];          // BW_12 only
+};
+
+// residues for t = 1..NM-1 of the 2 * NQ elements held as quads q[0..NQ) (NQ
+// even); store(t, pw[NQ/2]) receives the int8 residues of modulus t packed 4 per
+// word in element order (element 2i, 2i+1 of quad i).  Every lane of the warp
+// must call it (mma.sync).  Loop order: for each group of 4 elements (2 quads)
+// all modulus pairs back to back, so each A quad feeds its NM/2 MMAs in a row
+// and stays in its registers (the other order made ptxas copy the quads into
+// fresh registers before every MMA).
+template <int NM, int BW, int NQ, typename Store>
+__device__ __forceinline__ void residues_imma(const EQuad<BW> (&q)[NQ], Store&& store) {
+    static_assert(NQ % 2 == 0, "4 elements per packed word");
+    constexpr int NP = NM / 2;
+    const Oz2Table& T = c_tab[NM];
+    const int lane = threadIdx.x & 31;
+    const uint32_t* bf = &g_bfrag[NM][BW == BW_7 ? 1 : 0][0][lane][0];
+    uint32_t pw[NM][NQ / 2];                           // pw[t][u]: modulus t, elements 4u..4u+3
+    #pragma unroll
+    for (int u = 0; u < NQ / 2; u++) {
+        #pragma unroll
+        for (int p = 0; p < NP; p++) {
+            const int t0 = 1 + 2 * p, t1 = t0 + 1;
+            const bool two = t1 < NM;
+            const uint32_t b0 = __ldg(bf + p * 96), b1 = __ldg(bf + p * 96 + 1);
+            const uint32_t b2 = BW == BW_12 ? __ldg(bf + p * 96 + 2) : 0u;
+            const uint32_t g0 = BW == BW_7 ? 0u : (BW == BW_8 ? T.G63[t0] : T.G95[t0]);
+            const uint32_t g1 = BW == BW_7 || !two ? 0u : (BW == BW_8 ? T.G63[t1] : T.G95[t1]);
+            uint32_t r0[4], r1[4];
+            #pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const EQuad<BW>& e = q[2 * u + h];
+                uint32_t d[4];
+                imma_u8(d, e.a[0], e.a[1], e.a[2], e.a[3], b0, b1, g0, g1, g0, g1);
+                if (BW == BW_12) {
+                    uint32_t d2[4];
+                    imma_u8(d2, e.b[0], e.b[1], e.b[2], e.b[3], b2, 0u, d[0], d[1], d[2], d[3]);
+                    #pragma unroll
+                    for (int x = 0; x < 4; x++) d[x] = d2[x];
+                }
+                r0[2 * h] = sym_residue<NM>(d[0], t0);
+                r0[2 * h + 1] = sym_residue<NM>(d[2], t0);
+                if (two) {
+                    r1[2 * h] = sym_residue<NM>(d[1], t1);
+                    r1[2 * h + 1] = sym_residue<NM>(d[3], t1);
+                }
+            }
+            pw[t0][u] = pack_lo_bytes(r0[0], r0[1], r0[2], r0[3]);
+            if (two) pw[t1][u] = pack_lo_bytes(r1[0], r1[1], r1[2], r1[3]);
+        }
+    }
+    #pragma unroll
+    for (int t = 1; t < NM; t++) store(t, pw[t]);
+}
+
 // 2^e as the product s1 * s2 of two doubles (the two multiplications of
 // scale_pow2, hoisted out of the per-element loops: x s1 s2 is bitwise
 // scale_pow2(x, e) for every finite x)
@@ -106,6 +239,26 @@ __device__ __forceinline__ void to_words(double a, double s1, double s2, uint32_
     }
 }
 
+// elements a0, a1 -> their IMMA quad (BW_8 / BW_12: the words of to_words;
+// BW_7: U = x + 2^55 with byte 7 set to 1, x in [-2^55, 2^55))
+template <int BW>
+__device__ __forceinline__ void to_quad(double a0, double a1, double s1, double s2, EQuad<BW>& q) {
+    if (BW == BW_7) {
+        const long long x0 = __double2ll_rz((a0 * s1) * s2), x1 = __double2ll_rz((a1 * s1) * s2);
+        q.a[0] = (uint32_t)x0;
+        q.a[1] = (uint32_t)x1;
+        q.a[2] = (uint32_t)((unsigned long long)x0 >> 32) + 0x01800000u;   // + 2^23 (the bias), byte 7 := 1
+        q.a[3] = (uint32_t)((unsigned long long)x1 >> 32) + 0x01800000u;
+        return;
+    }
+    constexpr int W = BwWords<BW>::value;
+    uint32_t w0[3], w1[3];
+    to_words<W>(a0, s1, s2, w0);
+    to_words<W>(a1, s1, s2, w1);
+    q.a[0] = w0[0]; q.a[1] = w1[0]; q.a[2] = w0[1]; q.a[3] = w1[1];
+    if (BW == BW_12) { q.b[0] = w0[2]; q.b[1] = w1[2]; q.b[2] = 0u; q.b[3] = 0u; }
+}
+
 // ---------------------------------------------------------------------------
 // memory helpers: L2 eviction-priority policies, streaming stores
 // ---------------------------------------------------------------------------
@@ -131,6 +284,19 @@ __device__ __forceinline__ double ld1_hint(const double* a, uint64_t pol) {
 }
 __device__ __forceinline__ void st_cs_v2(void* a, uint32_t x, uint32_t y) {
     asm volatile("st.global.cs.v2.b32 [%0], {%1, %2};" :: "l"(a), "r"(x), "r"(y) : "memory");
+}
+// predicated forms (no branch around the store)
+__device__ __forceinline__ void st_cs_b32_if(bool p, void* a, uint32_t x) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.cs.b32 [%0], %1;\n\t}"
+                 :: "l"(a), "r"(x), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void st_cs_v2_if(bool p, void* a, uint32_t x, uint32_t y) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q st.global.cs.v2.b32 [%0], {%1, %2};\n\t}"
+                 :: "l"(a), "r"(x), "r"(y), "r"((int)p) : "memory");
+}
+__device__ __forceinline__ void st_cs_v4_if(bool p, void* a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};\n\t}"
+                 :: "l"(a), "r"(x), "r"(y), "r"(z), "r"(w), "r"((int)p) : "memory");
 }
 __device__ __forceinline__ void st_cs_v4(void* a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
     asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" :: "l"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
@@ -377,14 +543,136 @@ __device__ void row_residues(const double* __restrict__ X, int64_t k, int e, int
     }
 }
 
+#ifndef OZ2_RES_IMMA
+// 1: the byte dot products of the 7-byte width on the legacy IMMA path.  Measured
+// (round 2, tools/gpu/ab_conv.sh, 16384^2, N = 14): bitwise-correct, rows equal
+// to dp4a (1.87 vs 1.87-1.90 ms, 93 instructions per element either way: the
+// dp4a savings go to register moves that ptxas inserts around every MMA), the
+// column kernel slower (2.03 vs 1.73 ms: 80 registers, lower occupancy on a
+// latency-bound kernel).  Default 0 (dp4a); kept as a build option.
+#define OZ2_RES_IMMA 0
+#endif
+// the byte dot products on the IMMA path for the 7-byte width (the headline N
+// <= 14 with FAST / EQ17 exponents), dp4a otherwise (OZ2_RES_IMMA=0: always dp4a)
+template <int BW>
+struct UseImma { static constexpr bool value = OZ2_RES_IMMA && BW == BW_7; };
+
+// residues of RPT elements a[] of this thread (scale 2^e = s1 s2) for all NM
+// moduli; put(t, pw[RPT/4]) receives modulus t's bytes packed 4 per word.  On
+// the IMMA path every lane of the warp must call it.
+template <int NM, int BW, int RPT, typename Put>
+__device__ __forceinline__ void thread_residues(const double (&a)[RPT], double s1, double s2, Put&& put) {
+    if constexpr (UseImma<BW>::value) {
+        EQuad<BW> eq[RPT / 2];
+        #pragma unroll
+        for (int q = 0; q < RPT / 2; q++) to_quad<BW>(a[2 * q], a[2 * q + 1], s1, s2, eq[q]);
+        uint32_t pw[RPT / 4];                                     // t = 0: m = 256, the low byte
+        #pragma unroll
+        for (int u = 0; u < RPT / 4; u++)
+            pw[u] = pack_lo_bytes(eq[2 * u].a[0], eq[2 * u].a[1], eq[2 * u + 1].a[0], eq[2 * u + 1].a[1]);
+        put(0, pw);
+        residues_imma<NM, BW, RPT / 2>(eq, put);
+    } else {
+        constexpr int WORDS = BwWords<BW>::value;
+        uint32_t w[RPT][3];
+        #pragma unroll
+        for (int q = 0; q < RPT; q++) to_words<WORDS>(a[q], s1, s2, w[q]);
+        {
+            uint32_t pw[RPT / 4];                                 // t = 0: m = 256, the low byte
+            #pragma unroll
+            for (int u = 0; u < RPT / 4; u++)
+                pw[u] = pack_lo_bytes(w[4 * u][0], w[4 * u + 1][0], w[4 * u + 2][0], w[4 * u + 3][0]);
+            put(0, pw);
+        }
+        #pragma unroll
+        for (int t = 1; t < NM; t++) {
+            uint32_t pw[RPT / 4];
+            #pragma unroll
+            for (int u = 0; u < RPT / 4; u++)
+                pw[u] = pack_lo_bytes(residue_odd<NM, WORDS>(t, w[4 * u]), residue_odd<NM, WORDS>(t, w[4 * u + 1]),
+                                      residue_odd<NM, WORDS>(t, w[4 * u + 2]), residue_odd<NM, WORDS>(t, w[4 * u + 3]));
+            put(t, pw);
+        }
+    }
+}
+
+// row_residues with the IMMA byte dots: the same output; RVI elements per thread
+// and step; the loop runs while any lane of the warp has elements left (mma.sync
+// needs the whole warp), lanes past the row convert zeros and do not store
+#ifndef OZ2_ROW_RVI
+#define OZ2_ROW_RVI 8
+#endif
+template <int NM, int BW>
+__device__ void row_residues_imma(const double* __restrict__ X, int64_t k, int e, int8_t* __restrict__ out,
+                                  int64_t plane_stride) {
+    constexpr int RVI = OZ2_ROW_RVI;
+    static_assert(RVI == 4 || RVI == 8 || RVI == 16, "4, 8 or 16 elements per thread");
+    const bool vec = ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+    const uint64_t pol = l2_evict_first();
+    const int64_t step = RVI * (int64_t)blockDim.x;
+    const int64_t warp0 = RVI * (int64_t)(threadIdx.x & ~31);
+    const int64_t ldr = (k + 15) & ~(int64_t)15;
+    if (e == OZ2_EXP_NONFINITE_DEV) {                 // x = 0: every residue is 0
+        for (int64_t l0 = RV * (int64_t)threadIdx.x; l0 < k; l0 += RV * (int64_t)blockDim.x)
+            #pragma unroll 1
+            for (int t = 0; t < NM; t++) st_cs_v4(out + t * plane_stride + l0, 0u, 0u, 0u, 0u);
+        return;
+    }
+    double s1, s2;
+    pow2_factors(e, s1, s2);
+    #pragma unroll 1
+    for (int64_t base = warp0; base < k; base += step) {
+        const int64_t l0 = base + RVI * (int64_t)(threadIdx.x & 31);
+        double a[RVI];
+        if (vec && l0 + RVI <= k) {
+            #pragma unroll
+            for (int j = 0; j < RVI / 2; j++) {
+                const double2 p = ld2_hint(X + l0 + 2 * j, pol);
+                a[2 * j] = p.x; a[2 * j + 1] = p.y;
+            }
+        } else {
+            #pragma unroll
+            for (int j = 0; j < RVI; j++) a[j] = (l0 + j < k) ? ld1_hint(X + l0 + j, pol) : 0.0;
+        }
+        EQuad<BW> q[RVI / 2];
+        if (s2 == 1.0) {                              // block-uniform (one exponent per row)
+            #pragma unroll
+            for (int j = 0; j < RVI / 2; j++) to_quad<BW>(a[2 * j], a[2 * j + 1], s1, 1.0, q[j]);
+        } else {
+            #pragma unroll
+            for (int j = 0; j < RVI / 2; j++) to_quad<BW>(a[2 * j], a[2 * j + 1], s1, s2, q[j]);
+        }
+        const bool live = l0 < ldr;                   // l0 is a multiple of RVI: whole pieces
+        int8_t* o = out + l0;                          // walks the planes: t = 0, 1, 2, ... in order
+        auto put = [&](int t, const uint32_t (&pw)[RVI / 4]) {
+            if (t) o += plane_stride;
+            if constexpr (RVI == 16) st_cs_v4_if(live, o, pw[0], pw[1], pw[2], pw[3]);
+            else if constexpr (RVI == 8) st_cs_v2_if(live, o, pw[0], pw[1]);
+            else st_cs_b32_if(live, o, pw[0]);
+        };
+        {                                              // t = 0: m = 256, the low byte of x
+            uint32_t pw[RVI / 4];
+            #pragma unroll
+            for (int u = 0; u < RVI / 4; u++)
+                pw[u] = pack_lo_bytes(q[2 * u].a[0], q[2 * u].a[1], q[2 * u + 1].a[0], q[2 * u + 1].a[1]);
+            put(0, pw);
+        }
+        residues_imma<NM, BW, RVI / 2>(q, put);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Row kernels (A: m x k, row-major, lda); one CTA per row
 // ---------------------------------------------------------------------------
 // what: 1 = exponents, 2 = residues (given e), 3 = both
-template <int NM, int WORDS, int MODE, int THREADS>
-__global__ void __launch_bounds__(THREADS)
+#ifndef OZ2_ROW_MINB
+#define OZ2_ROW_MINB 3          // resident 256-thread row CTAs per SM the register budget allows
+#endif
+template <int NM, int BW, int MODE, int THREADS>
+__global__ void __launch_bounds__(THREADS, THREADS == 256 ? OZ2_ROW_MINB : 1)
 rows_kernel(const double* __restrict__ A, int64_t m, int64_t k, int64_t lda, int what, int kstar,
             int32_t* __restrict__ e_io, int8_t* __restrict__ res, int64_t ldr, int64_t pstride) {
+    constexpr int WORDS = BwWords<BW>::value;
     extern __shared__ __align__(16) unsigned char row_smem[];
     const int64_t nch = (k + KC - 1) / KC;
     RowSmem sm;
@@ -402,7 +690,11 @@ rows_kernel(const double* __restrict__ A, int64_t m, int64_t k, int64_t lda, int
         } else {
             e = e_io[i];
         }
-        if (what & 2) row_residues<NM, WORDS>(X, k, e, res + i * ldr, pstride);
+        if constexpr (UseImma<BW>::value) {
+            if (what & 2) row_residues_imma<NM, BW>(X, k, e, res + i * ldr, pstride);
+        } else {
+            if (what & 2) row_residues<NM, WORDS>(X, k, e, res + i * ldr, pstride);
+        }
     }
 }
 
@@ -544,10 +836,13 @@ __global__ void cols_finalize_kernel(const int32_t* __restrict__ Ec, const unsig
 // chunks XOR-swizzled by (col & 7): conflict-free), then every 128-byte plane
 // row segment is written by 8 consecutive threads with 16-byte stores (full
 // sectors, no partial-sector read-modify-write in L2).
-template <int NM, int WORDS, int CR_ROWS>
-__global__ void __launch_bounds__(256)
+// resident CTAs per SM the register budget allows: the kernel is latency-bound
+// on its loads, so occupancy matters (4 CTAs = 64 registers; N > 14 needs 80)
+template <int NM, int BW, int CR_ROWS>
+__global__ void __launch_bounds__(256, UseImma<BW>::value ? 4 : 1)
 cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t ldb,
                      const int32_t* __restrict__ f, int8_t* __restrict__ out, int64_t ldr, int64_t pstride) {
+    constexpr int WORDS = BwWords<BW>::value;
     constexpr int CR_RPT = CR_ROWS / 8;             // rows per thread (8 warps)
     constexpr int NPC = CR_ROWS / 16;               // 16-byte pieces per (t, col) segment
     extern __shared__ __align__(16) uint8_t sres[];
@@ -571,31 +866,18 @@ cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t
             #pragma unroll
             for (int q = 0; q < CR_RPT; q++) a[q] = (live && lw + q < k) ? ld1_hint(src + q * ldb, pol) : 0.0;
         }
-        uint32_t w[CR_RPT][3];
-        if (__all_sync(0xffffffffu, s2 == 1.0)) {           // one multiplication (normal scales)
-            #pragma unroll
-            for (int q = 0; q < CR_RPT; q++) to_words<WORDS>(a[q], s1, 1.0, w[q]);
-        } else {
-            #pragma unroll
-            for (int q = 0; q < CR_RPT; q++) to_words<WORDS>(a[q], s1, s2, w[q]);
-        }
         // 16-byte chunks XOR-swizzled within the segment (conflict-free stores and loads)
-        #pragma unroll
-        for (int t = 0; t < NM; t++) {
-            uint32_t r[CR_RPT];
-            #pragma unroll
-            for (int q = 0; q < CR_RPT; q++) r[q] = t == 0 ? w[q][0] : residue_odd<NM, WORDS>(t, w[q]);
+        auto put = [&](int t, const uint32_t (&pw)[CR_RPT / 4]) {
             uint8_t* seg = sres + (size_t)(t * 32 + lane) * CR_ROWS;
             if constexpr (CR_RPT == 16) {
-                *reinterpret_cast<uint4*>(seg + ((warp ^ (lane & 7)) * 16)) =
-                    make_uint4(pack_lo_bytes(r[0], r[1], r[2], r[3]), pack_lo_bytes(r[4], r[5], r[6], r[7]),
-                               pack_lo_bytes(r[8], r[9], r[10], r[11]), pack_lo_bytes(r[12], r[13], r[14], r[15]));
+                *reinterpret_cast<uint4*>(seg + ((warp ^ (lane & 7)) * 16)) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
             } else {                                   // 8 bytes: half of piece (warp >> 1)
                 const int pc = (warp >> 1) ^ (lane & 3);
-                *reinterpret_cast<uint2*>(seg + pc * 16 + (warp & 1) * 8) =
-                    make_uint2(pack_lo_bytes(r[0], r[1], r[2], r[3]), pack_lo_bytes(r[4], r[5], r[6], r[7]));
+                *reinterpret_cast<uint2*>(seg + pc * 16 + (warp & 1) * 8) = make_uint2(pw[0], pw[1]);
             }
-        }
+        };
+        const bool one = __all_sync(0xffffffffu, s2 == 1.0);    // one multiplication (normal scales)
+        thread_residues<NM, BW, CR_RPT>(a, s1, one ? 1.0 : s2, put);
     }
     __syncthreads();
     // write out: NPC threads per (t, col) row segment of CR_ROWS bytes, 16 bytes
@@ -629,11 +911,16 @@ __global__ void trunc_cols_kernel(const double* __restrict__ B, int64_t k, int64
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
+// The residue kernels' integer width for N moduli and a bound |x| < 2^xbits on
+// the scaled integers (xbits = T + 1 for FAST, k* for EQ17, 62 / 94 otherwise)
 template <int NM>
-static void launch_rows_nm(const double* A, int64_t m, int64_t k, int64_t lda, int what, int mode,
+constexpr int pick_bw(int xbits) {
+    return OZ2_RES_IMMA && NM <= 14 && xbits <= 55 ? BW_7 : (NM <= 16 ? BW_8 : BW_12);
+}
+
+template <int NM, int BW>
+static void launch_rows_bw(const double* A, int64_t m, int64_t k, int64_t lda, int what, int mode,
                            int kstar, int32_t* e, int8_t* res, int64_t ldr, int64_t pstride, cudaStream_t st) {
-    constexpr int W = NM <= 16 ? 2 : 3;
-    static const int threads = [] { const char* v = getenv("OZ2_ROW_THREADS"); return v && atoi(v) == 512 ? 512 : 256; }();
     // OZ2_ROW_CTAS_PER_SM = R > 0: a persistent grid of R CTAs per SM (rows in
     // flight R * SMs, each 8k bytes, sized against the L2); 0: one CTA per row
     static const int per_sm = [] { const char* v = getenv("OZ2_ROW_CTAS_PER_SM"); return v && *v ? atoi(v) : 0; }();
@@ -644,37 +931,48 @@ static void launch_rows_nm(const double* A, int64_t m, int64_t k, int64_t lda, i
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         g = std::min<int64_t>(m, (int64_t)sms * per_sm);
     }
-    dim3 grid((unsigned)g), block((unsigned)threads);
+    dim3 grid((unsigned)g), block(256);
     const size_t smem = row_smem_bytes(k);
-    auto kern = threads == 512 ? (mode == 0 ? rows_kernel<NM, W, 0, 512> : rows_kernel<NM, W, 1, 512>)
-                               : (mode == 0 ? rows_kernel<NM, W, 0, 256> : rows_kernel<NM, W, 1, 256>);
+    auto kern = mode == 0 ? rows_kernel<NM, BW, 0, 256> : rows_kernel<NM, BW, 1, 256>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, block, smem, st>>>(A, m, k, lda, what, kstar, e, res, ldr, pstride);
+    (kern<<<grid, block, smem, st>>>(A, m, k, lda, what, kstar, e, res, ldr, pstride), count_launch());
 }
 
-template <int NM, int ROWS>
-static void launch_cols_res_rows(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
-                                 int8_t* res, int64_t ldr, int64_t pstride, cudaStream_t st) {
+template <int NM>
+static void launch_rows_nm(const double* A, int64_t m, int64_t k, int64_t lda, int what, int mode,
+                           int kstar, int32_t* e, int8_t* res, int64_t ldr, int64_t pstride, cudaStream_t st,
+                           int xbits) {
+    // exponents only: any width (no residues are formed)
+    const int bw = (what & 2) ? pick_bw<NM>(xbits) : pick_bw<NM>(64);
+    if constexpr (NM <= 14 && OZ2_RES_IMMA) {
+        if (bw == BW_7) return launch_rows_bw<NM, BW_7>(A, m, k, lda, what, mode, kstar, e, res, ldr, pstride, st);
+    }
+    launch_rows_bw<NM, pick_bw<NM>(64)>(A, m, k, lda, what, mode, kstar, e, res, ldr, pstride, st);
+}
+
+template <int NM, int BW>
+static void launch_cols_res_bw(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
+                               int8_t* res, int64_t ldr, int64_t pstride, cudaStream_t st) {
+    constexpr int ROWS = 64;
     dim3 grid((unsigned)((n + 31) / 32), (unsigned)((k + ROWS - 1) / ROWS)), block(256);
-    constexpr int W = NM <= 16 ? 2 : 3;
     const size_t smem = (size_t)NM * 32 * ROWS;
     static bool attr_done[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 64 && !attr_done[dev]) {
-        cudaFuncSetAttribute(cols_residues_kernel<NM, W, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(cols_residues_kernel<NM, BW, ROWS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_done[dev] = true;
     }
-    cols_residues_kernel<NM, W, ROWS><<<grid, block, smem, st>>>(B, k, n, ldb, f, res, ldr, pstride);
+    (cols_residues_kernel<NM, BW, ROWS><<<grid, block, smem, st>>>(B, k, n, ldb, f, res, ldr, pstride), count_launch());
 }
 
-// rows of B per CTA: 64 (8 per thread) or 128 (16 per thread; OZ2_CR_ROWS=128)
 template <int NM>
 static void launch_cols_res_nm(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
-                               int8_t* res, int64_t ldr, int64_t pstride, cudaStream_t st) {
-    static const int rows = [] { const char* v = getenv("OZ2_CR_ROWS"); return v && atoi(v) == 128 ? 128 : 64; }();
-    if (rows == 128) launch_cols_res_rows<NM, 128>(B, k, n, ldb, f, res, ldr, pstride, st);
-    else launch_cols_res_rows<NM, 64>(B, k, n, ldb, f, res, ldr, pstride, st);
+                               int8_t* res, int64_t ldr, int64_t pstride, cudaStream_t st, int xbits) {
+    if constexpr (NM <= 14 && OZ2_RES_IMMA) {
+        if (pick_bw<NM>(xbits) == BW_7) return launch_cols_res_bw<NM, BW_7>(B, k, n, ldb, f, res, ldr, pstride, st);
+    }
+    launch_cols_res_bw<NM, pick_bw<NM>(64)>(B, k, n, ldb, f, res, ldr, pstride, st);
 }
 
 #define OZ2_DISPATCH_N(N, FN, ...)                                                   \
@@ -692,17 +990,17 @@ static void launch_cols_res_nm(const double* B, int64_t k, int64_t n, int64_t ld
     }
 
 void launch_rows(const double* A, int64_t m, int64_t k, int64_t lda, int N, int what, int mode,
-                 int kstar, int32_t* e, int8_t* res, int64_t ldr, cudaStream_t st, int64_t pstride) {
+                 int kstar, int32_t* e, int8_t* res, int64_t ldr, cudaStream_t st, int64_t pstride, int xbits) {
     if (m == 0) return;
     if (pstride <= 0) pstride = m * ldr;
-    OZ2_DISPATCH_N(N, launch_rows_nm, A, m, k, lda, what, mode, kstar, e, res, ldr, pstride, st);
+    OZ2_DISPATCH_N(N, launch_rows_nm, A, m, k, lda, what, mode, kstar, e, res, ldr, pstride, st, xbits);
 }
 
 void launch_trunc_rows(const double* A, int64_t m, int64_t k, int64_t lda, const int32_t* e,
                        double* out, cudaStream_t st) {
     int64_t tot = m * k;
     if (!tot) return;
-    trunc_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A, m, k, lda, e, out);
+    (trunc_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(A, m, k, lda, e, out), count_launch());
 }
 
 size_t cols_stats_bytes(int64_t k, int64_t n) {
@@ -723,26 +1021,26 @@ void launch_cols_exponents(const double* B, int64_t k, int64_t n, int64_t ldb, i
     int32_t* bad = Ec + nch * n;
     cudaMemsetAsync(bad, 0, sizeof(int32_t) * n, st);
     dim3 grid((unsigned)((n + 31) / 32), (unsigned)nch);
-    if (mode == 0) cols_stats_kernel<0><<<grid, 32 * CS_WARPS, 0, st>>>(B, k, n, ldb, Ec, Sc, bad);
-    else cols_stats_kernel<1><<<grid, 32 * CS_WARPS, 0, st>>>(B, k, n, ldb, Ec, Sc, bad);
+    if (mode == 0) (cols_stats_kernel<0><<<grid, 32 * CS_WARPS, 0, st>>>(B, k, n, ldb, Ec, Sc, bad), count_launch());
+    else (cols_stats_kernel<1><<<grid, 32 * CS_WARPS, 0, st>>>(B, k, n, ldb, Ec, Sc, bad), count_launch());
     unsigned g2 = (unsigned)((n + 255) / 256);
-    if (mode == 0) cols_finalize_kernel<0><<<g2, 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, host_T(N), kstar, f);
-    else if (mode == 1) cols_finalize_kernel<1><<<g2, 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, host_T(N), kstar, f);
-    else cols_finalize_kernel<2><<<g2, 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, host_T(N), kstar, f);
+    if (mode == 0) (cols_finalize_kernel<0><<<g2, 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, host_T(N), kstar, f), count_launch());
+    else if (mode == 1) (cols_finalize_kernel<1><<<g2, 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, host_T(N), kstar, f), count_launch());
+    else (cols_finalize_kernel<2><<<g2, 256, 0, st>>>(Ec, Sc, bad, n, (int)nch, host_T(N), kstar, f), count_launch());
 }
 
 void launch_cols_residues(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f, int N,
-                          int8_t* res, int64_t ldr, cudaStream_t st, int64_t pstride) {
+                          int8_t* res, int64_t ldr, cudaStream_t st, int64_t pstride, int xbits) {
     if (n == 0 || k == 0) return;
     if (pstride <= 0) pstride = n * ldr;
-    OZ2_DISPATCH_N(N, launch_cols_res_nm, B, k, n, ldb, f, res, ldr, pstride, st);
+    OZ2_DISPATCH_N(N, launch_cols_res_nm, B, k, n, ldb, f, res, ldr, pstride, st, xbits);
 }
 
 void launch_trunc_cols(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
                        double* out, cudaStream_t st) {
     int64_t tot = k * n;
     if (!tot) return;
-    trunc_cols_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(B, k, n, ldb, f, out);
+    (trunc_cols_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(B, k, n, ldb, f, out), count_launch());
 }
 
 }  // namespace oz2

@@ -35,7 +35,7 @@ SYMBOLS = [
     "oz2_scale_accu", "oz2_dgemm_scaled", "oz2_prepare_a", "oz2_prepare_b", "oz2_dgemm_prepared",
     "oz2_dgemm_prep2", "oz2_release", "oz2_certify", "oz2_set_certify", "oz2_status",
     "oz2_set_sm_limit", "oz2_kslice_stats_rows", "oz2_kslice_stats_cols", "oz2_exponents_from_stats",
-    "oz2_modmul_residues", "oz2_crt_sum", "oz2_dsyrk", "oz2_dtrmm",
+    "oz2_modmul_residues", "oz2_crt_sum", "oz2_dsyrk", "oz2_dtrmm", "oz2_kernel_launches",
 ]
 OP_N, OP_T = 0, 1
 # stage 0 times A's conversion (and B's too with OZ2_CONV_OVERLAP=1; the two column
@@ -112,6 +112,8 @@ def lib() -> ctypes.CDLL:
                 L.oz2_version.argtypes = []
                 L.oz2_set_profiling.argtypes = [P, i32]
                 L.oz2_stage_times.argtypes = [P, P, P]
+                L.oz2_kernel_launches.argtypes = []
+                L.oz2_kernel_launches.restype = ctypes.c_ulonglong
                 _lib = L
     return _lib
 
@@ -143,6 +145,11 @@ def tables(N: int) -> dict:
     return {"moduli": [int(v) for v in m], "y": [int(v) for v in y],
             "w": [words(w[5 * t:5 * t + 5]) for t in range(N)], "M": words(Mw),
             "nbytes": nb.value, "L": L.value, "T": T.value}
+
+
+def kernel_launches() -> int:
+    """liboz2 kernels launched since the library was loaded (oz2_kernel_launches)."""
+    return int(lib().oz2_kernel_launches())
 
 
 def eq17_k(N: int, q: int) -> int:

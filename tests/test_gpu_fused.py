@@ -145,10 +145,10 @@ def test_stray_env_knobs_are_inert(oz2, oracle, monkeypatch):
 
 
 def test_certificate_condition13(oz2, oracle):
-    """oz2_certify / oz2_dgemm_scaled / oz2_crt: the FAST
-    exponents certify (beta = 2T <= L); exponents raised past the bound are
-    refused -- C is all NaN and oz2_status reports OZ2_ERR_NOT_UNIQUE -- and
-    nothing is reported when the certificate holds."""
+    """oz2_certify / oz2_dgemm_scaled / oz2_crt (PAPER.md:370-381): FAST and
+    OS II-accu exponents are certified (beta <= L); exponents raised past the
+    bound are refused -- C is all NaN and oz2_status reports OZ2_ERR_NOT_UNIQUE
+    -- and nothing is reported when the certificate holds."""
     N = 14
     tab = oz2.tables(N)
     A = phi_matrix_np(300, 400, 1.0, seed=81)
@@ -158,16 +158,18 @@ def test_certificate_condition13(oz2, oracle):
     Ad, Bd = torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV)
     e = oz2.scale_rows(Ad, N)
     f = oz2.scale_cols(Bd, N)
-    beta = oz2.certify(Ad, Bd, e, f, N)
-    assert int(beta.item()) == 2 * tab["T"] <= tab["L"]
+    beta = int(oz2.certify(Ad, Bd, e, f, N).item())
+    assert beta <= 2 * tab["T"] <= tab["L"], beta           # the Cauchy-Schwarz bound alone gives 2T
     oz2.status()                                            # clears anything earlier
     C = oz2.dgemm_scaled(Ad, Bd, e, f, N).cpu().numpy()
     oz2.status()                                            # no refusal
     assert_bitwise(C, oracle.dgemm(A, B, N), "dgemm_scaled, certified")
-    # one row scaled 2^(L - 2T + 1) beyond the FAST bound: not certified
+    ea, fa = oz2.scale_accu(Ad, Bd, N)                      # accu exponents: certified too
+    assert int(oz2.certify(Ad, Bd, ea, fa, N).item()) <= tab["L"]
+    # one row scaled 2^40 beyond: no bound certifies it
     e_bad = e.clone()
-    e_bad[5] += tab["L"] - 2 * tab["T"] + 1
-    assert int(oz2.certify(Ad, Bd, e_bad, f, N).item()) == tab["L"] + 1
+    e_bad[5] += 40
+    assert int(oz2.certify(Ad, Bd, e_bad, f, N).item()) > tab["L"]
     Cb = oz2.dgemm_scaled(Ad, Bd, e_bad, f, N).cpu().numpy()
     assert np.isnan(Cb).all()
     with pytest.raises(oz2.Oz2Error) as ex:
@@ -177,7 +179,7 @@ def test_certificate_condition13(oz2, oracle):
     # the zero row may carry any exponent
     e_z = e.clone()
     e_z[7] += 1000
-    assert int(oz2.certify(Ad, Bd, e_z, f, N).item()) == 2 * tab["T"]
+    assert int(oz2.certify(Ad, Bd, e_z, f, N).item()) == beta
     # split API: oz2_crt with a certificate
     Ar = oz2.residues_rows(Ad, e_bad, N)
     Br = oz2.residues_cols(Bd, f, N)

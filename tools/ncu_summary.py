@@ -14,7 +14,8 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
         "smsp__inst_executed.sum", "launch__grid_size", "launch__block_size", "launch__cluster_dim_x",
-        "dram__bytes_read.sum.per_second", "l1tex__t_bytes.sum"]
+        "dram__bytes_read.sum.per_second", "l1tex__t_bytes.sum",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active"]
 
 
 def summary(rep):
