@@ -41,7 +41,8 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="oz2", choices=["oz2", "reference"])
-    p.add_argument("--n", "--size", dest="n", type=int, default=16384)
+    p.add_argument("--n", "--size", dest="n", type=int, default=None,
+                   help="n = k (default 16384; 32768 for multi-GPU strong scaling, BASELINE configs[3])")
     p.add_argument("--m", type=int, default=None, help="rows per rank (default n)")
     p.add_argument("--k", type=int, default=None)
     p.add_argument("--moduli", type=int, default=14)
@@ -53,8 +54,11 @@ def parse():
     p.add_argument("--parallel", default="rowblock", choices=["rowblock", "ksplit"],
                    help="multi-GPU partition: output row blocks (weak scaling, the default) or the "
                         "inner dimension (K-split, strong scaling of one m x n x k product)")
-    p.add_argument("--chunks", type=int, default=0, help="multi-GPU gather pipeline pieces (0: auto)")
-    p.add_argument("--reserve-sms", type=int, default=8, help="SMs left to NCCL when chunks > 1")
+    p.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                   help="multi-GPU row blocks: strong = one m x n x k product (default n = 32768, BASELINE "
+                        "configs[3]) split over the ranks; weak = m rows per rank (default 16384)")
+    p.add_argument("--panels", type=int, default=0, help="multi-GPU B broadcast column panels (0: auto)")
+    p.add_argument("--reserve-sms", type=int, default=8, help="SMs left to the overlapping NCCL kernels")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-context", action="store_true")
     p.add_argument("--acc-samples", type=int, default=256)
@@ -218,18 +222,31 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    n = args.n
-    m = args.m or n
+    multi_strong = world > 1 and args.parallel == "rowblock" and args.scaling == "strong"
+    n = args.n or (32768 if multi_strong else 16384)
+    m = args.m or n                                 # total rows (strong) or rows per rank (weak)
     k = args.k or n
     N = args.moduli
+    if world == 1:
+        wl = f"m=n=k={n}, N={N}, phi={args.phi:g}" if m == n == k else f"m={m}, n={n}, k={k}, N={N}, phi={args.phi:g}"
+        par, gat = "single-gpu", None
+    elif args.parallel == "ksplit":
+        wl = f"m={m}, n={n}, k={k}, N={N}, phi={args.phi:g}, K-split over {world} GPUs (strong)"
+        par, gat = f"ksplit-dp{world}", "stats all-reduces + residue all-to-all + rank-0 gather"
+    elif args.scaling == "strong":
+        wl = (f"m=n=k={n}, N={N}, phi={args.phi:g}, output row blocks over {world} GPUs (strong scaling)"
+              if m == n == k else f"m={m}, n={n}, k={k}, N={N}, phi={args.phi:g}, row blocks over {world} GPUs (strong)")
+        par = f"rowblock-dp{world}"
+        gat = "B broadcast from rank 0 in column panels, C row blocks gathered to rank 0 per panel (NCCL)"
+    else:
+        wl = f"{m} rows per GPU x n=k={n}, N={N}, phi={args.phi:g}, row blocks over {world} GPUs (weak scaling)"
+        par = f"rowblock-dp{world}"
+        gat = "B broadcast from rank 0 in column panels, C row blocks gathered to rank 0 per panel (NCCL)"
     cfg = {"n": n, "m": m, "k": k, "N": N,
-           "config": {"workload": f"m=n=k={n}, N={N}, phi={args.phi:g}" if m == n == k else
-                      f"m={m}, n={n}, k={k}, N={N}, phi={args.phi:g}",
-                      "m_per_rank": m, "n": n, "k": k, "num_moduli": N, "phi": args.phi,
-                      "parallelism": f"{args.parallel}-dp{world}" if world > 1 else "single-gpu",
-                      "gather": ("rank 0, NCCL, pipelined in row pieces" if args.parallel == "rowblock" else
-                                 "stats all-reduces + residue all-to-all + rank-0 gather") if world > 1 else None,
-                      "l2": "no flush: every step streams A, B (2.1 GB each at n=16384) > 126 MB L2",
+           "config": {"workload": wl,
+                      "m": m, "n": n, "k": k, "num_moduli": N, "phi": args.phi,
+                      "parallelism": par, "gather": gat,
+                      "l2": f"no flush: every step streams A, B ({8 * n * k / 1e9:.1f} GB each) > 126 MB L2",
                       "mode": {"fast": "fast (OS II-fast, Cauchy-Schwarz)",
                                "accu": "accu (OS II-accu, INT8 bound GEMM)",
                                "eq17": "eq17 (Eqs. 15-17)"}[args.mode]}}
@@ -256,7 +273,10 @@ def main():
             dist.init_process_group("gloo")
 
     ksplit = world > 1 and args.parallel == "ksplit"
+    rowblock = world > 1 and not ksplit
+    strong = rowblock and args.scaling == "strong"
     # inputs resident in HBM before the timed region
+    from paper_2504_08009_b200.dist import dgemm_rowblock_panels, row_partition
     if ksplit:
         # K-split: one m x n x k product, rank r holds A[:, K_r] and B[K_r, :]
         from paper_2504_08009_b200.dist import dgemm_ksplit, kslice_partition
@@ -267,30 +287,37 @@ def main():
         if rank != 0:
             del A, B
             A = B = None
-    else:
-        A = phi_matrix_torch(m, k, args.phi, SEED_A, device=dev, row_offset=rank * m)
-        B = phi_matrix_torch(k, n, args.phi, SEED_B, device=dev) if rank == 0 else \
-            torch.empty((k, n), dtype=torch.float64, device=dev)
-    C = torch.empty((m, n), dtype=torch.float64, device=dev)
-    h = oz2.handle(local)
-
-    from paper_2504_08009_b200.dist import dgemm_rowblock
-
-    # multi-GPU: B converted once per step (B-stationary), the local rows in
-    # `chunks` pieces whose NCCL gathers overlap the next piece's GEMM on SMs
-    # left free by the GEMM's SM budget (at 4+ GPUs, where the gather is large)
-    chunks = args.chunks if args.chunks else (4 if world >= 4 else 1)
-    if world > 1 and chunks > 1 and not ksplit:
+        m_total, r0, r1 = m, 0, m
+        C = torch.empty((m, n), dtype=torch.float64, device=dev)
+        C_full = C
+    elif rowblock:
+        # row blocks of A per rank; B (k x n) generated on rank 0 only and broadcast in
+        # column panels every step; C row blocks gathered to rank 0 panel by panel
+        m_total = m if strong else m * world
+        r0, r1 = row_partition(m_total, world, rank)
+        A = phi_matrix_torch(r1 - r0, k, args.phi, SEED_A, device=dev, row_offset=r0)
+        B = phi_matrix_torch(k, n, args.phi, SEED_B, device=dev) if rank == 0 else None
+        C = torch.empty((r1 - r0, n), dtype=torch.float64, device=dev)
+        C_full = torch.empty((m_total, n), dtype=torch.float64, device=dev) if rank == 0 else None
+        # leave SMs to the NCCL kernels that overlap the persistent GEMM
         oz2.set_sm_limit(torch.cuda.get_device_properties(dev).multi_processor_count - args.reserve_sms, local)
+    else:
+        m_total, r0, r1 = m, 0, m
+        A = phi_matrix_torch(m, k, args.phi, SEED_A, device=dev)
+        B = phi_matrix_torch(k, n, args.phi, SEED_B, device=dev)
+        C = torch.empty((m, n), dtype=torch.float64, device=dev)
+        C_full = C
+    h = oz2.handle(local)
+    panels = args.panels if args.panels else max(2, min(8, n // 4096))
 
     def step():
         if ksplit:
-            _, C_full = dgemm_ksplit(A_ks, B_ks, k, N, args.mode)
+            _, Cf = dgemm_ksplit(A_ks, B_ks, k, N, args.mode)
             if rank == 0:
-                C.copy_(C_full)
-        elif world > 1:
-            # B broadcast from rank 0, local row block, C gathered to rank 0 (NCCL)
-            dgemm_rowblock(A, B, N, args.mode, m_total=m * world, chunks=chunks, C_local=C)
+                C.copy_(Cf)
+        elif rowblock:
+            dgemm_rowblock_panels(A, B, N, args.mode, m_total=m_total, panels=panels, C_local=C,
+                                  C_full=C_full, n=n)
         else:
             oz2.dgemm(A, B, N, args.mode, out=C)
 
@@ -324,32 +351,34 @@ def main():
         t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
+        lt = torch.tensor([launches], dtype=torch.int64, device=dev)
+        dist.all_reduce(lt, op=dist.ReduceOp.SUM)
+        launches = int(lt.item())                    # every rank's library, summed
     ms_step = ms_total / args.steps
-    flops = 2.0 * m * (1 if ksplit else world) * n * k
+    flops = 2.0 * m_total * n * k
     value = flops / (ms_step * 1e-3) / 1e12
 
-    if rank != 0 and ksplit:                  # rank 0 holds the full operands and C
+    if rank != 0:                                    # rank 0 holds C (and B)
         dist.barrier()
         dist.destroy_process_group()
         return
-    # accuracy on sampled entries (bench-local exact reference)
+    # accuracy on sampled entries of the whole product (bench-local exact reference);
+    # the sampled rows of A are regenerated (any row range of the seeded matrix)
     rng = np.random.Generator(np.random.PCG64(3))
-    ii = rng.integers(0, m, args.acc_samples)
+    ii = rng.integers(0, m_total, args.acc_samples)
     jj = rng.integers(0, n, args.acc_samples)
-    Ai = A[torch.from_numpy(ii).to(dev)].cpu().numpy()
+    if world == 1:
+        Ai = A[torch.from_numpy(ii).to(dev)].cpu().numpy()
+    else:
+        Ai = np.stack([phi_matrix_torch(1, k, args.phi, SEED_A, device=dev, row_offset=int(i))[0].cpu().numpy()
+                       for i in ii])
     Bj = B[:, torch.from_numpy(jj).to(dev)].cpu().numpy()
     ab, absab = exact_entries(Ai, Bj)
-    cij = C[torch.from_numpy(ii).to(dev), torch.from_numpy(jj).to(dev)].cpu().numpy()
+    cij = C_full[torch.from_numpy(ii).to(dev), torch.from_numpy(jj).to(dev)].cpu().numpy()
     err = np.abs(cij - ab)
     compwise = float(np.max(err / absab))
     nz = ab != 0
     relerr = float(np.max(err[nz] / np.abs(ab[nz])))
-
-    if rank != 0:
-        if world > 1:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
 
     peaks, peak_src = measured_peaks()
     # dominant kernel: the tcgen05 modular GEMM (Alg. 1 line 6)
@@ -395,7 +424,7 @@ def main():
         conv["note"] = "in-step times (the kernels follow a power-capped GEMM at ~1.45 GHz)"
     line = {"metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if ksplit else "weak", "vs_baseline": None, "dtype": "int8 (tensor-core s8*s8->s32), f64 in/out",
+            "scaling": "strong" if (ksplit or strong) else "weak", "vs_baseline": None, "dtype": "int8 (tensor-core s8*s8->s32), f64 in/out",
             "data": "synthetic", "config": cfg["config"],
             "max_rel_err": relerr, "compwise_err": compwise, "acc_samples": int(args.acc_samples),
             "stage_ms": {s: v / max(calls, 1) for s, v in stages.items()},

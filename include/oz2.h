@@ -197,6 +197,10 @@ int oz2_prepare_b(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t
 int oz2_dgemm_prepared(oz2_handle_t h, oz2_prep_t pb, int64_t m, const double* A, int64_t lda,
                        double* C, int64_t ldc);
 int oz2_dgemm_prep2(oz2_handle_t h, oz2_prep_t pa, oz2_prep_t pb, double* C, int64_t ldc);
+/* Convert another matrix of the same shape (and side, N, mode) into p's memory,
+ * replacing its contents (stream-ordered on h: work already queued that reads
+ * p sees the old contents).  The pipelines reuse two objects per operand. */
+int oz2_reprepare(oz2_handle_t h, oz2_prep_t p, const double* X, int64_t ld);
 int oz2_release(oz2_prep_t p);
 /* Limit the persistent GEMM to `sms` SMs (0 = all; rounded down to even), e.g.
  * to leave SMs to NCCL kernels that overlap it.  Results do not depend on it. */

@@ -19,6 +19,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oz2_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "oz2_fp64_oracle.c")]
+_HDRS = [os.path.join(_HERE, "oz2_wide.h"), os.path.join(_HERE, "oz2_fast_rule.h")]
 _LIB = os.path.join(_HERE, "liboz2_oracle.so")
 
 MODE_FAST = 0
@@ -37,9 +39,9 @@ class OracleError(RuntimeError):
 
 def build(force: bool = False) -> str:
     """Compile liboz2_oracle.so (gcc, OpenMP, no FP contraction)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(f) for f in _SRCS + _HDRS):
         cmd = ["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared",
-               "-o", _LIB + ".tmp", _SRC, "-lm"]
+               "-o", _LIB + ".tmp", *_SRCS, "-lm"]
         subprocess.check_call(cmd)
         os.replace(_LIB + ".tmp", _LIB)
     return _LIB
@@ -81,6 +83,11 @@ def lib():
         L.oz2o_axpby.argtypes = [i64, ctypes.c_double, P, ctypes.c_double, P, P]
         L.oz2o_axpby.restype = None
         L.oz2o_set_threads.restype = None
+        L.oz2f_prime_bits.argtypes = [i64]
+        L.oz2f_moduli.argtypes = [i32, i64, P]
+        L.oz2f_constants.argtypes = [i32, i64, P, P, P, P, P, P]
+        L.oz2f_dgemm.argtypes = [i64, i64, i64, P, i64, P, i64, i32, i32, P, i64, P, P]
+        L.oz2f_crt_scalar.argtypes = [i32, i64, P, P]
         L.oz2o_get_threads.restype = i32
         _lib = L
     return _lib
@@ -329,3 +336,63 @@ def wide_from_double(x: float) -> int:
     out = np.zeros(4, np.uint64)
     lib().oz2o_wide_from_double(float(x), _p(out))
     return limbs_to_int(out)
+
+
+# ---------------------------------------------------------------------------
+# FP64 prime-modulus regime (Sec. 3.2; oz2_fp64_oracle.c)
+# ---------------------------------------------------------------------------
+FP64_WL = 10
+
+
+def fp64_prime_bits(q: int) -> int:
+    """Reading F1: b = floor((55 - ceil(log2 q)) / 2)."""
+    return int(lib().oz2f_prime_bits(int(q)))
+
+
+def fp64_moduli(s: int, q: int) -> list:
+    """Reading F1: the s largest primes below 2^b (Eqs. 19-21)."""
+    out = np.zeros(s, np.int64)
+    _check(lib().oz2f_moduli(s, int(q), _p(out)))
+    return [int(v) for v in out]
+
+
+def _limbs_to_int_wl(limbs) -> int:
+    v = 0
+    for i, x in enumerate(limbs):
+        v |= int(x) << (64 * i)
+    nb = 64 * len(limbs)
+    return v - (1 << nb) if v >> (nb - 1) else v
+
+
+def fp64_constants(s: int, q: int) -> dict:
+    m = np.zeros(s, np.int64)
+    y = np.zeros(s, np.int64)
+    M = np.zeros(FP64_WL, np.uint64)
+    w = np.zeros(s * FP64_WL, np.uint64)
+    L, T = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().oz2f_constants(s, int(q), _p(m), _p(y), _p(M), _p(w), ctypes.byref(L), ctypes.byref(T)))
+    return {"moduli": [int(v) for v in m], "y": [int(v) for v in y], "M": _limbs_to_int_wl(M),
+            "w": [_limbs_to_int_wl(w[t * FP64_WL:(t + 1) * FP64_WL]) for t in range(s)], "L": L.value, "T": T.value}
+
+
+def fp64_crt_scalar(s: int, q: int, residues) -> int:
+    c = np.asarray(residues, np.int64)
+    X = np.zeros(FP64_WL, np.uint64)
+    _check(lib().oz2f_crt_scalar(s, int(q), _p(c), _p(X)))
+    return _limbs_to_int_wl(X)
+
+
+def fp64_dgemm(A, B, s: int, v: int = 2, want_exponents: bool = False):
+    """C ~= A B in the FP64 prime regime with s primes for q = k: v binary64
+    words per entry, returned as [v][m][n] (most significant first, F3)."""
+    A = _as_f64(A)
+    B = _as_f64(B)
+    m, k = A.shape
+    n = B.shape[1]
+    C = np.zeros((v, m, n), np.float64)
+    e = np.zeros(max(m, 1), np.int32)
+    f = np.zeros(max(n, 1), np.int32)
+    _check(lib().oz2f_dgemm(m, n, k, _p(A), k, _p(B), n, s, v, _p(C), n, _p(e), _p(f)))
+    if want_exponents:
+        return C, e[:m], f[:n]
+    return C

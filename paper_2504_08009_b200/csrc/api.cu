@@ -1049,6 +1049,29 @@ int prepared_product(oz2_handle_t h, int64_t m, int64_t n, int64_t k, int N, con
 }
 }  // namespace
 
+int oz2_reprepare(oz2_handle_t h, oz2_prep_t p, const double* X, int64_t ld) {
+    if (!h || !p || p->device != h->device || h->mode != p->mode) return OZ2_ERR_INVALID_ARG;
+    const int64_t need_ld = p->side == OZ2_LEFT ? (p->k > 0 ? p->k : 1) : (p->rows > 0 ? p->rows : 1);
+    if (ld < need_ld || (p->k > 0 && p->rows > 0 && !X)) return OZ2_ERR_INVALID_ARG;
+    int kstar = 0, rc;
+    if (p->k > 0 && (rc = kstar_for(h, p->N, p->k, &kstar))) return rc;
+    DevGuard g(h->device);
+    if (p->k > 0 && p->rows > 0) {
+        uint8_t* base = (uint8_t*)p->mem;
+        if (p->side == OZ2_LEFT) {
+            oz2::launch_rows(X, p->rows, p->k, ld, p->N, 3, h->mode, kstar, p->exps, p->planes, p->ldr, h->stream, 0,
+                             xbits_rule(h, p->N, kstar));
+        } else {
+            const size_t off_stats = (size_t)round_up(
+                (int64_t)((size_t)((uint8_t*)p->planes - base) + (size_t)p->N * (size_t)p->rows * (size_t)p->ldr), 256);
+            oz2::launch_cols_exponents(X, p->k, p->rows, ld, p->N, h->mode, kstar, p->exps, base + off_stats, h->stream);
+            oz2::launch_cols_residues(X, p->k, p->rows, ld, p->exps, p->N, p->planes, p->ldr, h->stream, 0,
+                                      xbits_rule(h, p->N, kstar));
+        }
+    }
+    return cuda_status();
+}
+
 int oz2_prepare_a(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda, int N, oz2_prep_t* out) {
     return prepare_common(h, OZ2_LEFT, m, k, A, lda, N, out);
 }

@@ -236,3 +236,141 @@ def dgemm_ksplit(A_ks, B_ks, k_total: int, num_moduli: int = 14, mode: str = "fa
     if rank != gather_to:
         return C_local, None
     return C_local, torch.cat(bufs, dim=0)[:m].to(A_ks.device)
+
+
+def panel_partition(n: int, panels: int, align: int = 512) -> list[tuple[int, int]]:
+    """Column panels [c0, c1) of n columns, boundaries on multiples of `align`
+    (the GEMM's 512-column pair tile), as even as that allows; empty panels dropped."""
+    units = (n + align - 1) // align
+    out = []
+    for p in range(panels):
+        a, b = row_partition(units, panels, p)
+        c0, c1 = min(n, a * align), min(n, b * align)
+        if c1 > c0:
+            out.append((c0, c1))
+    return out
+
+
+class Oz2PanelOps:
+    """The CUDA library behind dgemm_rowblock_panels: A converted once
+    (oz2_prepare_a), each B panel converted into one of two reused objects
+    (oz2_prepare_b / oz2_reprepare), lines 6-10 by oz2_dgemm_prep2."""
+
+    def __init__(self, num_moduli: int, mode: str):
+        from . import oz2
+        self.oz2 = oz2
+        self.N, self.mode = num_moduli, mode
+        self.slots = {}
+
+    def prepare_a(self, A):
+        return self.oz2.PreparedA(A, self.N, self.mode)
+
+    def prepare_b(self, Bp, slot: int):
+        s = self.slots.get(slot)
+        if s is not None and (s.k, s.n) == tuple(Bp.shape):
+            return s.reprepare(Bp)
+        s = self.oz2.PreparedB(Bp, self.N, self.mode)
+        self.slots[slot] = s
+        return s
+
+    def product(self, pa, pb, out):
+        self.oz2.dgemm_prep2(pa, pb, out=out)
+
+    def close(self):
+        for s in self.slots.values():
+            s.release()
+        self.slots.clear()
+
+
+def dgemm_rowblock_panels(A_local, B, num_moduli: int = 14, mode: str = "fast", group=None, src: int = 0,
+                          gather_to: Optional[int] = 0, m_total: Optional[int] = None, panels: int = 4,
+                          C_local=None, C_full=None, ops=None, n: Optional[int] = None):
+    """C = A B with A sharded by output rows and B broadcast from `src` in column
+    panels ("Overlap mechanics" option 1), FAST / EQ17.
+
+    Every rank converts its rows of A once; then for panel p (columns [c0, c1)
+    on the 512-column tile grid) it waits for panel p's broadcast, converts it
+    (f and the B planes of those columns: f_j depends on column j only) and runs
+    the fused GEMM into C_local[:, c0:c1].  Panel p + 1 is packed (on `src`: a
+    contiguous copy of the strided column block) and broadcast while panel p is
+    converted and multiplied, and panel p's C block is gathered to `gather_to`
+    while panel p + 1 computes -- one collective stream, overlapped with the
+    compute stream.  Results are bit-identical to one GPU for any panel count.
+
+    A_local: this rank's rows (row_partition(m_total, world, rank)); B: k x n
+    on `src` (None elsewhere, with n given: the panels arrive in local buffers).  C_full
+    (gather_to only, optional): the m_total x n result, row-major.  ops: the
+    local operations (tests inject a CPU stand-in).  Returns (C_local, C_full)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    host_coll = dist.get_backend(group) == "gloo" and A_local.is_cuda
+    dev = A_local.device
+    k = A_local.shape[1]
+    if n is None:
+        n = B.shape[1]
+    if m_total is None:
+        sizes = torch.tensor([A_local.shape[0]], dtype=torch.int64, device=dev if not host_coll else "cpu")
+        all_sizes = [torch.zeros_like(sizes) for _ in range(world)]
+        dist.all_gather(all_sizes, sizes, group=group)
+        rows = [int(v.item()) for v in all_sizes]
+        m_total = sum(rows)
+    else:
+        rows = [b - a for a, b in (row_partition(m_total, world, r) for r in range(world))]
+    m_loc = A_local.shape[0]
+    mr = max(rows)
+    own_ops = ops is None
+    if ops is None:
+        ops = Oz2PanelOps(num_moduli, mode)
+    if C_local is None:
+        C_local = torch.empty((m_loc, n), dtype=torch.float64, device=dev)
+    pl = panel_partition(n, panels)
+    npmax = max(c1 - c0 for c0, c1 in pl) if pl else 0
+    cdev = "cpu" if host_coll else dev
+    # two flat panel buffers; panel p is a contiguous k x (c1 - c0) view (collectives need contiguity)
+    bufs = [torch.empty(k * npmax, dtype=torch.float64, device=cdev) for _ in range(min(2, len(pl)))]
+    do_gather = gather_to is not None and world > 1
+    if gather_to is not None and rank == gather_to and C_full is None:
+        C_full = torch.empty((m_total, n), dtype=torch.float64, device=dev)
+    rstart = [sum(rows[:r]) for r in range(world)]
+
+    def bcast(p):
+        c0, c1 = pl[p]
+        buf = bufs[p % 2][:k * (c1 - c0)].view(k, c1 - c0)
+        if rank == src:
+            buf.copy_(B[:, c0:c1])                        # strided column block -> contiguous
+        return dist.broadcast(buf, src=src, group=group, async_op=True), buf
+
+    pa = ops.prepare_a(A_local) if m_loc > 0 else None
+    pending = bcast(0) if pl else None
+    gathers = []
+    for p, (c0, c1) in enumerate(pl):
+        work, buf = pending
+        work.wait()                                       # compute stream waits for panel p
+        if host_coll:
+            bdev = buf.to(dev)
+        else:
+            bdev = buf
+        if p + 1 < len(pl):
+            pending = bcast(p + 1)                        # overlaps panel p's conversion + GEMM
+        if m_loc > 0:
+            pb = ops.prepare_b(bdev, p % 2)
+            ops.product(pa, pb, C_local[:, c0:c1])
+        if do_gather:
+            send = torch.zeros((mr, c1 - c0), dtype=torch.float64, device=cdev)
+            send[:m_loc] = C_local[:, c0:c1]
+            recv = ([torch.empty((mr, c1 - c0), dtype=torch.float64, device=cdev) for _ in range(world)]
+                    if rank == gather_to else None)
+            gathers.append((dist.gather(send, recv, dst=gather_to, group=group, async_op=True), recv, c0, c1, send))
+        elif gather_to is not None and rank == gather_to:
+            C_full[:, c0:c1] = C_local[:, c0:c1]
+    for w, recv, c0, c1, _ in gathers:
+        w.wait()
+        if rank == gather_to:
+            for r in range(world):
+                C_full[rstart[r]:rstart[r] + rows[r], c0:c1] = recv[r][:rows[r]].to(dev)
+    if own_ops:
+        ops.close()
+    return C_local, (C_full if gather_to is not None and rank == gather_to else None)

@@ -33,7 +33,7 @@ SYMBOLS = [
     "oz2_modmul", "oz2_crt", "oz2_tables", "oz2_eq17_k", "oz2_strerror", "oz2_version",
     "oz2_set_profiling", "oz2_stage_times", "oz2_dgemm_op", "oz2_dgemm_strided_batched",
     "oz2_scale_accu", "oz2_dgemm_scaled", "oz2_prepare_a", "oz2_prepare_b", "oz2_dgemm_prepared",
-    "oz2_dgemm_prep2", "oz2_release", "oz2_certify", "oz2_set_certify", "oz2_status",
+    "oz2_dgemm_prep2", "oz2_reprepare", "oz2_release", "oz2_certify", "oz2_set_certify", "oz2_status",
     "oz2_set_sm_limit", "oz2_kslice_stats_rows", "oz2_kslice_stats_cols", "oz2_exponents_from_stats",
     "oz2_modmul_residues", "oz2_crt_sum", "oz2_dsyrk", "oz2_dtrmm", "oz2_kernel_launches",
 ]
@@ -89,6 +89,7 @@ def lib() -> ctypes.CDLL:
                 L.oz2_dgemm_prepared.argtypes = [P, P, i64, P, i64, P, i64]
                 L.oz2_dgemm_prep2.argtypes = [P, P, P, P, i64]
                 L.oz2_release.argtypes = [P]
+                L.oz2_reprepare.argtypes = [P, P, P, i64]
                 L.oz2_certify.argtypes = [P, i64, i64, i64, P, i64, P, i64, P, P, i32, P]
                 L.oz2_set_certify.argtypes = [P, i32]
                 L.oz2_status.argtypes = [P]
@@ -327,6 +328,20 @@ class Prepared:
         if self._p is None or not self._p.value:
             raise ValueError("prepared operand already released")
         return self._p
+
+    def reprepare(self, X):
+        """Convert another matrix of the same shape into this object's memory
+        (oz2_reprepare; stream-ordered after work already queued that reads it)."""
+        import torch
+
+        X = _rowmajor(X, torch.float64)
+        _same_device(self.device, X)
+        shape = (self.rows, self.k) if self.side == "A" else (self.k, self.rows)
+        if tuple(X.shape) != shape:
+            raise ValueError(f"reprepare: shape {tuple(X.shape)}, prepared with {shape}")
+        self.h.prepare(self.mode)
+        _check(lib().oz2_reprepare(self.h.ptr, self.ptr, _vp(X), _ld(X)), "oz2_reprepare")
+        return self
 
     def release(self):
         if self._p is not None and self._p.value:

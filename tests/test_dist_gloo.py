@@ -124,3 +124,55 @@ def test_rowblock_gloo_world2(tmp_path, oracle, m, chunks):
     ref = oracle.dgemm(A, B, N)
     assert C.shape == (m, n)
     assert np.array_equal(C.view(np.int64), ref.view(np.int64))
+
+
+class _OraclePanelOps:
+    """CPU stand-in for dist.Oz2PanelOps: 'prepared' operands are the matrices,
+    the product is the oracle (FAST): the host logic of the panel pipeline
+    (panel packing, broadcast, per-panel gather, reassembly) is what is tested."""
+
+    def __init__(self, N):
+        self.N = N
+
+    def prepare_a(self, A):
+        return A.clone()
+
+    def prepare_b(self, Bp, slot):
+        return Bp.clone()
+
+    def product(self, pa, pb, out):
+        import oracle
+        out.copy_(torch.from_numpy(oracle.dgemm(pa.numpy(), pb.numpy(), self.N)))
+
+
+def _worker_panels(rank, world, port, m, n, k, N, panels, out_path):
+    from paper_2504_08009_b200.dist import dgemm_rowblock_panels
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = phi_matrix_np(m, k, 1.0, seed=17)
+        r0, r1 = row_partition(m, world, rank)
+        A_local = torch.from_numpy(A[r0:r1].copy())
+        B = torch.from_numpy(phi_matrix_np(k, n, 1.0, seed=18)) if rank == 0 else None
+        _, C_full = dgemm_rowblock_panels(A_local, B, N, m_total=m, panels=panels, ops=_OraclePanelOps(N), n=n)
+        if rank == 0:
+            np.save(out_path, C_full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("m,n,panels", [(37, 1300, 3), (8, 700, 4), (5, 1030, 1)])
+def test_rowblock_panels_gloo_world2(tmp_path, oracle, m, n, panels):
+    """B broadcast in 512-column-aligned panels (ragged last panel), C gathered
+    per panel and reassembled on rank 0 (ragged row blocks): bit-identical to
+    the single-process product (f_j depends on column j only, reading R4)."""
+    from paper_2504_08009_b200.dist import panel_partition
+    k, N = 300, 14
+    pl = panel_partition(n, panels)
+    assert pl[0][0] == 0 and pl[-1][1] == n and all(c0 % 512 == 0 for c0, _ in pl)
+    out = str(tmp_path / "c.npy")
+    mp.spawn(_worker_panels, args=(2, _free_port(), m, n, k, N, panels, out), nprocs=2, join=True)
+    C = np.load(out)
+    ref = oracle.dgemm(phi_matrix_np(m, k, 1.0, seed=17), phi_matrix_np(k, n, 1.0, seed=18), N)
+    assert np.array_equal(C.view(np.int64), ref.view(np.int64))

@@ -87,9 +87,13 @@ def _worker(rank, world, port, out):
         r0, r1 = row_partition(m, world, rank)
         Bb = B.clone() if rank == 0 else torch.empty_like(B)
         _, Cr = dgemm_rowblock(A[r0:r1].contiguous(), Bb, N, m_total=m, chunks=2)
+        from paper_2504_08009_b200.dist import dgemm_rowblock_panels
+        # B in 2 column panels (512-aligned: 512 + 138 columns), C gathered per panel
+        _, Cp = dgemm_rowblock_panels(A[r0:r1].contiguous(), B if rank == 0 else None, N, m_total=m, panels=2,
+                                      n=n)
         if rank == 0:
             ref = oz2.dgemm(A, B, N)
-            np.save(out, np.stack([Ck.cpu().numpy(), Cr.cpu().numpy(), ref.cpu().numpy()]))
+            np.save(out, np.stack([Ck.cpu().numpy(), Cr.cpu().numpy(), Cp.cpu().numpy(), ref.cpu().numpy()]))
     finally:
         dist.destroy_process_group()
 
@@ -98,6 +102,7 @@ def test_dist_ksplit_and_rowblock_two_ranks_one_gpu(oz2, tmp_path):
     import torch.multiprocessing as mp
     out = str(tmp_path / "k.npy")
     mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
-    Ck, Cr, ref = np.load(out)
+    Ck, Cr, Cp, ref = np.load(out)
     assert np.array_equal(Ck.view(np.int64), ref.view(np.int64)), "dgemm_ksplit"
     assert np.array_equal(Cr.view(np.int64), ref.view(np.int64)), "dgemm_rowblock (prepared B, pieces)"
+    assert np.array_equal(Cp.view(np.int64), ref.view(np.int64)), "dgemm_rowblock_panels (prepared A, B panels)"
