@@ -261,6 +261,28 @@ int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                    int num_moduli);
 
+/* ---- the FP64 prime-modulus regime (Sec. 3.2) -----------
+ * C ~= A B with s pairwise-coprime primes m_t: the s largest primes below 2^b,
+ * b = floor((55 - ceil(log2 k)) / 2) (reading F1), so that k m_t^2 <= 2^55 =
+ * 4 u^-1 (Eq. 19) and every residue product is exact in binary64 (Eq. 20);
+ * for k = 1024 the moduli are Eq. (21) verbatim.  Line 1 is the OS II-fast rule
+ * with this M's T (reading F2); lines 2-5 form binary64 residue planes; line 6
+ * runs as s FP64 tensor-core GEMMs (cuBLAS DGEMM, strided batched, loaded at
+ * run time); lines 7-10 reconstruct X exactly and write v binary64 words per
+ * entry (reading F3: word w at C + w * strideC, most significant first, each
+ * the nearest binary64 to what the earlier words leave) -- results beyond
+ * binary64 precision (k_A ~ 170 at s = 16).
+ * s in [2, 22]; v in [1, 4]; m k, k n, m n < 2^31 (cuBLAS).  Workspace:
+ * oz2_fp64mod_workspace_bytes (8 s (mk + kn + mn) + small).  Errors as
+ * oz2_dgemm_ex; cuBLAS missing or failing: OZ2_ERR_CUDA. */
+int oz2_dgemm_fp64mod(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A,
+                      int64_t lda, const double* B, int64_t ldb, int s, int v, double* C,
+                      int64_t ldc, int64_t strideC);
+size_t oz2_fp64mod_workspace_bytes(int64_t m, int64_t n, int64_t k, int s);
+/* The regime's constants (host only): moduli[s], M as 17 little-endian 32-bit
+ * words, L = floor(log2(M/2 - 1)), T = floor(L/2); q = the inner dimension. */
+int oz2_fp64mod_tables(int s, int64_t q, int64_t* moduli, uint32_t* M_words, int32_t* L, int32_t* T);
+
 /* ---- split API: each stage of Algorithm 1 on its own (stage parity) ------- */
 /* Alg. 1 line 1 for the rows of A (m x k): e[i] such that D = diag(2^e[i])
  * (reading R4 / R5 by the handle's mode).  e: int32[m]. */

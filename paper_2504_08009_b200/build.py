@@ -21,7 +21,7 @@ OBJDIR = os.path.join(HERE, "build")
 
 COMMON = ["oz2_device.cuh", "oz2_kernels.h", "oz2_tables.h", "crt_device.cuh"]
 UNITS = {
-    "liboz2.cu": COMMON + ["liboz2.cu", "scale.cu", "crt.cu", "accu.cu", "kslice.cu", "certify.cu", "api.cu"],
+    "liboz2.cu": COMMON + ["liboz2.cu", "scale.cu", "crt.cu", "accu.cu", "kslice.cu", "certify.cu", "fp64mod.cu", "api.cu"],
     "liboz2_gemm.cu": COMMON + ["liboz2_gemm.cu", "gemm.cu"],
     "tables.cpp": ["tables.cpp", "oz2_tables.h"],
 }

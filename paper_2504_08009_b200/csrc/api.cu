@@ -1049,6 +1049,43 @@ int prepared_product(oz2_handle_t h, int64_t m, int64_t n, int64_t k, int N, con
 }
 }  // namespace
 
+int oz2_fp64mod_tables(int s, int64_t q, int64_t* moduli, uint32_t* M_words, int32_t* L, int32_t* T) {
+    if (s < 2 || s > oz2::F64_MAX_S) return OZ2_ERR_NUM_MODULI;
+    if (q < 1 || q > OZ2_MAX_K) return OZ2_ERR_INVALID_ARG;
+    return oz2::f64_tables(s, q, moduli, M_words, L, T) ? OZ2_ERR_INVALID_ARG : OZ2_OK;
+}
+
+size_t oz2_fp64mod_workspace_bytes(int64_t m, int64_t n, int64_t k, int s) {
+    if (m < 0 || n < 0 || k < 1 || s < 2 || s > oz2::F64_MAX_S) return 0;
+    return oz2::f64_workspace_bytes(m, n, k, s);
+}
+
+int oz2_dgemm_fp64mod(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                      const double* B, int64_t ldb, int s, int v, double* C, int64_t ldc, int64_t strideC) {
+    if (!h) return OZ2_ERR_INVALID_ARG;
+    if (s < 2 || s > oz2::F64_MAX_S) return OZ2_ERR_NUM_MODULI;
+    if (m < 0 || n < 0 || k < 0 || v < 1 || v > 4) return OZ2_ERR_INVALID_ARG;
+    if (k >= OZ2_MAX_K) return OZ2_ERR_K_TOO_LARGE;
+    if (m > INT32_MAX || n > INT32_MAX || m * k > INT32_MAX || k * n > INT32_MAX || m * n > INT32_MAX)
+        return OZ2_ERR_INVALID_ARG;                   // cuBLAS int dimensions / strides
+    if (lda < (k > 0 ? k : 1) || ldb < (n > 0 ? n : 1) || ldc < (n > 0 ? n : 1) ||
+        (v > 1 && strideC < m * ldc) || (m > 0 && n > 0 && (!C || (k > 0 && (!A || !B)))))
+        return OZ2_ERR_INVALID_ARG;
+    if (m == 0 || n == 0) return OZ2_OK;
+    DevGuard g(h->device);
+    if (k == 0) {
+        for (int w = 0; w < v; w++) oz2::launch_scale_c(C + w * strideC, m, n, ldc, 0.0, h->stream);
+        return cuda_status();
+    }
+    uint8_t* ws;
+    int rc;
+    if ((rc = get_workspace(h, oz2::f64_workspace_bytes(m, n, k, s), &ws))) return rc;
+    const int r = oz2::launch_fp64mod(h->device, A, m, k, lda, B, n, ldb, s, v, C, ldc, strideC, ws, h->stream);
+    if (r == -1) return OZ2_ERR_INVALID_ARG;
+    if (r) return OZ2_ERR_CUDA;
+    return cuda_status();
+}
+
 int oz2_reprepare(oz2_handle_t h, oz2_prep_t p, const double* X, int64_t ld) {
     if (!h || !p || p->device != h->device || h->mode != p->mode) return OZ2_ERR_INVALID_ARG;
     const int64_t need_ld = p->side == OZ2_LEFT ? (p->k > 0 ? p->k : 1) : (p->rows > 0 ? p->rows : 1);

@@ -172,6 +172,14 @@ void launch_exponents_from_stats(const int32_t* E, const unsigned long long* S, 
     else (exponents_from_stats_kernel<1><<<g, 256, 0, st>>>(E, S, cnt, host_T(N), kstar, e), count_launch());
 }
 
+// FAST exponents from the statistics with an explicit bound exponent T (the FP64
+// prime regime's M, fp64mod.cu)
+void launch_exponents_T(const int32_t* E, const unsigned long long* S, int64_t cnt, int T, int32_t* e,
+                        cudaStream_t st) {
+    if (cnt <= 0) return;
+    (exponents_from_stats_kernel<0><<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(E, S, cnt, T, 0, e), count_launch());
+}
+
 template <int NM>
 static void launch_crt_sum_nm(const uint8_t* R, int G, int64_t part_stride, int64_t m, int64_t n, const int32_t* e,
                               const int32_t* f, double* C, int64_t ldc, cudaStream_t st) {

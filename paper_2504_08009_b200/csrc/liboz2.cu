@@ -8,4 +8,5 @@
 #include "accu.cu"
 #include "kslice.cu"
 #include "certify.cu"
+#include "fp64mod.cu"
 #include "api.cu"

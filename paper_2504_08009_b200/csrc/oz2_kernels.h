@@ -108,6 +108,20 @@ void launch_certify(const double* A, int64_t m, int64_t k, int64_t lda, const do
 void launch_refuse(const int32_t* beta, int N, double* C, int64_t m, int64_t n, int64_t ldc, int* status,
                    cudaStream_t st);
 
+// fp64mod.cu -- the FP64 prime-modulus regime (Eqs. 19-21)
+constexpr int F64_MAX_S = 22;      // primes (reading F4)
+constexpr int F64_MAX_W = 17;      // 32-bit words of S = sum c''_t w_t < s 2^22 M < 2^511
+constexpr int F64_POW2 = 256;      // 2^j mod m_t table: trunc(2^e a) < 2^(T+1) <= 2^242 = mant 2^sh, sh < 192
+int f64_prime_bits(int64_t q);
+int f64_tables(int s, int64_t q, int64_t* moduli, uint32_t* M_words, int32_t* L, int32_t* T);
+size_t f64_workspace_bytes(int64_t m, int64_t n, int64_t k, int s);
+// 0 ok, -1 bad (s, k), -2 cuBLAS unavailable, -3 cuBLAS error, -4 CUDA error
+int launch_fp64mod(int device, const double* A, int64_t m, int64_t k, int64_t lda, const double* B, int64_t n,
+                   int64_t ldb, int s, int v, double* C, int64_t ldc, int64_t strideC, uint8_t* ws,
+                   cudaStream_t st);
+void launch_exponents_T(const int32_t* E, const unsigned long long* S, int64_t cnt, int T, int32_t* e,
+                        cudaStream_t st);
+
 // crt.cu -- Alg. 1 lines 7-10
 void launch_crt(const int32_t* cprod, int64_t m, int64_t n, const int32_t* e, const int32_t* f,
                 int N, double* C, int64_t ldc, cudaStream_t st);

@@ -36,6 +36,7 @@ SYMBOLS = [
     "oz2_dgemm_prep2", "oz2_reprepare", "oz2_release", "oz2_certify", "oz2_set_certify", "oz2_status",
     "oz2_set_sm_limit", "oz2_kslice_stats_rows", "oz2_kslice_stats_cols", "oz2_exponents_from_stats",
     "oz2_modmul_residues", "oz2_crt_sum", "oz2_dsyrk", "oz2_dtrmm", "oz2_kernel_launches",
+    "oz2_dgemm_fp64mod", "oz2_fp64mod_workspace_bytes", "oz2_fp64mod_tables",
 ]
 OP_N, OP_T = 0, 1
 # stage 0 times A's conversion (and B's too with OZ2_CONV_OVERLAP=1; the two column
@@ -113,6 +114,10 @@ def lib() -> ctypes.CDLL:
                 L.oz2_version.argtypes = []
                 L.oz2_set_profiling.argtypes = [P, i32]
                 L.oz2_stage_times.argtypes = [P, P, P]
+                L.oz2_dgemm_fp64mod.argtypes = [P, i64, i64, i64, P, i64, P, i64, i32, i32, P, i64, i64]
+                L.oz2_fp64mod_workspace_bytes.argtypes = [i64, i64, i64, i32]
+                L.oz2_fp64mod_workspace_bytes.restype = sz
+                L.oz2_fp64mod_tables.argtypes = [i32, i64, P, P, P, P]
                 L.oz2_kernel_launches.argtypes = []
                 L.oz2_kernel_launches.restype = ctypes.c_ulonglong
                 _lib = L
@@ -768,3 +773,40 @@ def status(device=None):
 
 def set_certify(on: bool, device=None):
     _check(lib().oz2_set_certify(handle(device).ptr, 1 if on else 0), "oz2_set_certify")
+
+
+# ---------------------------------------------------------------------------
+# the FP64 prime-modulus regime (include/oz2.h)
+# ---------------------------------------------------------------------------
+def fp64mod_tables(s: int, q: int) -> dict:
+    m = np.zeros(s, np.int64)
+    Mw = np.zeros(17, np.uint32)
+    L, T = ctypes.c_int32(), ctypes.c_int32()
+    c = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    _check(lib().oz2_fp64mod_tables(s, int(q), c(m), c(Mw), ctypes.byref(L), ctypes.byref(T)), "oz2_fp64mod_tables")
+    return {"moduli": [int(v) for v in m], "M": sum(int(v) << (32 * i) for i, v in enumerate(Mw)),
+            "L": L.value, "T": T.value}
+
+
+def dgemm_fp64mod(A, B, s: int = 16, v: int = 2, out=None):
+    """C ~= A @ B in the FP64 prime-modulus regime with s primes: a (v, m, n)
+    float64 tensor, word 0 the most significant (oz2_dgemm_fp64mod)."""
+    import torch
+
+    A = _rowmajor(A, torch.float64)
+    B = _rowmajor(B, torch.float64)
+    _same_device(A.device, B)
+    m, k = A.shape
+    k2, n = B.shape
+    if k != k2:
+        raise ValueError(f"inner dimensions differ: {A.shape} @ {B.shape}")
+    if out is None:
+        out = torch.empty((v, m, n), dtype=torch.float64, device=A.device)
+    if not (out.dtype == torch.float64 and out.device == A.device and tuple(out.shape) == (v, m, n)
+            and out.is_contiguous()):
+        raise ValueError(f"out must be a contiguous float64 ({v}, {m}, {n}) tensor on {A.device}")
+    h = handle(A.device.index)
+    h.prepare("fast", int(lib().oz2_fp64mod_workspace_bytes(m, n, max(k, 1), s)))
+    _check(lib().oz2_dgemm_fp64mod(h.ptr, m, n, k, _vp(A), _ld(A), _vp(B), _ld(B), s, v, _vp(out), max(1, n),
+                                   m * max(1, n)), "oz2_dgemm_fp64mod")
+    return out

@@ -5,6 +5,6 @@
 mkdir -p gpurun_out
 N=${N:-4096}
 timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
-   --master-port 29511 bench.py --gpus 2 --steps 1 --warmup 3 --dist-backend gloo --n $N --acc-samples 64 \
+   --master-port 29511 bench.py --gpus 2 --steps 1 --warmup 3 --dist-backend gloo --size $N --acc-samples 64 \
    > gpurun_out/dist_check_$N.json 2> gpurun_out/dist_check_$N.err
 echo "dist check n=$N rc=$?"; tail -c 1500 gpurun_out/dist_check_$N.json; tail -5 gpurun_out/dist_check_$N.err
