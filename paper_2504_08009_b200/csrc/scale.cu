@@ -150,6 +150,71 @@ struct EQuad {
     uint32_t b[4];          // BW_12 only
 };
 
+// One A quad (two elements, fragment order as residues_imma) against NP modulus
+// pairs' B fragments in ONE asm statement: the quad stays in its registers for
+// all NP MMAs (separate statements let ptxas copy it before every MMA), the
+// accumulator addend is RZ (the 7-byte width puts the bias into B).
+template <int NP>
+__device__ __forceinline__ void imma_block(uint32_t (&d)[4 * NP], const uint32_t (&a)[4], const uint32_t (&b)[2 * NP]) {
+    if constexpr (NP == 1) {
+        asm(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {0,0,0,0};\n\t"
+            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+    } else if constexpr (NP == 2) {
+        asm(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%8,%9,%10,%11}, {%12,%13}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%4,%5,%6,%7}, {%8,%9,%10,%11}, {%14,%15}, {0,0,0,0};\n\t"
+            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]));
+    } else if constexpr (NP == 3) {
+        asm(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%12,%13,%14,%15}, {%16,%17}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%4,%5,%6,%7}, {%12,%13,%14,%15}, {%18,%19}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%8,%9,%10,%11}, {%12,%13,%14,%15}, {%20,%21}, {0,0,0,0};\n\t"
+            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]));
+    } else if constexpr (NP == 4) {
+        asm(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%16,%17,%18,%19}, {%20,%21}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%4,%5,%6,%7}, {%16,%17,%18,%19}, {%22,%23}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%8,%9,%10,%11}, {%16,%17,%18,%19}, {%24,%25}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%12,%13,%14,%15}, {%16,%17,%18,%19}, {%26,%27}, {0,0,0,0};\n\t"
+            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]), "r"(b[6]), "r"(b[7]));
+    } else if constexpr (NP == 5) {
+        asm(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%20,%21,%22,%23}, {%24,%25}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%4,%5,%6,%7}, {%20,%21,%22,%23}, {%26,%27}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%8,%9,%10,%11}, {%20,%21,%22,%23}, {%28,%29}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%12,%13,%14,%15}, {%20,%21,%22,%23}, {%30,%31}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%16,%17,%18,%19}, {%20,%21,%22,%23}, {%32,%33}, {0,0,0,0};\n\t"
+            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]), "r"(b[6]), "r"(b[7]), "r"(b[8]), "r"(b[9]));
+    } else if constexpr (NP == 6) {
+        asm(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%24,%25,%26,%27}, {%28,%29}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%4,%5,%6,%7}, {%24,%25,%26,%27}, {%30,%31}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%8,%9,%10,%11}, {%24,%25,%26,%27}, {%32,%33}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%12,%13,%14,%15}, {%24,%25,%26,%27}, {%34,%35}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%16,%17,%18,%19}, {%24,%25,%26,%27}, {%36,%37}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%20,%21,%22,%23}, {%24,%25,%26,%27}, {%38,%39}, {0,0,0,0};\n\t"
+            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]), "=r"(d[20]), "=r"(d[21]), "=r"(d[22]), "=r"(d[23])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]), "r"(b[6]), "r"(b[7]), "r"(b[8]), "r"(b[9]), "r"(b[10]), "r"(b[11]));
+    } else if constexpr (NP == 7) {
+        asm(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%28,%29,%30,%31}, {%32,%33}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%4,%5,%6,%7}, {%28,%29,%30,%31}, {%34,%35}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%8,%9,%10,%11}, {%28,%29,%30,%31}, {%36,%37}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%12,%13,%14,%15}, {%28,%29,%30,%31}, {%38,%39}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%16,%17,%18,%19}, {%28,%29,%30,%31}, {%40,%41}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%20,%21,%22,%23}, {%28,%29,%30,%31}, {%42,%43}, {0,0,0,0};\n\t"
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%24,%25,%26,%27}, {%28,%29,%30,%31}, {%44,%45}, {0,0,0,0};\n\t"
+            : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]), "=r"(d[20]), "=r"(d[21]), "=r"(d[22]), "=r"(d[23]), "=r"(d[24]), "=r"(d[25]), "=r"(d[26]), "=r"(d[27])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]), "r"(b[6]), "r"(b[7]), "r"(b[8]), "r"(b[9]), "r"(b[10]), "r"(b[11]), "r"(b[12]), "r"(b[13]));
+    }
+}
+
 // residues for t = 1..NM-1 of the 2 * NQ elements held as quads q[0..NQ) (NQ
 // even); store(t, pw[NQ/2]) receives the int8 residues of modulus t packed 4 per
 // word in element order (element 2i, 2i+1 of quad i).  Every lane of the warp
@@ -164,6 +229,38 @@ __device__ __forceinline__ void residues_imma(const EQuad<BW> (&q)[NQ], Store&& 
     const Oz2Table& T = c_tab[NM];
     const int lane = threadIdx.x & 31;
     const uint32_t* bf = &g_bfrag[NM][BW == BW_7 ? 1 : 0][0][lane][0];
+    if constexpr (BW == BW_7) {
+        // all NP pairs of one quad in one asm statement (imma_block); the B
+        // fragments stay live in registers for the thread's NQ quads
+        uint32_t b[2 * NP];
+        #pragma unroll
+        for (int p = 0; p < NP; p++) { b[2 * p] = __ldg(bf + p * 96); b[2 * p + 1] = __ldg(bf + p * 96 + 1); }
+        uint32_t pw[NM][NQ / 2];
+        #pragma unroll
+        for (int u = 0; u < NQ / 2; u++) {
+            uint32_t half[NM];                             // modulus t: bytes of elements 4u, 4u + 1
+            #pragma unroll
+            for (int h = 0; h < 2; h++) {
+                uint32_t d[4 * NP];
+                imma_block<NP>(d, q[2 * u + h].a, b);
+                #pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    const int t0 = 1 + 2 * p, t1 = t0 + 1;
+                    const uint32_t r0a = sym_residue<NM>(d[4 * p], t0), r0b = sym_residue<NM>(d[4 * p + 2], t0);
+                    if (h == 0) half[t0] = prmt(r0a, r0b, 0x0040u);
+                    else pw[t0][u] = prmt(half[t0], prmt(r0a, r0b, 0x0040u), 0x5410u);
+                    if (t1 < NM) {
+                        const uint32_t r1a = sym_residue<NM>(d[4 * p + 1], t1), r1b = sym_residue<NM>(d[4 * p + 3], t1);
+                        if (h == 0) half[t1] = prmt(r1a, r1b, 0x0040u);
+                        else pw[t1][u] = prmt(half[t1], prmt(r1a, r1b, 0x0040u), 0x5410u);
+                    }
+                }
+            }
+        }
+        #pragma unroll
+        for (int t = 1; t < NM; t++) store(t, pw[t]);
+        return;
+    }
     uint32_t pw[NM][NQ / 2];                           // pw[t][u]: modulus t, elements 4u..4u+3
     #pragma unroll
     for (int u = 0; u < NQ / 2; u++) {
@@ -556,13 +653,18 @@ __device__ void row_residues(const double* __restrict__ X, int64_t k, int e, int
 // <= 14 with FAST / EQ17 exponents), dp4a otherwise (OZ2_RES_IMMA=0: always dp4a)
 template <int BW>
 struct UseImma { static constexpr bool value = OZ2_RES_IMMA && BW == BW_7; };
+#ifndef OZ2_COLS_IMMA
+#define OZ2_COLS_IMMA 0          // the column kernel on the IMMA path too (measured slower: see section 7)
+#endif
+template <int BW>
+struct UseImmaCols { static constexpr bool value = OZ2_COLS_IMMA && UseImma<BW>::value; };
 
 // residues of RPT elements a[] of this thread (scale 2^e = s1 s2) for all NM
 // moduli; put(t, pw[RPT/4]) receives modulus t's bytes packed 4 per word.  On
 // the IMMA path every lane of the warp must call it.
 template <int NM, int BW, int RPT, typename Put>
 __device__ __forceinline__ void thread_residues(const double (&a)[RPT], double s1, double s2, Put&& put) {
-    if constexpr (UseImma<BW>::value) {
+    if constexpr (UseImmaCols<BW>::value) {
         EQuad<BW> eq[RPT / 2];
         #pragma unroll
         for (int q = 0; q < RPT / 2; q++) to_quad<BW>(a[2 * q], a[2 * q + 1], s1, s2, eq[q]);
@@ -839,7 +941,7 @@ __global__ void cols_finalize_kernel(const int32_t* __restrict__ Ec, const unsig
 // resident CTAs per SM the register budget allows: the kernel is latency-bound
 // on its loads, so occupancy matters (4 CTAs = 64 registers; N > 14 needs 80)
 template <int NM, int BW, int CR_ROWS>
-__global__ void __launch_bounds__(256, UseImma<BW>::value ? 4 : 1)
+__global__ void __launch_bounds__(256, UseImmaCols<BW>::value ? 3 : 1)
 cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t ldb,
                      const int32_t* __restrict__ f, int8_t* __restrict__ out, int64_t ldr, int64_t pstride) {
     constexpr int WORDS = BwWords<BW>::value;
