@@ -94,3 +94,35 @@ def test_fp64mod_errors(oz2):
         oz2.dgemm_fp64mod(A, A, 1, 2)
     with pytest.raises(oz2.Oz2Error):
         oz2.dgemm_fp64mod(A, A, 16, 5)
+
+
+def test_fp64mod_products_exact_at_the_eq20_bound(oz2, oracle):
+    """Eq. (20): |C'_t| <= q (m_t/2)^2 <= 2^53 keeps the FP64 residue GEMMs
+    exact.  Constant A (value c) and B (value d) rows give C'_t = k r_t(a') r_t(b')
+    with every term of one sign; c, d are chosen (Python integers, from the
+    oracle's exponents) so that some |C'_t| exceeds 2^52.9 at k = 2048, the
+    largest k with 22-bit primes (k m^2 <= 2^55).  The GPU words must equal
+    the oracle's, whose products are int64."""
+    k, s, v = 2048, 16, 2
+    mods = oracle.fp64_moduli(s, k)
+    best = None
+    for c in range(3, 4000, 2):
+        A = np.full((1, k), float(c))
+        C, e, f = oracle.fp64_dgemm(A, A.T.copy(), s, 1, want_exponents=True)
+        ap = c * 2 ** int(e[0])
+        rs = []
+        for m in mods:
+            r = ap % m
+            rs.append(r - m if r > (m - 1) // 2 else r)
+        worst = max(k * r * r for r in rs)
+        if best is None or worst > best[0]:
+            best = (worst, c)
+        if worst > 2.0 ** 52.9:
+            break
+    worst, c = best
+    assert worst > 2.0 ** 52.9 and worst <= 2 ** 53, (worst, c)
+    A = np.full((64, k), float(c))
+    A[1::2] *= -1.0                       # mixed signs across rows, one sign within a row
+    B = A[:48].T.copy()
+    got = oz2.dgemm_fp64mod(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), s, v).cpu().numpy()
+    _bitwise(got, oracle.fp64_dgemm(A, B, s, v), "fp64mod at the Eq. 20 bound")
