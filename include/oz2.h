@@ -278,6 +278,13 @@ int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double
 int oz2_dgemm_fp64mod(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A,
                       int64_t lda, const double* B, int64_t ldb, int s, int v, double* C,
                       int64_t ldc, int64_t strideC);
+/* The same for double-word inputs (Eqs. 22-23, reading F6): A = A + A2, B = B + B2
+ * (A2, B2 with the leading dimensions of A, B; either may be NULL = zero),
+ * with |A2| <= u |A| and |B2| <= u |B| elementwise (Eq. 23; u = 2^-53).  Line 1
+ * uses |A| + |A2| rounded upward; trunc(2^e (a + a2)) is formed exactly. */
+int oz2_dgemm_fp64mod_dw(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A,
+                         const double* A2, int64_t lda, const double* B, const double* B2,
+                         int64_t ldb, int s, int v, double* C, int64_t ldc, int64_t strideC);
 size_t oz2_fp64mod_workspace_bytes(int64_t m, int64_t n, int64_t k, int s);
 /* The regime's constants (host only): moduli[s], M as 17 little-endian 32-bit
  * words, L = floor(log2(M/2 - 1)), T = floor(L/2); q = the inner dimension. */

@@ -87,6 +87,9 @@ def lib():
         L.oz2f_moduli.argtypes = [i32, i64, P]
         L.oz2f_constants.argtypes = [i32, i64, P, P, P, P, P, P]
         L.oz2f_dgemm.argtypes = [i64, i64, i64, P, i64, P, i64, i32, i32, P, i64, P, P]
+        L.oz2f_dgemm_mw.argtypes = [i64, i64, i64, P, P, i64, P, P, i64, i32, i32, P, i64, P, P]
+        L.oz2f_scaled_trunc_mw.argtypes = [ctypes.c_double, ctypes.c_double, i32, P]
+        L.oz2f_scaled_trunc_mw.restype = None
         L.oz2f_crt_scalar.argtypes = [i32, i64, P, P]
         L.oz2o_get_threads.restype = i32
         _lib = L
@@ -382,9 +385,10 @@ def fp64_crt_scalar(s: int, q: int, residues) -> int:
     return _limbs_to_int_wl(X)
 
 
-def fp64_dgemm(A, B, s: int, v: int = 2, want_exponents: bool = False):
+def fp64_dgemm(A, B, s: int, v: int = 2, want_exponents: bool = False, A2=None, B2=None):
     """C ~= A B in the FP64 prime regime with s primes for q = k: v binary64
-    words per entry, returned as [v][m][n] (most significant first, F3)."""
+    words per entry, returned as [v][m][n] (most significant first, F3).
+    A2 / B2: second words of double-word inputs (A = A + A2, reading F6)."""
     A = _as_f64(A)
     B = _as_f64(B)
     m, k = A.shape
@@ -392,7 +396,20 @@ def fp64_dgemm(A, B, s: int, v: int = 2, want_exponents: bool = False):
     C = np.zeros((v, m, n), np.float64)
     e = np.zeros(max(m, 1), np.int32)
     f = np.zeros(max(n, 1), np.int32)
-    _check(lib().oz2f_dgemm(m, n, k, _p(A), k, _p(B), n, s, v, _p(C), n, _p(e), _p(f)))
+    if A2 is None and B2 is None:
+        _check(lib().oz2f_dgemm(m, n, k, _p(A), k, _p(B), n, s, v, _p(C), n, _p(e), _p(f)))
+    else:
+        A2 = _as_f64(A2) if A2 is not None else None
+        B2 = _as_f64(B2) if B2 is not None else None
+        _check(lib().oz2f_dgemm_mw(m, n, k, _p(A), _p(A2) if A2 is not None else None, k, _p(B),
+                                   _p(B2) if B2 is not None else None, n, s, v, _p(C), n, _p(e), _p(f)))
     if want_exponents:
         return C, e[:m], f[:n]
     return C
+
+
+def fp64_scaled_trunc_mw(a1: float, a2: float, e: int) -> int:
+    """Reading F6 for one element: trunc(2^e (a1 + a2))."""
+    out = np.zeros(FP64_WL, np.uint64)
+    lib().oz2f_scaled_trunc_mw(float(a1), float(a2), int(e), _p(out))
+    return _limbs_to_int_wl(out)

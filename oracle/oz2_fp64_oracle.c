@@ -20,6 +20,9 @@
  *      multi-word format): w_1 = RN(X), w_2 = RN(X - w_1), ... then scaled.
  *  F4  s in [2, 22] (T <= 241 < 256 keeps A' in the 256-bit path of the
  *      residue code; M < 2^484 fits the 640-bit integers with room for S).
+ *  F6  double-word inputs A = A1 + A2 with |A2| <= u |A1| (Eqs. 22-23): line 1
+ *      on |A1| + |A2| rounded up; x' = trunc(2^e (a1 + a2)) exactly
+ *      (scaled_trunc_mw).
  *
  * Build: compiled with oz2_oracle.c into liboz2_oracle.so (oracle/__init__.py).
  */
@@ -153,35 +156,77 @@ static void crt_words(const fconsts_t* c, const int64_t* cp, int32_t e, int32_t 
     }
 }
 
+/* |a1| + |a2| rounded upward (an upper bound of |a1 + a2|): TwoSum, then one
+ * step up when the rounded sum fell below the exact one                       */
+static double abs_sum_up(double a1, double a2) {
+    const double x = fabs(a1), y = fabs(a2);
+    const double s = x + y, bb = s - x, err = (x - (s - bb)) + (y - bb);
+    return err > 0 ? nextafter(s, INFINITY) : s;
+}
+
+/* Reading F6 (multi-word inputs, Eqs. 22-23): x' = trunc(2^e (x1 + x2)) exactly,
+ * for |x2| <= u |x1| (so the sum has the sign of x1).  Plainly: if |2^e x1| < 1
+ * the truncation is 0; otherwise 2^e x1 has no bits below 2^-52, and
+ * X = 2^128 (2^e x1) + R(2^128 2^e x2) is an exact integer with R = floor for
+ * x1 > 0 and ceil for x1 < 0 -- rounding x2 on the 2^-128 grid toward the side
+ * that keeps floor (resp. ceil) of the sum -- and x' = trunc(X / 2^128).  A
+ * scaled second word of magnitude below 2^-64 (or underflowing) acts only
+ * through its sign and is taken as +-2^-64.                                    */
+static wide_t scaled_trunc_mw(double a1, double a2, int e) {
+    const double x1 = ldexp(a1, e);
+    if (fabs(x1) < 1.0) return w_from_i64(0);
+    double x2 = ldexp(a2, e);
+    if (a2 != 0.0 && fabs(x2) < 0x1p-64) x2 = copysign(0x1p-64, a2);
+    const double g = ldexp(x2, 128);
+    const double gr = x1 > 0 ? floor(g) : ceil(g);
+    const wide_t X = w_add(w_from_double(ldexp(x1, 128)), w_from_double(gr));
+    return w_is_neg(X) ? w_neg(w_shr(w_neg(X), 128)) : w_shr(X, 128);
+}
+
 /* The whole product in the FP64 prime regime: C (v words [v][m][n], word plane
  * stride m*ldc) ~= A B, A m x k (lda), B k x n (ldb), row-major, s primes for
- * q = k.  e_out / f_out optional.                                              */
-int oz2f_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B, int64_t ldb,
-               int s, int v, double* C, int64_t ldc, int32_t* e_out, int32_t* f_out) {
+ * q = k.  A2 / B2 (NULL or the second words of double-word inputs, same
+ * layout, reading F6).  e_out / f_out optional.                               */
+int oz2f_dgemm_mw(int64_t m, int64_t n, int64_t k, const double* A, const double* A2, int64_t lda,
+                  const double* B, const double* B2, int64_t ldb, int s, int v, double* C, int64_t ldc,
+                  int32_t* e_out, int32_t* f_out) {
     if (m < 0 || n < 0 || k < 1 || v < 1 || v > 4) return OZ2F_ERR_ARG;
     fconsts_t c; int rc = make_fconsts(s, k, &c); if (rc) return rc;
     int32_t* e = (int32_t*)malloc(sizeof(int32_t) * (m ? m : 1));
     int32_t* f = (int32_t*)malloc(sizeof(int32_t) * (n ? n : 1));
-    /* line 1 (F2): OS II-fast with this regime's T */
+    /* line 1 (F2, F6): OS II-fast with this regime's T, on |x1| + |x2| rounded up */
+    double* Ab = (double*)malloc(sizeof(double) * (size_t)(m * k ? m * k : 1));
+    double* Bb = (double*)malloc(sizeof(double) * (size_t)(n * k ? n * k : 1));
+    for (int64_t i = 0; i < m; i++)
+        for (int64_t l = 0; l < k; l++)
+            Ab[i * k + l] = A2 ? abs_sum_up(A[i * lda + l], A2[i * lda + l]) : A[i * lda + l];
+    for (int64_t l = 0; l < k; l++)
+        for (int64_t j = 0; j < n; j++)
+            Bb[l * n + j] = B2 ? abs_sum_up(B[l * ldb + j], B2[l * ldb + j]) : B[l * ldb + j];
     #pragma omp parallel for schedule(dynamic, 16)
-    for (int64_t i = 0; i < m; i++) e[i] = fast_exponent_one(k, A + i * lda, 1, c.T);
+    for (int64_t i = 0; i < m; i++) e[i] = fast_exponent_one(k, Ab + i * k, 1, c.T);
     #pragma omp parallel for schedule(dynamic, 16)
-    for (int64_t j = 0; j < n; j++) f[j] = fast_exponent_one(k, B + j, ldb, c.T);
+    for (int64_t j = 0; j < n; j++) f[j] = fast_exponent_one(k, Bb + j, n, c.T);
+    free(Ab); free(Bb);
     /* lines 2-5: A' = trunc(D A), residues A'_t = A' mod m_t (Eq. 1), as int64 */
     int64_t* Ar = (int64_t*)malloc(sizeof(int64_t) * (size_t)s * (size_t)(m * k ? m * k : 1));
     int64_t* Br = (int64_t*)malloc(sizeof(int64_t) * (size_t)s * (size_t)(n * k ? n * k : 1));
     #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < m; i++)
         for (int64_t l = 0; l < k; l++) {
-            const double x = e[i] == OZ2O_EXP_NONFINITE ? 0.0 : trunc(ldexp(A[i * lda + l], e[i]));
-            const wide_t xw = w_from_double(x);
+            wide_t xw;
+            if (e[i] == OZ2O_EXP_NONFINITE) xw = w_from_i64(0);
+            else if (A2) xw = scaled_trunc_mw(A[i * lda + l], A2[i * lda + l], e[i]);
+            else xw = w_from_double(trunc(ldexp(A[i * lda + l], e[i])));
             for (int t = 0; t < s; t++) Ar[((int64_t)t * m + i) * k + l] = (int64_t)w_smod_small(xw, c.m[t]).l[0];
         }
     #pragma omp parallel for schedule(static)
     for (int64_t j = 0; j < n; j++)
         for (int64_t l = 0; l < k; l++) {
-            const double x = f[j] == OZ2O_EXP_NONFINITE ? 0.0 : trunc(ldexp(B[l * ldb + j], f[j]));
-            const wide_t xw = w_from_double(x);
+            wide_t xw;
+            if (f[j] == OZ2O_EXP_NONFINITE) xw = w_from_i64(0);
+            else if (B2) xw = scaled_trunc_mw(B[l * ldb + j], B2[l * ldb + j], f[j]);
+            else xw = w_from_double(trunc(ldexp(B[l * ldb + j], f[j])));
             for (int t = 0; t < s; t++) Br[((int64_t)t * n + j) * k + l] = (int64_t)w_smod_small(xw, c.m[t]).l[0];
         }
     /* line 6: C'_t = A'_t B'_t exactly (int64: |.| <= k (m_t/2)^2 <= 2^53, Eq. 20) */
@@ -207,6 +252,11 @@ int oz2f_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, co
     return OZ2F_OK;
 }
 
+int oz2f_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B, int64_t ldb,
+               int s, int v, double* C, int64_t ldc, int32_t* e_out, int32_t* f_out) {
+    return oz2f_dgemm_mw(m, n, k, A, NULL, lda, B, NULL, ldb, s, v, C, ldc, e_out, f_out);
+}
+
 /* Eq. (8) + line 9 for one element (tests): X = (sum_t c_t w_t) mod M as WL limbs */
 int oz2f_crt_scalar(int s, int64_t q, const int64_t* cres, uint64_t* X_limbs) {
     fconsts_t c; int rc = make_fconsts(s, q, &c); if (rc) return rc;
@@ -215,4 +265,10 @@ int oz2f_crt_scalar(int s, int64_t q, const int64_t* cres, uint64_t* X_limbs) {
     wide_t X = w_smod(S, c.M);
     for (int i = 0; i < WL; i++) X_limbs[i] = X.l[i];
     return OZ2F_OK;
+}
+
+/* reading F6 for one element (tests): trunc(2^e (a1 + a2)) as WL limbs */
+void oz2f_scaled_trunc_mw(double a1, double a2, int e, uint64_t* limbs) {
+    const wide_t x = scaled_trunc_mw(a1, a2, e);
+    for (int i = 0; i < WL; i++) limbs[i] = x.l[i];
 }

@@ -1062,6 +1062,12 @@ size_t oz2_fp64mod_workspace_bytes(int64_t m, int64_t n, int64_t k, int s) {
 
 int oz2_dgemm_fp64mod(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
                       const double* B, int64_t ldb, int s, int v, double* C, int64_t ldc, int64_t strideC) {
+    return oz2_dgemm_fp64mod_dw(h, m, n, k, A, nullptr, lda, B, nullptr, ldb, s, v, C, ldc, strideC);
+}
+
+int oz2_dgemm_fp64mod_dw(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, const double* A2,
+                         int64_t lda, const double* B, const double* B2, int64_t ldb, int s, int v, double* C,
+                         int64_t ldc, int64_t strideC) {
     if (!h) return OZ2_ERR_INVALID_ARG;
     if (s < 2 || s > oz2::F64_MAX_S) return OZ2_ERR_NUM_MODULI;
     if (m < 0 || n < 0 || k < 0 || v < 1 || v > 4) return OZ2_ERR_INVALID_ARG;
@@ -1080,7 +1086,8 @@ int oz2_dgemm_fp64mod(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const dou
     uint8_t* ws;
     int rc;
     if ((rc = get_workspace(h, oz2::f64_workspace_bytes(m, n, k, s), &ws))) return rc;
-    const int r = oz2::launch_fp64mod(h->device, A, m, k, lda, B, n, ldb, s, v, C, ldc, strideC, ws, h->stream);
+    const int r = oz2::launch_fp64mod(h->device, A, A2, m, k, lda, B, B2, n, ldb, s, v, C, ldc, strideC, ws,
+                                      h->stream);
     if (r == -1) return OZ2_ERR_INVALID_ARG;
     if (r) return OZ2_ERR_CUDA;
     return cuda_status();

@@ -153,10 +153,38 @@ __device__ __forceinline__ double mod_small(double a, double m, double minv) {
     return r;
 }
 
+// reading F6 (double-word inputs, Eqs. 22-23): for x1 = 2^e a1, x2 = 2^e a2
+// with |x2| <= u |x1|, trunc(x1 + x2) = trunc(x1) + adj, where f1 = x1 -
+// trunc(x1) is exact, (s, t) = TwoSum(f1, x2) is the exact sum f1 + x2, and adj
+// = floor(s + t) (x1 > 0) or ceil(s + t) (x1 < 0), in {-2, ..., 1} / {-1, ..., 2};
+// a scaled second word below 2^-64 acts only through its sign (+-2^-64)
+__device__ __forceinline__ double trunc_adj_mw(double x1, double x2) {
+    if (x2 != 0.0 && fabs(x2) < 0x1p-64) x2 = copysign(0x1p-64, x2);
+    const double f1 = x1 - trunc(x1);
+    const double s = f1 + x2, bb = s - f1, t = (f1 - (s - bb)) + (x2 - bb);
+    if (x1 > 0.0) return floor(s) - ((s == floor(s) && t < 0.0) ? 1.0 : 0.0);
+    if (x1 < 0.0) return ceil(s) + ((s == ceil(s) && t > 0.0) ? 1.0 : 0.0);
+    return 0.0;
+}
+
+// |a1| + |a2| rounded upward (line 1 of double-word inputs, reading F6), into a
+// packed R x C matrix
 __global__ void __launch_bounds__(256)
-fp64mod_residues_kernel(const double* __restrict__ X, int64_t R, int64_t Cc, int64_t ld, int is_cols,
-                        const int32_t* __restrict__ ex, const uint32_t* __restrict__ pow2tab,
-                        double* __restrict__ out, const __grid_constant__ F64Tab T) {
+fp64mod_abs_sum_up_kernel(const double* __restrict__ X, const double* __restrict__ X2, int64_t R, int64_t Cc,
+                          int64_t ld, double* __restrict__ out) {
+    const int64_t total = R * Cc;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = idx / Cc, c = idx % Cc;
+        out[idx] = __dadd_ru(fabs(X[r * ld + c]), fabs(X2[r * ld + c]));
+    }
+}
+
+__global__ void __launch_bounds__(256)
+fp64mod_residues_kernel(const double* __restrict__ X, const double* __restrict__ X2, int64_t R, int64_t Cc,
+                        int64_t ld, int is_cols, const int32_t* __restrict__ ex,
+                        const uint32_t* __restrict__ pow2tab, double* __restrict__ out,
+                        const __grid_constant__ F64Tab T) {
     // 2^j mod m_t for j < F64_POW2 (host table): |x| < 2^(T + 1), x = mant 2^sh, sh <= T - 52
     __shared__ float p2[F64_MAX_S][F64_POW2];            // values < 2^22: exact in binary32
     for (int x = threadIdx.x; x < T.s * F64_POW2; x += blockDim.x)
@@ -167,8 +195,12 @@ fp64mod_residues_kernel(const double* __restrict__ X, int64_t R, int64_t Cc, int
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = idx / Cc, c = idx % Cc;
         const int e = ex[is_cols ? c : r];
-        double x = 0.0;
-        if (e != OZ2_EXP_NONFINITE_DEV) x = trunc(scale_pow2(X[r * ld + c], e));   // Alg. 1 lines 2-3
+        double x = 0.0, adj = 0.0;
+        if (e != OZ2_EXP_NONFINITE_DEV) {
+            const double x1 = scale_pow2(X[r * ld + c], e);
+            x = trunc(x1);                                              // Alg. 1 lines 2-3
+            if (X2) adj = trunc_adj_mw(x1, scale_pow2(X2[r * ld + c], e));
+        }
         // |x| = mant 2^sh exactly, mant < 2^53 an integer (sh = 0 when |x| < 2^53)
         const uint64_t bits = (uint64_t)__double_as_longlong(x);
         const int bexp = (int)((bits >> 52) & 0x7ff);
@@ -187,6 +219,7 @@ fp64mod_residues_kernel(const double* __restrict__ X, int64_t R, int64_t Cc, int
             const double mt = T.md[t], mi = T.minv[t];
             double rr = mod_small(mod_small(mant, mt, mi) * (double)p2[t][sh], mt, mi);   // |x| mod m_t
             if (neg && rr != 0.0) rr = mt - rr;                                          // x mod m_t
+            if (adj != 0.0) rr = mod_small(rr + adj + mt, mt, mi);                       // + adj (F6)
             out[(int64_t)t * plane + idx] = rr > 0.5 * (mt - 1.0) ? rr - mt : rr;        // Eq. (1), m_t odd
         }
     }
@@ -414,6 +447,7 @@ int f64_tables(int s, int64_t q, int64_t* moduli, uint32_t* M_words, int32_t* L,
 size_t f64_workspace_bytes(int64_t m, int64_t n, int64_t k, int s) {
     auto r = [](size_t b) { return (b + 255) / 256 * 256; };
     return r((size_t)s * 8 * (size_t)(m * k)) + r((size_t)s * 8 * (size_t)(k * n)) + r((size_t)s * 8 * (size_t)(m * n)) +
+           r(8 * (size_t)(m * k)) + r(8 * (size_t)(k * n)) +                     // double-word bounds (F6)
            2 * r(4 * (size_t)(m > 0 ? m : 1)) + 2 * r(4 * (size_t)(n > 0 ? n : 1)) + r(8 * (size_t)(m > 0 ? m : 1)) +
            r(8 * (size_t)(n > 0 ? n : 1)) + r(cols_stats_bytes(k, n)) + r(4 * (size_t)s * F64_POW2) + 256;
 }
@@ -426,9 +460,9 @@ static void launch_crt_nw(const double* Cp, int64_t m, int64_t n, const int32_t*
     (fp64mod_crt_kernel<NW><<<g, 128, 0, st>>>(Cp, m, n, e, f, v, C, ldc, strideC, T), count_launch());
 }
 
-int launch_fp64mod(int device, const double* A, int64_t m, int64_t k, int64_t lda, const double* B, int64_t n,
-                   int64_t ldb, int s, int v, double* C, int64_t ldc, int64_t strideC, uint8_t* ws,
-                   cudaStream_t st) {
+int launch_fp64mod(int device, const double* A, const double* A2, int64_t m, int64_t k, int64_t lda,
+                   const double* B, const double* B2, int64_t n, int64_t ldb, int s, int v, double* C, int64_t ldc,
+                   int64_t strideC, uint8_t* ws, cudaStream_t st) {
     F64Tab T;
     if (build_f64tab(s, k, &T)) return -1;
     if (cublas_ready(device)) return -2;
@@ -451,22 +485,39 @@ int launch_fp64mod(int device, const double* A, int64_t m, int64_t k, int64_t ld
     unsigned long long* SB = (unsigned long long*)take(8 * (size_t)(n > 0 ? n : 1));
     void* stats = take(cols_stats_bytes(k, n));
     uint32_t* p2d = (uint32_t*)take(sizeof(uint32_t) * pow2tab.size());
+    double* Abar = A2 ? (double*)take(sizeof(double) * (size_t)m * k) : nullptr;
+    double* Bbar = B2 ? (double*)take(sizeof(double) * (size_t)k * n) : nullptr;
     if (cudaMemcpyAsync(p2d, pow2tab.data(), sizeof(uint32_t) * pow2tab.size(), cudaMemcpyHostToDevice, st) !=
         cudaSuccess)
         return -4;
-    // line 1 (reading F2): FAST statistics (phase 1: max chunk exponents; phase 2: sums), then e, f with T
-    launch_kslice_rows(A, m, k, lda, 0, nullptr, EA, nullptr, st);
-    launch_kslice_rows(A, m, k, lda, 0, EA, nullptr, SA, st);
-    launch_kslice_cols(B, k, n, ldb, 0, nullptr, EB, nullptr, stats, st);
-    launch_kslice_cols(B, k, n, ldb, 0, EB, nullptr, SB, stats, st);
+    // line 1 (reading F2): FAST statistics (phase 1: max chunk exponents; phase 2: sums), then e, f with T;
+    // double-word inputs (F6): the statistics of |x1| + |x2| rounded up
+    const double* As = A;
+    int64_t ldas = lda;
+    const double* Bs = B;
+    int64_t ldbs = ldb;
+    if (A2) {
+        const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m * k + 255) / 256, 148 * 8));
+        (fp64mod_abs_sum_up_kernel<<<g, 256, 0, st>>>(A, A2, m, k, lda, Abar), count_launch());
+        As = Abar; ldas = k;
+    }
+    if (B2) {
+        const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((k * n + 255) / 256, 148 * 8));
+        (fp64mod_abs_sum_up_kernel<<<g, 256, 0, st>>>(B, B2, k, n, ldb, Bbar), count_launch());
+        Bs = Bbar; ldbs = n;
+    }
+    launch_kslice_rows(As, m, k, ldas, 0, nullptr, EA, nullptr, st);
+    launch_kslice_rows(As, m, k, ldas, 0, EA, nullptr, SA, st);
+    launch_kslice_cols(Bs, k, n, ldbs, 0, nullptr, EB, nullptr, stats, st);
+    launch_kslice_cols(Bs, k, n, ldbs, 0, EB, nullptr, SB, stats, st);
     launch_exponents_T(EA, SA, m, T.T, e, st);
     launch_exponents_T(EB, SB, n, T.T, f, st);
     // lines 2-5
     {
         const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m * k + 255) / 256, 148 * 8));
-        (fp64mod_residues_kernel<<<g, 256, 0, st>>>(A, m, k, lda, 0, e, p2d, Ares, T), count_launch());
+        (fp64mod_residues_kernel<<<g, 256, 0, st>>>(A, A2, m, k, lda, 0, e, p2d, Ares, T), count_launch());
         const unsigned g2 = (unsigned)std::max<int64_t>(1, std::min<int64_t>((k * n + 255) / 256, 148 * 8));
-        (fp64mod_residues_kernel<<<g2, 256, 0, st>>>(B, k, n, ldb, 1, f, p2d, Bres, T), count_launch());
+        (fp64mod_residues_kernel<<<g2, 256, 0, st>>>(B, B2, k, n, ldb, 1, f, p2d, Bres, T), count_launch());
     }
     // line 6: C'_t = A'_t B'_t on the FP64 tensor cores, exact (Eq. 20); row-major
     // C (m x n) = A B  <=>  column-major C^T = B^T A^T

@@ -116,9 +116,10 @@ int f64_prime_bits(int64_t q);
 int f64_tables(int s, int64_t q, int64_t* moduli, uint32_t* M_words, int32_t* L, int32_t* T);
 size_t f64_workspace_bytes(int64_t m, int64_t n, int64_t k, int s);
 // 0 ok, -1 bad (s, k), -2 cuBLAS unavailable, -3 cuBLAS error, -4 CUDA error
-int launch_fp64mod(int device, const double* A, int64_t m, int64_t k, int64_t lda, const double* B, int64_t n,
-                   int64_t ldb, int s, int v, double* C, int64_t ldc, int64_t strideC, uint8_t* ws,
-                   cudaStream_t st);
+// A2, B2: NULL or the second words of double-word inputs (reading F6)
+int launch_fp64mod(int device, const double* A, const double* A2, int64_t m, int64_t k, int64_t lda,
+                   const double* B, const double* B2, int64_t n, int64_t ldb, int s, int v, double* C, int64_t ldc,
+                   int64_t strideC, uint8_t* ws, cudaStream_t st);
 void launch_exponents_T(const int32_t* E, const unsigned long long* S, int64_t cnt, int T, int32_t* e,
                         cudaStream_t st);
 

@@ -36,7 +36,7 @@ SYMBOLS = [
     "oz2_dgemm_prep2", "oz2_reprepare", "oz2_release", "oz2_certify", "oz2_set_certify", "oz2_status",
     "oz2_set_sm_limit", "oz2_kslice_stats_rows", "oz2_kslice_stats_cols", "oz2_exponents_from_stats",
     "oz2_modmul_residues", "oz2_crt_sum", "oz2_dsyrk", "oz2_dtrmm", "oz2_kernel_launches",
-    "oz2_dgemm_fp64mod", "oz2_fp64mod_workspace_bytes", "oz2_fp64mod_tables",
+    "oz2_dgemm_fp64mod", "oz2_dgemm_fp64mod_dw", "oz2_fp64mod_workspace_bytes", "oz2_fp64mod_tables",
 ]
 OP_N, OP_T = 0, 1
 # stage 0 times A's conversion (and B's too with OZ2_CONV_OVERLAP=1; the two column
@@ -115,6 +115,7 @@ def lib() -> ctypes.CDLL:
                 L.oz2_set_profiling.argtypes = [P, i32]
                 L.oz2_stage_times.argtypes = [P, P, P]
                 L.oz2_dgemm_fp64mod.argtypes = [P, i64, i64, i64, P, i64, P, i64, i32, i32, P, i64, i64]
+                L.oz2_dgemm_fp64mod_dw.argtypes = [P, i64, i64, i64, P, P, i64, P, P, i64, i32, i32, P, i64, i64]
                 L.oz2_fp64mod_workspace_bytes.argtypes = [i64, i64, i64, i32]
                 L.oz2_fp64mod_workspace_bytes.restype = sz
                 L.oz2_fp64mod_tables.argtypes = [i32, i64, P, P, P, P]
@@ -788,14 +789,21 @@ def fp64mod_tables(s: int, q: int) -> dict:
             "L": L.value, "T": T.value}
 
 
-def dgemm_fp64mod(A, B, s: int = 16, v: int = 2, out=None):
+def dgemm_fp64mod(A, B, s: int = 16, v: int = 2, out=None, A2=None, B2=None):
     """C ~= A @ B in the FP64 prime-modulus regime with s primes: a (v, m, n)
-    float64 tensor, word 0 the most significant (oz2_dgemm_fp64mod)."""
+    float64 tensor, word 0 the most significant (oz2_dgemm_fp64mod).  A2, B2:
+    second words of double-word inputs (A + A2, B + B2; |A2| <= u |A|, Eq. 23)."""
     import torch
 
-    A = _rowmajor(A, torch.float64)
-    B = _rowmajor(B, torch.float64)
-    _same_device(A.device, B)
+    A = _rowmajor(A, torch.float64).contiguous()
+    B = _rowmajor(B, torch.float64).contiguous()
+    _same_device(A.device, B, A2, B2)
+    if A2 is not None:
+        A2 = A2.to(torch.float64).contiguous()
+        assert A2.shape == A.shape
+    if B2 is not None:
+        B2 = B2.to(torch.float64).contiguous()
+        assert B2.shape == B.shape
     m, k = A.shape
     k2, n = B.shape
     if k != k2:
@@ -807,6 +815,6 @@ def dgemm_fp64mod(A, B, s: int = 16, v: int = 2, out=None):
         raise ValueError(f"out must be a contiguous float64 ({v}, {m}, {n}) tensor on {A.device}")
     h = handle(A.device.index)
     h.prepare("fast", int(lib().oz2_fp64mod_workspace_bytes(m, n, max(k, 1), s)))
-    _check(lib().oz2_dgemm_fp64mod(h.ptr, m, n, k, _vp(A), _ld(A), _vp(B), _ld(B), s, v, _vp(out), max(1, n),
-                                   m * max(1, n)), "oz2_dgemm_fp64mod")
+    _check(lib().oz2_dgemm_fp64mod_dw(h.ptr, m, n, k, _vp(A), _vp(A2), _ld(A), _vp(B), _vp(B2), _ld(B), s, v,
+                                      _vp(out), max(1, n), m * max(1, n)), "oz2_dgemm_fp64mod_dw")
     return out

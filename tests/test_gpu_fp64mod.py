@@ -126,3 +126,26 @@ def test_fp64mod_products_exact_at_the_eq20_bound(oz2, oracle):
     B = A[:48].T.copy()
     got = oz2.dgemm_fp64mod(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), s, v).cpu().numpy()
     _bitwise(got, oracle.fp64_dgemm(A, B, s, v), "fp64mod at the Eq. 20 bound")
+
+
+@pytest.mark.parametrize("m,n,k,s,v", [(40, 50, 300, 16, 3), (65, 33, 1024, 22, 4), (20, 20, 64, 8, 2)])
+def test_fp64mod_double_word_inputs(oz2, oracle, m, n, k, s, v):
+    """Double-word inputs (Eqs. 22-23, reading F6): A + A2, B + B2 with |A2| <=
+    u |A|; every output word bitwise vs the oracle, which truncates the exact
+    sum on a 2^-128 grid (the GPU uses trunc(x1) + an exact TwoSum adjustment).
+    Includes integral first words with tiny second words of the other sign and
+    second words that underflow when scaled."""
+    rng = np.random.Generator(np.random.PCG64(m + n + k))
+    A = phi_matrix_np(m, k, 1.0, seed=931 + m)
+    B = phi_matrix_np(k, n, 1.0, seed=932 + n)
+    A2 = A * 2.0 ** -53 * rng.uniform(-1, 1, A.shape)
+    B2 = B * 2.0 ** -53 * rng.uniform(-1, 1, B.shape)
+    A[0, :8] = np.round(A[0, :8] * 2.0 ** 40)          # integral after scaling, tiny opposite second words
+    A2[0, :8] = -np.sign(A[0, :8]) * 1e-300
+    A2[1, :4] = 5e-324 * np.sign(A[1, :4])
+    B2[:, 0] = 0.0
+    Ad, Bd = torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV)
+    got = oz2.dgemm_fp64mod(Ad, Bd, s, v, A2=torch.from_numpy(A2).to(DEV), B2=torch.from_numpy(B2).to(DEV))
+    _bitwise(got.cpu().numpy(), oracle.fp64_dgemm(A, B, s, v, A2=A2, B2=B2), f"double-word s={s} v={v}")
+    one = oz2.dgemm_fp64mod(Ad, Bd, s, v, A2=torch.zeros_like(Ad))         # A2 = 0: the single-word result
+    _bitwise(one.cpu().numpy(), oracle.fp64_dgemm(A, B, s, v), "A2 = 0")

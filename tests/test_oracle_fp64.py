@@ -148,3 +148,49 @@ def test_error_falls_with_s(oracle):
         errs.append(err)
     assert all(b < a for a, b in zip(errs, errs[1:]) if a > 2.0**-100), errs
     assert errs[0] > 2.0**-60 and errs[-1] < 2.0**-100, errs
+
+
+def _trunc_fraction(x: Fraction) -> int:
+    return math.floor(x) if x >= 0 else math.ceil(x)
+
+
+def test_double_word_scaled_trunc(oracle):
+    """Reading F6 (Eqs. 22-23): trunc(2^e (a1 + a2)) equals the truncation of the
+    exact rational sum, including sums that sit on an integer with a tiny second
+    word of the other sign and second words that underflow when scaled."""
+    import random
+    rng = random.Random(7)
+    u = 2.0 ** -53
+    cases = []
+    for _ in range(3000):
+        a1 = rng.uniform(-1, 1) * 2.0 ** rng.randint(-30, 30)
+        a2 = a1 * u * rng.uniform(-1, 1)
+        cases.append((a1, a2, rng.randint(-40, 120)))
+    for n in (1.0, 5.0, -7.0, 2.0 ** 60, -(2.0 ** 70) - 2.0 ** 18):   # integral x1, tiny opposite x2
+        for a2 in (-1e-300, 1e-300, -5e-324, 5e-324, -(2.0 ** -80), 2.0 ** -80, 0.0):
+            cases.append((n, a2, 0))
+            cases.append((n * 0.5, a2, 1))
+    cases.append((3.0, -1e-310, -1000))                                  # scaled a1 < 1: 0
+    cases.append((2.0 ** 100, -(2.0 ** 47), 50))                         # |a2| = u |a1|
+    for a1, a2, e in cases:
+        exact = (Fraction(a1) + Fraction(a2)) * Fraction(2) ** e
+        assert oracle.fp64_scaled_trunc_mw(a1, a2, e) == _trunc_fraction(exact), (a1, a2, e)
+
+
+@pytest.mark.parametrize("s,v", [(16, 3), (22, 4)])
+def test_double_word_inputs_exact_multiword(oracle, s, v):
+    """Double-word inputs whose words need no truncation (short mantissas, small
+    exponent range): the result is the exactly rounded v-word expansion of
+    (A1 + A2)(B1 + B2)."""
+    A1 = dyadic_matrix_np(5, 64, 20, 20, seed=11)
+    B1 = dyadic_matrix_np(64, 4, 20, 20, seed=12)
+    A2 = dyadic_matrix_np(5, 64, 20, 20, seed=13) * 2.0 ** -60
+    B2 = dyadic_matrix_np(64, 4, 20, 20, seed=14) * 2.0 ** -60
+    A2 = np.where(np.abs(A2) <= np.abs(A1) * 2.0 ** -53, A2, 0.0)         # Eq. (23)
+    B2 = np.where(np.abs(B2) <= np.abs(B1) * 2.0 ** -53, B2, 0.0)
+    C = oracle.fp64_dgemm(A1, B1, s, v, A2=A2, B2=B2)
+    for i in range(5):
+        for j in range(4):
+            ab = sum((Fraction(a) + Fraction(a2)) * (Fraction(b) + Fraction(b2))
+                     for a, a2, b, b2 in zip(A1[i], A2[i], B1[:, j], B2[:, j]))
+            assert C[:, i, j].tolist() == _words_exact(ab, v), (i, j)
