@@ -201,25 +201,31 @@ fp64mod_residues_kernel(const double* __restrict__ X, const double* __restrict__
             x = trunc(x1);                                              // Alg. 1 lines 2-3
             if (X2) adj = trunc_adj_mw(x1, scale_pow2(X2[r * ld + c], e));
         }
-        // |x| = mant 2^sh exactly, mant < 2^53 an integer (sh = 0 when |x| < 2^53)
-        const uint64_t bits = (uint64_t)__double_as_longlong(x);
-        const int bexp = (int)((bits >> 52) & 0x7ff);
-        double mant;
-        int sh;
-        if (bexp >= 1023 + 53) {
-            mant = (double)((bits & 0xfffffffffffffull) | (1ull << 52));
-            sh = bexp - 1075;
-        } else {
-            mant = fabs(x);
-            sh = 0;
-        }
-        const bool neg = x < 0.0;
+        // residues of the integral doubles x (and adj, reading F6: adj may be as large
+        // as u |x1|) from |v| = mant 2^sh, mant < 2^53 an integer (sh = 0 when |v| < 2^53)
         #pragma unroll 1
         for (int t = 0; t < T.s; t++) {
             const double mt = T.md[t], mi = T.minv[t];
-            double rr = mod_small(mod_small(mant, mt, mi) * (double)p2[t][sh], mt, mi);   // |x| mod m_t
-            if (neg && rr != 0.0) rr = mt - rr;                                          // x mod m_t
-            if (adj != 0.0) rr = mod_small(rr + adj + mt, mt, mi);                       // + adj (F6)
+            double rr = 0.0;
+            #pragma unroll
+            for (int part = 0; part < 2; part++) {
+                const double vv = part == 0 ? x : adj;
+                if (vv == 0.0) continue;
+                const uint64_t bits = (uint64_t)__double_as_longlong(vv);
+                const int bexp = (int)((bits >> 52) & 0x7ff);
+                double mant;
+                int sh;
+                if (bexp >= 1023 + 53) {
+                    mant = (double)((bits & 0xfffffffffffffull) | (1ull << 52));
+                    sh = bexp - 1075;
+                } else {
+                    mant = fabs(vv);
+                    sh = 0;
+                }
+                double r = mod_small(mod_small(mant, mt, mi) * (double)p2[t][sh], mt, mi);   // |v| mod m_t
+                if (vv < 0.0 && r != 0.0) r = mt - r;                                       // v mod m_t
+                rr = mod_small(rr + r, mt, mi);
+            }
             out[(int64_t)t * plane + idx] = rr > 0.5 * (mt - 1.0) ? rr - mt : rr;        // Eq. (1), m_t odd
         }
     }
