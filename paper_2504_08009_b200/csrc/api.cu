@@ -11,6 +11,8 @@
 #include <new>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/oz2.h"
 #include "oz2_device.cuh"
 #include "oz2_kernels.h"
@@ -81,6 +83,13 @@ int host_L(int N) {
     return g_tabs[N].L;
 }
 }  // namespace oz2
+
+// NVTX ranges (SURVEY section 5 tracing): one per public entry point, named after
+// it; free when no tool is attached (nvtx3 is header-only and dormant)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct oz2_context {
     int device;
@@ -408,6 +417,7 @@ int oz2_status(oz2_handle_t h) {
 
 int oz2_certify(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
                 int64_t ldb, const int32_t* e, const int32_t* f, int N, int32_t* beta) {
+    NvtxRange nvtx_("oz2_certify");
     if (!h) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(m, n, k, N);
     if (rc) return rc;
@@ -463,6 +473,7 @@ size_t oz2_workspace_bytes(int64_t m, int64_t n, int64_t k, int N) {
 // split API
 // ---------------------------------------------------------------------------
 int oz2_scale_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda, int N, int32_t* e) {
+    NvtxRange nvtx_("oz2_scale_rows");
     if (!h || h->mode == OZ2_MODE_ACCU) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(m, 1, k, N);
     if (rc) return rc;
@@ -475,6 +486,7 @@ int oz2_scale_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_
 }
 
 int oz2_scale_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb, int N, int32_t* f) {
+    NvtxRange nvtx_("oz2_scale_cols");
     if (!h || h->mode == OZ2_MODE_ACCU) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(1, n, k, N);
     if (rc) return rc;
@@ -490,6 +502,7 @@ int oz2_scale_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_
 
 int oz2_scale_accu(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
                    const double* B, int64_t ldb, int N, int32_t* e, int32_t* f) {
+    NvtxRange nvtx_("oz2_scale_accu");
     if (!h) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(m, n, k, N);
     if (rc) return rc;
@@ -525,6 +538,7 @@ int oz2_trunc_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_
 
 int oz2_residues_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int64_t lda, const int32_t* e,
                       int N, int8_t* Ares, int64_t ld_res) {
+    NvtxRange nvtx_("oz2_residues_rows");
     if (!h) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(m, 1, k, N);
     if (rc) return rc;
@@ -536,6 +550,7 @@ int oz2_residues_rows(oz2_handle_t h, int64_t m, int64_t k, const double* A, int
 
 int oz2_residues_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int64_t ldb, const int32_t* f,
                       int N, int8_t* Bres, int64_t ld_res) {
+    NvtxRange nvtx_("oz2_residues_cols");
     if (!h) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(1, n, k, N);
     if (rc) return rc;
@@ -547,6 +562,7 @@ int oz2_residues_cols(oz2_handle_t h, int64_t k, int64_t n, const double* B, int
 
 int oz2_modmul(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const int8_t* Ares, const int8_t* Bres,
                int64_t ld_res, int N, int32_t* Cprod) {
+    NvtxRange nvtx_("oz2_modmul");
     if (!h) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(m, n, k, N);
     if (rc) return rc;
@@ -569,6 +585,7 @@ int oz2_modmul(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const int8_t* Ar
 
 int oz2_crt(oz2_handle_t h, int64_t m, int64_t n, const int32_t* Cprod, const int32_t* e, const int32_t* f,
             int N, double* C, int64_t ldc, const int32_t* beta) {
+    NvtxRange nvtx_("oz2_crt");
     if (!h) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(m, n, 0, N);
     if (rc) return rc;
@@ -673,6 +690,7 @@ int certify_into(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* 
 int dgemm_core(oz2_handle_t h, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
                int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int N,
                const int32_t* e_given = nullptr, const int32_t* f_given = nullptr, int tri = 0, int kskip = 0) {
+    NvtxRange nvtx_("dgemm_core");
     if (m == 0 || n == 0) return OZ2_OK;
     const bool given = e_given && f_given;
     int rc, kstar = 0;
@@ -942,6 +960,7 @@ int oz2_dgemm_op(oz2_handle_t h, int transA, int transB, int64_t m, int64_t n, i
 
 int oz2_dtrmm(oz2_handle_t h, int side, int uplo, int transA, int diag, int64_t m, int64_t n, double alpha,
               const double* A, int64_t lda, double* B, int64_t ldb, int N) {
+    NvtxRange nvtx_("oz2_dtrmm");
     if (!h) return OZ2_ERR_INVALID_ARG;
     if ((side != OZ2_LEFT && side != OZ2_RIGHT) || (uplo != OZ2_LOWER && uplo != OZ2_UPPER) ||
         (transA != OZ2_OP_N && transA != OZ2_OP_T) || (diag != OZ2_NON_UNIT && diag != OZ2_UNIT))
@@ -975,6 +994,7 @@ int oz2_dtrmm(oz2_handle_t h, int side, int uplo, int transA, int diag, int64_t 
 
 int oz2_dsyrk(oz2_handle_t h, int uplo, int trans, int64_t n, int64_t k, double alpha, const double* A,
               int64_t lda, double beta, double* C, int64_t ldc, int N) {
+    NvtxRange nvtx_("oz2_dsyrk");
     if (!h) return OZ2_ERR_INVALID_ARG;
     if (uplo != OZ2_LOWER && uplo != OZ2_UPPER) return OZ2_ERR_INVALID_ARG;
     if (trans != OZ2_OP_N && trans != OZ2_OP_T) return OZ2_ERR_INVALID_ARG;
@@ -998,6 +1018,7 @@ struct oz2_prepared {
 namespace {
 int prepare_common(oz2_handle_t h, int side, int64_t rows, int64_t k, const double* X, int64_t ld, int N,
                    oz2_prep_t* out) {
+    NvtxRange nvtx_("prepare_common");
     if (!h || !out) return OZ2_ERR_INVALID_ARG;
     *out = nullptr;
     int rc = check_common(rows, rows, k, N);
@@ -1068,6 +1089,7 @@ int oz2_dgemm_fp64mod(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const dou
 int oz2_dgemm_fp64mod_dw(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, const double* A2,
                          int64_t lda, const double* B, const double* B2, int64_t ldb, int s, int v, double* C,
                          int64_t ldc, int64_t strideC) {
+    NvtxRange nvtx_("oz2_dgemm_fp64mod_dw");
     if (!h) return OZ2_ERR_INVALID_ARG;
     if (s < 2 || s > oz2::F64_MAX_S) return OZ2_ERR_NUM_MODULI;
     if (m < 0 || n < 0 || k < 0 || v < 1 || v > 4) return OZ2_ERR_INVALID_ARG;
@@ -1094,6 +1116,7 @@ int oz2_dgemm_fp64mod_dw(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const 
 }
 
 int oz2_reprepare(oz2_handle_t h, oz2_prep_t p, const double* X, int64_t ld) {
+    NvtxRange nvtx_("oz2_reprepare");
     if (!h || !p || p->device != h->device || h->mode != p->mode) return OZ2_ERR_INVALID_ARG;
     const int64_t need_ld = p->side == OZ2_LEFT ? (p->k > 0 ? p->k : 1) : (p->rows > 0 ? p->rows : 1);
     if (ld < need_ld || (p->k > 0 && p->rows > 0 && !X)) return OZ2_ERR_INVALID_ARG;
@@ -1134,6 +1157,7 @@ int oz2_release(oz2_prep_t p) {
 
 int oz2_dgemm_prepared(oz2_handle_t h, oz2_prep_t pb, int64_t m, const double* A, int64_t lda, double* C,
                        int64_t ldc) {
+    NvtxRange nvtx_("oz2_dgemm_prepared");
     if (!h || !pb || pb->side != OZ2_RIGHT || pb->device != h->device || h->mode != pb->mode)
         return OZ2_ERR_INVALID_ARG;
     const int64_t k = pb->k, n = pb->rows;
@@ -1168,6 +1192,7 @@ int oz2_dgemm_prepared(oz2_handle_t h, oz2_prep_t pb, int64_t m, const double* A
 }
 
 int oz2_dgemm_prep2(oz2_handle_t h, oz2_prep_t pa, oz2_prep_t pb, double* C, int64_t ldc) {
+    NvtxRange nvtx_("oz2_dgemm_prep2");
     if (!h || !pa || !pb || pa->side != OZ2_LEFT || pb->side != OZ2_RIGHT || pa->device != h->device ||
         pb->device != h->device || pa->N != pb->N || pa->k != pb->k || pa->mode != pb->mode)
         return OZ2_ERR_INVALID_ARG;
@@ -1226,6 +1251,7 @@ int oz2_exponents_from_stats(oz2_handle_t h, int64_t count, const int32_t* E, co
 
 int oz2_modmul_residues(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const int8_t* Ares, const int8_t* Bres,
                         int64_t ld_res, int N, uint8_t* R, int64_t rows_per_block) {
+    NvtxRange nvtx_("oz2_modmul_residues");
     if (!h) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(m, n, k, N);
     if (rc) return rc;
@@ -1251,6 +1277,7 @@ int oz2_modmul_residues(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const i
 
 int oz2_crt_sum(oz2_handle_t h, int parts, int64_t m, int64_t n, const uint8_t* R, int64_t part_stride,
                 const int32_t* e, const int32_t* f, int N, double* C, int64_t ldc, const int32_t* beta) {
+    NvtxRange nvtx_("oz2_crt_sum");
     if (!h || parts < 1 || parts > (1 << 20)) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(m, n, 0, N);
     if (rc) return rc;
@@ -1285,6 +1312,7 @@ int oz2_dgemm_strided_batched(oz2_handle_t h, int transA, int transB, int64_t m,
                               double alpha, const double* A, int64_t lda, int64_t strideA, const double* B,
                               int64_t ldb, int64_t strideB, double beta, double* C, int64_t ldc,
                               int64_t strideC, int64_t batch, int N) {
+    NvtxRange nvtx_("oz2_dgemm_strided_batched");
     if (!h || batch < 0 || strideA < 0 || strideB < 0 || strideC < 0) return OZ2_ERR_INVALID_ARG;
     int rc = check_op_args(transA, transB, m, n, k, A, lda, B, ldb, C, ldc, N);
     if (rc) return rc;
@@ -1313,6 +1341,7 @@ int oz2_dgemm(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, con
 
 int oz2_dgemm_host(oz2_handle_t h, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
                    const double* B, int64_t ldb, double* C, int64_t ldc, int N) {
+    NvtxRange nvtx_("oz2_dgemm_host");
     if (!h) return OZ2_ERR_INVALID_ARG;
     int rc = check_common(m, n, k, N);
     if (rc) return rc;
