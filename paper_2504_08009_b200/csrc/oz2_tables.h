@@ -40,6 +40,11 @@ struct Oz2Table {
     uint32_t Mh32[OZ2_MAX_WORDS];     // M / 2, same
     float qscale;                     // 2^(32 (WS - 2)) / M (WS >= 2), 1 / M (WS = 1)
     int32_t y[OZ2_MAX_MODULI];        // least positive inverse of M_t mod m_t (host only)
+    // residue kernels, q = rint(y / m_t) on the FP32 pipe: the dp4a addend
+    // 0x4B000000 + G makes y's bits the binary32 2^23 + y (y < 2^20)
+    uint32_t G63f[OZ2_MAX_MODULI];    // 0x4B000000 + G63
+    uint32_t G95f[OZ2_MAX_MODULI];    // 0x4B000000 + G95
+    float invm[OZ2_MAX_MODULI];       // RN_binary32(1 / m_t)
 };
 
 // Fill tabs[2..20]; tabs[0], tabs[1] are zeroed.  Returns 0 on success.

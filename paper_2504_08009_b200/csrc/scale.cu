@@ -59,14 +59,28 @@ __device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
 // one 64-bit multiply-add ((y magic_t + h_t magic_t) >> 32, exact since
 // (y + h_t)(magic_t m_t - 2^32) < 2^32).  The low byte is the int8 residue.
 // ---------------------------------------------------------------------------
+//
+// q = rint(y / m_t) (= floor((y + h_t) / m_t) for odd m_t) is formed on the
+// full-rate FP32 pipe instead of a quarter-rate IMAD.HI (measured on sm_100a,
+// tools/mb/op_rates.cu: IDP, IMAD 2 cycles per warp instruction and SMSP,
+// IMAD.HI 4, FFMA / FADD 1): the dp4a addend carries 0x4B000000, so the bits
+// of y' = 0x4B000000 + y are the binary32 2^23 + y (y < 2^20), f = y' - 2^23
+// is y exactly, and one FMA f * RN(1/m_t) + 1.5 2^23 rounds to 1.5 2^23 +
+// rint(y / m_t): the product's error is below y 2^-24 / m_t < 2^-4 / m_t,
+// while y / m_t lies at least 1 / (2 m_t) from every half-integer (m_t odd).
+// Then y - q m_t = y' + qb (2^32 - m_t) - (0x4B000000 - 0x4B400000 m_t), and
+// that constant is 0 mod 256, so the low byte is the residue.
+// (tools/mb/residue_pipes.cu: 114 vs 145 cycles per warp-element at N = 14,
+// bitwise equal.)
 template <int NM, int WORDS>
 __device__ __forceinline__ uint32_t residue_odd(int t, const uint32_t (&w)[3]) {
     const Oz2Table& T = c_tab[NM];
-    uint32_t y = dp4a_uu(w[0], T.cw[0][t], WORDS == 2 ? T.G63[t] : T.G95[t]);
+    uint32_t y = dp4a_uu(w[0], T.cw[0][t], WORDS == 2 ? T.G63f[t] : T.G95f[t]);
     y = dp4a_uu(w[1], T.cw[1][t], y);
     if (WORDS == 3) y = dp4a_uu(w[2], T.cw[2][t], y);
-    const uint32_t q = (uint32_t)(((uint64_t)y * T.magic[t] + T.hmagic[t]) >> 32);
-    return q * T.negm[t] + y;                                   // y - q m_t (mod 2^32)
+    const float f = __fsub_rn(__uint_as_float(y), 8388608.0f);                      // y, exact
+    const uint32_t qb = __float_as_uint(__fmaf_rn(f, T.invm[t], 12582912.0f));      // 1.5 2^23 + q
+    return qb * T.negm[t] + y;                                  // low byte: y - q m_t (mod 256)
 }
 
 // ---------------------------------------------------------------------------
@@ -940,8 +954,11 @@ __global__ void cols_finalize_kernel(const int32_t* __restrict__ Ec, const unsig
 // sectors, no partial-sector read-modify-write in L2).
 // resident CTAs per SM the register budget allows: the kernel is latency-bound
 // on its loads, so occupancy matters (4 CTAs = 64 registers; N > 14 needs 80)
+#ifndef OZ2_COLS_MINB
+#define OZ2_COLS_MINB 4          // resident CTAs per SM (register cap 64)
+#endif
 template <int NM, int BW, int CR_ROWS>
-__global__ void __launch_bounds__(256, UseImmaCols<BW>::value ? 3 : 1)
+__global__ void __launch_bounds__(256, UseImmaCols<BW>::value ? 3 : OZ2_COLS_MINB)
 cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t ldb,
                      const int32_t* __restrict__ f, int8_t* __restrict__ out, int64_t ldr, int64_t pstride) {
     constexpr int WORDS = BwWords<BW>::value;
@@ -954,19 +971,26 @@ cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t
     const int64_t j = j0 + lane;
     const uint64_t pol = l2_evict_first();
     {
-        const int e = j < n ? f[j] : 0;
-        const bool live = j < n && e != OZ2_EXP_NONFINITE_DEV;     // sentinel column: x = 0
-        double s1, s2;
-        pow2_factors(e, s1, s2);
+        // the element loads do not wait for the exponent: they are issued with the
+        // load of f[j] (one memory round trip per CTA, not two), and a sentinel
+        // column's values are replaced by zeros afterwards
         const int64_t lw = l0 + warp * CR_RPT;
         const double* src = B + lw * ldb + j;
         double a[CR_RPT];
-        if (live && lw + CR_RPT <= k) {
+        if (j < n && lw + CR_RPT <= k) {
             #pragma unroll
             for (int q = 0; q < CR_RPT; q++) { a[q] = ld1_hint(src, pol); src += ldb; }
         } else {
             #pragma unroll
-            for (int q = 0; q < CR_RPT; q++) a[q] = (live && lw + q < k) ? ld1_hint(src + q * ldb, pol) : 0.0;
+            for (int q = 0; q < CR_RPT; q++) a[q] = (j < n && lw + q < k) ? ld1_hint(src + q * ldb, pol) : 0.0;
+        }
+        const int e = j < n ? __ldg(f + j) : 0;
+        const bool live = j < n && e != OZ2_EXP_NONFINITE_DEV;     // sentinel column: x = 0
+        double s1, s2;
+        pow2_factors(e, s1, s2);
+        if (!live) {
+            #pragma unroll
+            for (int q = 0; q < CR_RPT; q++) a[q] = 0.0;
         }
         // 16-byte chunks XOR-swizzled within the segment (conflict-free stores and loads)
         auto put = [&](int t, const uint32_t (&pw)[CR_RPT / 4]) {

@@ -129,6 +129,9 @@ int oz2_build_tables(Oz2Table tabs[OZ2_MAX_MODULI + 1]) {
             T.G63[t] = (uint32_t)((m - pow2_mod(63, m)) % m);
             T.G95[t] = (uint32_t)((m - pow2_mod(95, m)) % m);
             T.hmagic[t] = (uint64_t)T.h[t] * (uint64_t)T.magic[t];
+            T.G63f[t] = 0x4B000000u + T.G63[t];
+            T.G95f[t] = 0x4B000000u + T.G95[t];
+            T.invm[t] = 1.0f / (float)m;                  // correctly rounded (IEEE division)
             uint32_t rem;
             Nat Mt = divmod_small(M, (uint32_t)m, &rem);
             if (rem) return 1;
