@@ -85,6 +85,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         :: "r"(bar), "r"(parity) : "memory");
 }
 
+// non-blocking: has the phase with this parity completed?
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    return done != 0;
+}
+
 // ---------------------------------------------------------------------------
 // TMA (cp.async.bulk.tensor) 3-D tile load, completion on an mbarrier
 // ---------------------------------------------------------------------------
