@@ -31,6 +31,28 @@ __device__ __forceinline__ uint32_t reduce_line7(int32_t c, int t) {
     return q * T.negm[t] + y;                                   // y - q m_t (mod 2^32)
 }
 
+// line 7 for the GEMM drain, with the floor on the full-rate FP32 pipe instead
+// of a quarter-rate IMAD.HI (tools/mb/op_rates.cu): c' = hi 2^18 + lo (hi
+// signed, |hi| <= 2^13; lo in [0, 2^18)); L = lo | 0x4B200000 is the bits of the
+// binary32 2^23 + 2^21 + lo; y' = hi k18s + L + K with k18s == 2^18 (mod m_t),
+// |k18s| <= m_t / 2, and K = -8 k18s (so that the 2^21 offset cancels mod m_t)
+// is the bits of 2^23 + y with y == c' (mod m_t), 2^20 <= y < 2^22.2.
+// f = y - h_t exactly, one FMA f RN(1/m_t) + 1.5 2^23 rounds to 1.5 2^23 +
+// floor(y / m_t) (|f| < 2^22.2: the product's error is < 0.27 / m_t, and
+// (y - h_t) / m_t lies at least 1 / (2 m_t) from every half-integer), and the
+// low byte of y' + qb (2^32 - m_t) is c'' (the bit offsets 0x4B000000 and
+// 0x4B400000 m_t vanish mod 256).  Odd m_t only (m_1 = 256: the low byte of c').
+// The upper bytes of the result are not the residue.
+template <int NM>
+__device__ __forceinline__ uint32_t reduce_line7_lowbyte(int32_t c, int t) {
+    const Oz2Table& T = c_tab[NM];
+    const uint32_t L = ((uint32_t)c & 0x3ffffu) | 0x4B200000u;
+    const uint32_t y = (uint32_t)((c >> 18) * T.k18s[t]) + L + T.k18k[t];
+    const float f = __fsub_rn(__uint_as_float(y), T.h23f[t]);                    // y - h_t, exact
+    const uint32_t qb = __float_as_uint(__fmaf_rn(f, T.invm[t], 12582912.0f));
+    return qb * T.negm[t] + y;
+}
+
 // ---------------------------------------------------------------------------
 // multi-word (32-bit) two's-complement integers, PTX carry chains
 // ---------------------------------------------------------------------------

@@ -196,8 +196,12 @@ __device__ __forceinline__ uint32_t add_mod_bytes(uint32_t a, uint32_t b, uint32
 }
 
 // 32 reduced residues (bytes) of one modulus -> 8 words
+#ifndef OZ2_LINE7_FP32
+#define OZ2_LINE7_FP32 1            // line 7 with the floor on the FP32 pipe (0: IMAD.HI magic multiply)
+#endif
 template <int NM>
 __device__ __forceinline__ void reduce32(const uint32_t (&v)[32], int t, uint32_t (&w)[8]) {
+#if !OZ2_LINE7_FP32
     #pragma unroll
     for (int q = 0; q < 8; q++) {
         const uint32_t r0 = reduce_line7<NM>((int32_t)v[4 * q + 0], t);
@@ -206,6 +210,19 @@ __device__ __forceinline__ void reduce32(const uint32_t (&v)[32], int t, uint32_
         const uint32_t r3 = reduce_line7<NM>((int32_t)v[4 * q + 3], t);
         w[q] = r3 * 16777216u + (r2 * 65536u + (r1 * 256u + r0));     // bytes < 256: three IMADs
     }
+    return;
+#endif
+    if (t == 0) {                                         // m_1 = 256: the low bytes of c' (warp-uniform)
+        #pragma unroll
+        for (int q = 0; q < 8; q++) w[q] = pack_lo_bytes(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        return;
+    }
+    #pragma unroll
+    for (int q = 0; q < 8; q++)                           // low bytes only: PRMT packing on the ALU pipe
+        w[q] = pack_lo_bytes(reduce_line7_lowbyte<NM>((int32_t)v[4 * q + 0], t),
+                             reduce_line7_lowbyte<NM>((int32_t)v[4 * q + 1], t),
+                             reduce_line7_lowbyte<NM>((int32_t)v[4 * q + 2], t),
+                             reduce_line7_lowbyte<NM>((int32_t)v[4 * q + 3], t));
 }
 
 // lines 8-10 for this thread's row and 8 columns [col0, col0 + 8) of a finished
@@ -629,24 +646,27 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             }
                         }
                     }
-                } else if (last && t == NM - 1) {                 // the tile's N residues are complete
-                    // one tile awaits lines 8-10 at a time (two scratch slots): finish
-                    // the previous one, then queue this one
-                    if (pend && !p.exp_no_crt) while (next_sl < SLICES) run_slice(next_sl++);
-                    pend = true; ptm = tm; ptn = tn; pslot = slot; slot ^= 1; next_sl = 0;
-                }
-                // lines 8-10 of the queued tile in this warp's idle time, one 8-column
-                // slice at a time, until the next unit's accumulators are ready: the
-                // TMEM drain (line 7) never waits behind CRT work, so the MMAs of the
-                // next unit are not held back (round 2: the fixed per-unit share of
-                // slices delayed the drain -- MMA waits on TMEM were 23 % of the GEMM
-                // at 4096^3, 7 % at 16384^3)
-                if (pend && !p.exp_no_crt && !p.res_out) {
+                } else {
+                    // lines 8-10 of the queued tile in this warp's idle time, one 8-column
+                    // slice at a time, until the next unit's accumulators are ready: the
+                    // TMEM drain (line 7) never waits behind CRT work, so the MMAs of the
+                    // next unit are not held back (round 2: the fixed per-unit share of
+                    // slices delayed the drain).  When this unit completes a tile (its N
+                    // residues are in scratch), the queued tile is finished first -- one
+                    // tile awaits lines 8-10 at a time, two scratch slots -- and this one
+                    // is queued.  One call site of run_slice (code size, registers).
+                    bool complete = last && t == NM - 1;
                     const int nacc = NH == 1 ? (acc + 1) & 1 : 0;
                     const uint32_t naph = NH == 1 ? (acc == 1 ? aph ^ 1 : aph) : aph ^ 1;
-                    while (next_sl < SLICES && !mbar_test(smem_u32(&s.tfull[nacc]), naph)) {
-                        if (p.crt_prefetch && next_sl + 1 < SLICES) prefetch_slice(next_sl + 1);
-                        run_slice(next_sl++);
+                    for (;;) {
+                        while (pend && !p.exp_no_crt && next_sl < SLICES &&
+                               (complete || !mbar_test(smem_u32(&s.tfull[nacc]), naph))) {
+                            if (p.crt_prefetch && next_sl + 1 < SLICES) prefetch_slice(next_sl + 1);
+                            run_slice(next_sl++);
+                        }
+                        if (!complete) break;
+                        pend = true; ptm = tm; ptn = tn; pslot = slot; slot ^= 1; next_sl = 0;
+                        complete = false;
                     }
                 }
             }

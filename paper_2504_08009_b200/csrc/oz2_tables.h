@@ -45,6 +45,10 @@ struct Oz2Table {
     uint32_t G63f[OZ2_MAX_MODULI];    // 0x4B000000 + G63
     uint32_t G95f[OZ2_MAX_MODULI];    // 0x4B000000 + G95
     float invm[OZ2_MAX_MODULI];       // RN_binary32(1 / m_t)
+    // GEMM drain (line 7) on the FP32 pipe: c' = hi 2^18 + lo
+    int32_t k18s[OZ2_MAX_MODULI];     // 2^18 mod m_t, |k18s| <= m_t / 2
+    uint32_t k18k[OZ2_MAX_MODULI];    // -8 k18s mod 2^32 (cancels the 2^21 offset of the lo bits)
+    float h23f[OZ2_MAX_MODULI];       // 2^23 + (m_t - 1) / 2 (odd m_t; exact in binary32)
 };
 
 // Fill tabs[2..20]; tabs[0], tabs[1] are zeroed.  Returns 0 on success.

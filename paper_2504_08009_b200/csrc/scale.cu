@@ -997,9 +997,13 @@ cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t
             uint8_t* seg = sres + (size_t)(t * 32 + lane) * CR_ROWS;
             if constexpr (CR_RPT == 16) {
                 *reinterpret_cast<uint4*>(seg + ((warp ^ (lane & 7)) * 16)) = make_uint4(pw[0], pw[1], pw[2], pw[3]);
-            } else {                                   // 8 bytes: half of piece (warp >> 1)
-                const int pc = (warp >> 1) ^ (lane & 3);
-                *reinterpret_cast<uint2*>(seg + pc * 16 + (warp & 1) * 8) = make_uint2(pw[0], pw[1]);
+            } else {
+                // 8 bytes (rows 8 warp .. 8 warp + 7) at the 8-byte slot warp ^ ((lane >> 1) & 7):
+                // the 16 lanes of each parity hit 8 distinct slots, 2 lanes per bank
+                // pair (2 wavefronts, the minimum for 256 bytes; the chunk-level XOR
+                // of round 1 gave 8-way conflicts)
+                const int slot = warp ^ ((lane >> 1) & 7);
+                *reinterpret_cast<uint2*>(seg + slot * 8) = make_uint2(pw[0], pw[1]);
             }
         };
         const bool one = __all_sync(0xffffffffu, s2 == 1.0);    // one multiplication (normal scales)
@@ -1014,14 +1018,29 @@ cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t
     const int t0 = (threadIdx.x / NPC) >> 5;
     const int64_t l = l0 + 16 * piece;
     if (l >= ldr || j0 + col >= n) return;                   // ldr % 16 == 0: pieces are whole
-    const uint8_t* sp = sres + (size_t)(t0 * 32 + col) * CR_ROWS + ((piece ^ (col & (NPC - 1))) * 16);
     int8_t* gp = out + (int64_t)t0 * pstride + (j0 + col) * ldr + l;
     const int64_t gstep = (int64_t)TSTEP * pstride;
-    #pragma unroll 4
-    for (int t = t0; t < NM; t += TSTEP) {
-        *reinterpret_cast<uint4*>(gp) = *reinterpret_cast<const uint4*>(sp);
-        sp += TSTEP * 32 * CR_ROWS;
-        gp += gstep;
+    if constexpr (CR_RPT == 16) {
+        const uint8_t* sp = sres + (size_t)(t0 * 32 + col) * CR_ROWS + ((piece ^ (col & (NPC - 1))) * 16);
+        #pragma unroll 4
+        for (int t = t0; t < NM; t += TSTEP) {
+            *reinterpret_cast<uint4*>(gp) = *reinterpret_cast<const uint4*>(sp);
+            sp += TSTEP * 32 * CR_ROWS;
+            gp += gstep;
+        }
+    } else {
+        // piece = rows 16 piece .. + 15 = the slots of warps 2 piece, 2 piece + 1
+        const int sw = (col >> 1) & 7;
+        const uint8_t* sp0 = sres + (size_t)(t0 * 32 + col) * CR_ROWS + (((2 * piece) ^ sw) * 8);
+        const uint8_t* sp1 = sres + (size_t)(t0 * 32 + col) * CR_ROWS + (((2 * piece + 1) ^ sw) * 8);
+        #pragma unroll 4
+        for (int t = t0; t < NM; t += TSTEP) {
+            const uint2 lo = *reinterpret_cast<const uint2*>(sp0), hi = *reinterpret_cast<const uint2*>(sp1);
+            *reinterpret_cast<uint4*>(gp) = make_uint4(lo.x, lo.y, hi.x, hi.y);
+            sp0 += TSTEP * 32 * CR_ROWS;
+            sp1 += TSTEP * 32 * CR_ROWS;
+            gp += gstep;
+        }
     }
 }
 

@@ -132,6 +132,12 @@ int oz2_build_tables(Oz2Table tabs[OZ2_MAX_MODULI + 1]) {
             T.G63f[t] = 0x4B000000u + T.G63[t];
             T.G95f[t] = 0x4B000000u + T.G95[t];
             T.invm[t] = 1.0f / (float)m;                  // correctly rounded (IEEE division)
+            {
+                const int64_t k18 = (int64_t)pow2_mod(18, m);
+                T.k18s[t] = (int32_t)(2 * k18 > m ? k18 - m : k18);
+                T.k18k[t] = (uint32_t)(-8 * (int64_t)T.k18s[t]);
+                T.h23f[t] = 8388608.0f + (float)((m - 1) / 2);
+            }
             uint32_t rem;
             Nat Mt = divmod_small(M, (uint32_t)m, &rem);
             if (rem) return 1;
