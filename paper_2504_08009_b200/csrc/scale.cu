@@ -782,10 +782,10 @@ __device__ void row_residues_imma(const double* __restrict__ X, int64_t k, int e
 // ---------------------------------------------------------------------------
 // what: 1 = exponents, 2 = residues (given e), 3 = both
 #ifndef OZ2_ROW_MINB
-#define OZ2_ROW_MINB 3          // resident 256-thread row CTAs per SM the register budget allows
+#define OZ2_ROW_MINB 4          // resident 256-thread row CTAs per SM for N <= 16 (64 registers; A/B round 2: 1.58 -> 1.55 ms vs 3); 96-bit inputs (N > 16) keep 3
 #endif
 template <int NM, int BW, int MODE, int THREADS>
-__global__ void __launch_bounds__(THREADS, THREADS == 256 ? OZ2_ROW_MINB : 1)
+__global__ void __launch_bounds__(THREADS, THREADS == 256 ? (NM <= 16 ? OZ2_ROW_MINB : 3) : 1)
 rows_kernel(const double* __restrict__ A, int64_t m, int64_t k, int64_t lda, int what, int kstar,
             int32_t* __restrict__ e_io, int8_t* __restrict__ res, int64_t ldr, int64_t pstride) {
     constexpr int WORDS = BwWords<BW>::value;
@@ -954,8 +954,11 @@ __global__ void cols_finalize_kernel(const int32_t* __restrict__ Ec, const unsig
 // sectors, no partial-sector read-modify-write in L2).
 // resident CTAs per SM the register budget allows: the kernel is latency-bound
 // on its loads, so occupancy matters (4 CTAs = 64 registers; N > 14 needs 80)
+#ifndef OZ2_CR_ROWS
+#define OZ2_CR_ROWS 128          // rows of B per column-residue CTA, 16 per thread (A/B round 2: 1.56 -> 1.33 ms vs 64)
+#endif
 #ifndef OZ2_COLS_MINB
-#define OZ2_COLS_MINB 4          // resident CTAs per SM (register cap 64)
+#define OZ2_COLS_MINB 3          // resident CTAs per SM (register cap 85; 16 loads in flight per thread)
 #endif
 template <int NM, int BW, int CR_ROWS>
 __global__ void __launch_bounds__(256, UseImmaCols<BW>::value ? 3 : OZ2_COLS_MINB)
@@ -1098,7 +1101,7 @@ static void launch_rows_nm(const double* A, int64_t m, int64_t k, int64_t lda, i
 template <int NM, int BW>
 static void launch_cols_res_bw(const double* B, int64_t k, int64_t n, int64_t ldb, const int32_t* f,
                                int8_t* res, int64_t ldr, int64_t pstride, cudaStream_t st) {
-    constexpr int ROWS = 64;
+    constexpr int ROWS = OZ2_CR_ROWS;
     dim3 grid((unsigned)((n + 31) / 32), (unsigned)((k + ROWS - 1) / ROWS)), block(256);
     const size_t smem = (size_t)NM * 32 * ROWS;
     static bool attr_done[64] = {false};
