@@ -420,6 +420,9 @@ __device__ __forceinline__ void st_cs_v4(void* a, uint32_t x, uint32_t y, uint32
 //   S_c = sum u^2, u = ceil(|x| 2^(15-E_c)) (>= 1 for x != 0) in FP64: every u
 //   <= 2^16, so u^2 <= 2^32 and a 256-term sum <= 2^40 are exact.
 // ---------------------------------------------------------------------------
+#ifndef OZ2_ROW_CU
+#define OZ2_ROW_CU 2             // KC-chunks per warp step in the rows' pass 1 (loads in flight)
+#endif
 constexpr uint64_t ABS_MASK = 0x7fffffffffffffffull;
 constexpr uint64_t INF_BITS = 0x7ff0000000000000ull;
 
@@ -510,7 +513,7 @@ __device__ void row_chunk_stats(const double* __restrict__ X, int64_t k, RowSmem
     // flight before the first reduction.  The chunk maximum comes from the high
     // words of |x| (exponent field; >= 0x7ff00000 flags Inf/NaN); a chunk whose
     // maximum is subnormal or zero takes the full 64-bit patterns (warp-uniform)
-    constexpr int CU = 2, VP = KC / 32;
+    constexpr int CU = OZ2_ROW_CU, VP = KC / 32;
     for (int c0 = warp; c0 < nch; c0 += CU * nwarps) {
         double v[CU][VP];
         #pragma unroll
