@@ -51,6 +51,9 @@ constexpr int BN = 256;             // UMMA N (columns of one accumulator half)
 #ifndef OZ2_EARLY_RELEASE
 #define OZ2_EARLY_RELEASE 1         // free a TMEM half before reducing its last chunk (A/B: +0.3 %, 86 GPU tests pass)
 #endif
+#ifndef OZ2_DRAIN4
+#define OZ2_DRAIN4 1                // TMEM drain with four 32-column chunks in flight (NH = 2)
+#endif
 #ifndef OZ2_CRT_UNROLL
 #define OZ2_CRT_UNROLL 2            // both column pairs of a CRT slice inline (measured: 16384^3 -1 %, k = 256 -12 %, 4096^3 +3 %; 1: one after the other)
 #endif
@@ -594,6 +597,43 @@ modmul_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 const bool quad_live = tm * C_::TILE_M + (int)rank * BM + q * 32 < p.m;
                 uint32_t va[32], vb[32];
                 bool released = false;
+#if OZ2_DRAIN4
+                if constexpr (CH == 8) {
+                  if (quad_live && ch_valid == CH) {
+                    // four chunks in flight (128 registers): TMEM is released after the
+                    // line-7 work of 4 chunks instead of 7 -- the next unit's first MMAs
+                    // wait on this drain (round 2: 7 % of the MMA issuer's cycles at
+                    // 16384^3, 23 % at 4096^3)
+                    uint32_t v0[32], v1[32], v2[32], v3[32], w[8];
+                    const uint32_t tb = tbase + (uint32_t)(half * CH * 32);
+                    const int c0 = half * CH;
+                    auto red_store = [&](const uint32_t (&v)[32], int c) {
+                        reduce32<NM>(v, t, w);
+                        store_residues<NM>(reinterpret_cast<uint4*>(tile_scr + ((size_t)(c * BM + r)) * 32), w, ch, t);
+                    };
+                    tmem_ld_32x32b_x32(tb + 0 * 32, v0); tmem_ld_32x32b_x32(tb + 1 * 32, v1);
+                    tmem_ld_32x32b_x32(tb + 2 * 32, v2); tmem_ld_32x32b_x32(tb + 3 * 32, v3);
+                    tmem_ld_wait_regs(v0); tmem_regs_fence(v1); tmem_regs_fence(v2); tmem_regs_fence(v3);
+                    red_store(v0, c0 + 0); red_store(v1, c0 + 1);
+                    tmem_ld_32x32b_x32(tb + 4 * 32, v0); tmem_ld_32x32b_x32(tb + 5 * 32, v1);
+                    red_store(v2, c0 + 2); red_store(v3, c0 + 3);
+                    tmem_ld_32x32b_x32(tb + 6 * 32, v2); tmem_ld_32x32b_x32(tb + 7 * 32, v3);
+                    tmem_ld_wait_regs(v0); tmem_regs_fence(v1); tmem_regs_fence(v2); tmem_regs_fence(v3);
+                    release(); released = true;              // every TMEM read of this unit is done
+                    red_store(v0, c0 + 4); red_store(v1, c0 + 5); red_store(v2, c0 + 6); red_store(v3, c0 + 7);
+                  } else if (quad_live) {                       // partial tile: the live chunks only
+                    #pragma unroll 1
+                    for (int cc = 0; cc < ch_valid; cc++) {
+                        const int c = half * CH + cc;
+                        uint32_t w[8];
+                        tmem_ld_32x32b_x32(tbase + (uint32_t)(c * 32), va);
+                        tmem_ld_wait_regs(va);
+                        reduce32<NM>(va, t, w);
+                        store_residues<NM>(reinterpret_cast<uint4*>(tile_scr + ((size_t)(c * BM + r)) * 32), w, ch, t);
+                    }
+                  }
+                } else
+#endif
                 if (quad_live && ch_valid == CH) {
                 tmem_ld_32x32b_x32(tbase + (uint32_t)(half * CH * 32), va);
                 #pragma unroll
