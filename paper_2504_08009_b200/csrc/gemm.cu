@@ -112,6 +112,8 @@ struct Params {
     int pf_dist;                    // k-blocks of L2 prefetch ahead of the TMA loads
     int exp_skip_b1;                // experiment only (wrong results): skip the second B half's load
     int exp_no_crt;                 // experiment only (wrong results): skip lines 8-10 (the CRT slices)
+    int exp_crt_mem;                // experiment only (wrong results): 1 = CRT on synthetic residues (no scratch
+                                    //   loads), 2 = CRT without the C stores (results folded into one word)
     int crt_prefetch;               // L2 prefetch of the next unit's CRT slice inputs
     int32_t* cprod;                 // RAW: [N][m][n]
     uint8_t* scratch;               // FUSED: [grid][2 slots][N][BM*BN] uint8 residues
@@ -248,6 +250,10 @@ __device__ __forceinline__ void crt_slice(const Params& p, const uint8_t* tile_s
     uint32_t wt[NM][2];
     #pragma unroll
     for (int tt = 0; tt < NM; tt++) {
+        if (p.exp_crt_mem == 1) {                      // experiment: no scratch traffic
+            wt[tt][0] = (uint32_t)(row * 0x01030507 + tt * 0x11 + c); wt[tt][1] = wt[tt][0] ^ 0x5a5a5a5au;
+            continue;
+        }
         const uint2 x = *reinterpret_cast<const uint2*>(
             tile_scr + (size_t)tt * TILE_BYTES + ((size_t)(c * BM + r)) * 32 + hh * 8);
         wt[tt][0] = x.x; wt[tt][1] = x.y;
@@ -295,6 +301,10 @@ __device__ __forceinline__ void crt_slice(const Params& p, const uint8_t* tile_s
                     if (keep[jj])
                         o[jj] = p.beta == 0.0 ? p.alpha * o[jj] : fma(p.alpha, o[jj], p.beta * crow[j + jj]);
                 }
+            }
+            if (p.exp_crt_mem == 2) {                   // experiment: no C traffic (kept alive by a test)
+                if (__double_as_longlong(o[0]) == 0x7ff0dead12345678ll) crow[j] = o[1];
+                continue;
             }
             if (vec && keep[0] && keep[1]) {
                 *reinterpret_cast<double2*>(crow + j) = make_double2(o[0], o[1]);
@@ -870,6 +880,7 @@ static gemm::Params make_params(int64_t m, int64_t n, int64_t k, int N, int num_
     p.pf_dist = exp_int("OZ2_PF_DIST", 0);       // measured: L2 prefetch slows the GEMM (TMA contention)
     p.exp_skip_b1 = exp_int("OZ2_EXP_SKIP_B1", 0);
     p.exp_no_crt = exp_int("OZ2_EXP_NO_CRT", 0);
+    p.exp_crt_mem = exp_int("OZ2_EXP_CRT_MEM", 0);
     p.crt_prefetch = exp_int("OZ2_CRT_PREFETCH", 0);   // measured: no gain (the slices are issue-latency-bound, not HBM-bound)
     const int tiles = p.num_tm * p.num_tn;
     const int nclusters = std::max(1, std::min(num_sms / cg, max_clusters(cg, nh)));
