@@ -784,11 +784,14 @@ __device__ void row_residues_imma(const double* __restrict__ X, int64_t k, int e
 // Row kernels (A: m x k, row-major, lda); one CTA per row
 // ---------------------------------------------------------------------------
 // what: 1 = exponents, 2 = residues (given e), 3 = both
+#ifndef OZ2_ROW_THREADS
+#define OZ2_ROW_THREADS 256      // threads per row CTA (256 or 512)
+#endif
 #ifndef OZ2_ROW_MINB
 #define OZ2_ROW_MINB 4          // resident 256-thread row CTAs per SM for N <= 16 (64 registers; A/B round 2: 1.58 -> 1.55 ms vs 3); 96-bit inputs (N > 16) keep 3
 #endif
 template <int NM, int BW, int MODE, int THREADS>
-__global__ void __launch_bounds__(THREADS, THREADS == 256 ? (NM <= 16 ? OZ2_ROW_MINB : 3) : 1)
+__global__ void __launch_bounds__(THREADS, (THREADS == 256 ? (NM <= 16 ? OZ2_ROW_MINB : 3) : (NM <= 16 ? 2 : 1)))
 rows_kernel(const double* __restrict__ A, int64_t m, int64_t k, int64_t lda, int what, int kstar,
             int32_t* __restrict__ e_io, int8_t* __restrict__ res, int64_t ldr, int64_t pstride) {
     constexpr int WORDS = BwWords<BW>::value;
@@ -1085,9 +1088,9 @@ static void launch_rows_bw(const double* A, int64_t m, int64_t k, int64_t lda, i
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         g = std::min<int64_t>(m, (int64_t)sms * per_sm);
     }
-    dim3 grid((unsigned)g), block(256);
+    dim3 grid((unsigned)g), block(OZ2_ROW_THREADS);
     const size_t smem = row_smem_bytes(k);
-    auto kern = mode == 0 ? rows_kernel<NM, BW, 0, 256> : rows_kernel<NM, BW, 1, 256>;
+    auto kern = mode == 0 ? rows_kernel<NM, BW, 0, OZ2_ROW_THREADS> : rows_kernel<NM, BW, 1, OZ2_ROW_THREADS>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     (kern<<<grid, block, smem, st>>>(A, m, k, lda, what, kstar, e, res, ldr, pstride), count_launch());
 }
