@@ -233,3 +233,20 @@ def test_out_and_device_validation(oz2):
         oz2.dgemm(A, A, 14, out=torch.empty((8, 8), dtype=torch.float64))
     with pytest.raises(ValueError):
         oz2.dgemm_scaled(A, A, torch.zeros(7, dtype=torch.int32), torch.zeros(8, dtype=torch.int32), 14)
+
+
+@pytest.mark.parametrize("shape", [(2, 1), (1, 1)])
+@pytest.mark.parametrize("N", [9, 14, 17])
+def test_alternative_tile_shapes(oz2, oracle, monkeypatch, shape, N):
+    """The env-selectable GEMM shapes other than the default 256 x 512 pair tile:
+    OZ2_CG=2 OZ2_NH=1 (256 x 256 pair tile, TMEM double buffer) and OZ2_CG=1
+    (128 x 256 single-CTA tile), fused epilogue on several tiles with ragged
+    edges, bitwise against the oracle."""
+    cg, nh = shape
+    monkeypatch.setenv("OZ2_CG", str(cg))
+    monkeypatch.setenv("OZ2_NH", str(nh))
+    monkeypatch.setenv("OZ2_UNIT_PARALLEL", "0")
+    A = phi_matrix_np(700, 500, 1.0, seed=700 + N)
+    B = phi_matrix_np(500, 1300, 1.0, seed=800 + N)
+    C = oz2.dgemm(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), N).cpu().numpy()
+    assert_bitwise(C, oracle.dgemm(A, B, N), f"shape cg={cg} nh={nh} N={N}")
