@@ -1018,8 +1018,9 @@ cols_residues_kernel(const double* __restrict__ B, int64_t k, int64_t n, int64_t
                 *reinterpret_cast<uint2*>(seg + slot * 8) = make_uint2(pw[0], pw[1]);
             }
         };
-        const bool one = __all_sync(0xffffffffu, s2 == 1.0);    // one multiplication (normal scales)
-        thread_residues<NM, BW, CR_RPT>(a, s1, one ? 1.0 : s2, put);
+        // one multiplication per element when every lane's scale is a normal number
+        if (__all_sync(0xffffffffu, s2 == 1.0)) thread_residues<NM, BW, CR_RPT>(a, s1, 1.0, put);
+        else thread_residues<NM, BW, CR_RPT>(a, s1, s2, put);
     }
     __syncthreads();
     // write out: NPC threads per (t, col) row segment of CR_ROWS bytes, 16 bytes
