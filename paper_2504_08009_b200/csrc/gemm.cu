@@ -818,9 +818,24 @@ int gemm_bk() { return gemm::BK; }
 int gemm_halves() { return gemm_cta_group() == 2 && env_int("OZ2_NH", 2) == 2 ? 2 : 1; }
 static int gemm_shape() { return gemm_cta_group() * 10 + gemm_halves(); }
 
-// threshold in output tiles below which the unit-parallel path is used
-static int unit_parallel_tiles(int num_sms) {
-    return env_int("OZ2_UNIT_PARALLEL", 1) ? env_int("OZ2_UP_TILES", num_sms / gemm_cta_group()) : 0;
+static int max_clusters(int cg, int nh);
+// the unit-parallel schedule ((tile, modulus) units spread over the clusters,
+// residues to uint8 planes, lines 8-10 in a separate kernel) instead of the
+// fused one (whole tiles per cluster, CRT in the epilogue): below one tile per
+// cluster, and for a few waves of tiles whose last wave is badly filled (the
+// fused schedule's makespan is ceil(tiles / clusters) tiles; measured round 2,
+// N = 14: 3584^3 (98 tiles, 0.66 of 2 waves) 93.5 -> 108.4 TFLOPS, 4608^3 (162,
+// 0.73 of 3) 118.0 -> 123.8; 4096^3 (128, 0.86) and 5120^3 (200, 0.90) stay
+// fused: 124.8 vs 118.6, 144.5 vs 127.2).  OZ2_UP_TILES=t: unit-parallel below t tiles.
+static bool use_unit_parallel(int tiles, int num_sms) {
+    if (!env_int("OZ2_UNIT_PARALLEL", 1)) return false;
+    const int up = env_int("OZ2_UP_TILES", -1);
+    if (up >= 0) return tiles < up;
+    const int cg = gemm_cta_group();
+    const int ncl = std::max(1, std::min(num_sms / cg, max_clusters(cg, gemm_halves())));
+    if (tiles < ncl) return true;
+    const int waves = (tiles + ncl - 1) / ncl;
+    return waves <= 4 && (int64_t)tiles * 5 < (int64_t)waves * ncl * 4;      // wave fill below 0.8
 }
 
 // clusters of the persistent GEMM that can be resident at once on this device
@@ -901,14 +916,14 @@ size_t fused_scratch_bytes(int64_t m, int64_t n, int N, int num_sms) {
     const int cg = gemm_cta_group(), nh = gemm_halves();
     gemm::Params p = make_params(m, n, 1, N, num_sms, cg, nh, &grid);
     const int tiles = p.num_tm * p.num_tn, ncl_max = std::min(num_sms / cg, max_clusters(cg, nh));
-    if (tiles < unit_parallel_tiles(num_sms)) grid = std::max(grid, std::min(tiles * N, ncl_max) * cg);   // unit-parallel
+    if (use_unit_parallel(tiles, num_sms)) grid = std::max(grid, std::min(tiles * N, ncl_max) * cg);   // unit-parallel
     return (size_t)grid * 2 * N * gemm::BM * gemm::BN * nh;
 }
 
 bool gemm_unit_parallel(int64_t m, int64_t n, int num_sms) {
     int grid;
     gemm::Params p = make_params(m, n, 1, 2, num_sms, gemm_cta_group(), gemm_halves(), &grid);
-    return p.num_tm * p.num_tn < unit_parallel_tiles(num_sms);
+    return use_unit_parallel(p.num_tm * p.num_tn, num_sms);
 }
 
 int launch_modmul(const CUtensorMap* tmA, const CUtensorMap* tmB, int64_t m, int64_t n, int64_t k,
@@ -932,7 +947,7 @@ int launch_modmul_residues(const CUtensorMap* tmA, const CUtensorMap* tmB, int64
         // fewer tiles than clusters: spread the (tile, modulus) units instead
         const int tiles = p.num_tm * p.num_tn,
                   ncl_max = std::min(num_sms / gemm_cta_group(), max_clusters(gemm_cta_group(), gemm_halves()));
-        if (tiles < unit_parallel_tiles(num_sms)) {
+        if (use_unit_parallel(tiles, num_sms)) {
             p.unit_parallel = 1;
             grid = std::min(tiles * N, ncl_max) * gemm_cta_group();
             const int ncl = grid / gemm_cta_group();

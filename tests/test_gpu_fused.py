@@ -48,10 +48,12 @@ def _fused_shape_ok(m, n):
 
 
 @pytest.mark.parametrize("N", list(range(2, 21)))
-def test_fused_every_N(oz2, oracle, N):
-    """80 pair tiles (>= 74: the fused epilogue), ragged n = 3900 (a partial
-    last tile: 316 of 512 columns) and ragged k = 300 (3 k-blocks, the last
-    partial), full matrix bitwise for every N."""
+def test_fused_every_N(oz2, oracle, monkeypatch, N):
+    """80 pair tiles on the fused epilogue (OZ2_UNIT_PARALLEL=0: the default
+    schedule picks unit-parallel for a badly filled second wave), ragged n = 3900
+    (a partial last tile: 316 of 512 columns) and ragged k = 300 (3 k-blocks, the
+    last partial), full matrix bitwise for every N."""
+    monkeypatch.setenv("OZ2_UNIT_PARALLEL", "0")
     m, n, k = 2560, 3900, 300
     assert _fused_shape_ok(m, n)
     A = phi_matrix_np(m, k, 1.0, seed=300 + N)
@@ -250,3 +252,17 @@ def test_alternative_tile_shapes(oz2, oracle, monkeypatch, shape, N):
     B = phi_matrix_np(500, 1300, 1.0, seed=800 + N)
     C = oz2.dgemm(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), N).cpu().numpy()
     assert_bitwise(C, oracle.dgemm(A, B, N), f"shape cg={cg} nh={nh} N={N}")
+
+
+@pytest.mark.parametrize("N", [8, 14, 20])
+def test_unit_parallel_midsize_default(oz2, oracle, N):
+    """The default schedule on 98 pair tiles (3584 x 3584 output: a 0.66-full
+    second wave) takes the unit-parallel path (units spread, lines 8-10 in the
+    CRT kernel); full matrix bitwise with k = 257."""
+    m = n = 3584
+    k = 257
+    assert oz2.lib().oz2_version() > 0
+    A = phi_matrix_np(m, k, 1.0, seed=900 + N)
+    B = phi_matrix_np(k, n, 1.0, seed=950 + N)
+    C = oz2.dgemm(torch.from_numpy(A).to(DEV), torch.from_numpy(B).to(DEV), N).cpu().numpy()
+    assert_bitwise(C, oracle.dgemm(A, B, N), f"unit-parallel (default) N={N}")
