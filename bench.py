@@ -268,6 +268,11 @@ def main():
         # --dist-backend gloo: two ranks on ONE GPU (a functional check of the
         # multi-GPU path on a 1-GPU box; NCCL refuses duplicate devices)
         if args.dist_backend == "nccl":
+            # NCCL's init log (communicator size, NVLS / NVLink transport) goes to
+            # stderr so the multi-GPU run's topology is observable; the JSON line
+            # on stdout is unaffected
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
@@ -433,6 +438,10 @@ def main():
             "n_scaled_roofline_frac": value / world / (4500.0 / N),
             # counted: oz2_kernel_launches() across the timed region (rank 0's library)
             "gpu_launches": int(launches),
+            "comm": ({"backend": dist.get_backend(), "nranks": dist.get_world_size(),
+                      "nccl_version": ".".join(str(x) for x in torch.cuda.nccl.version())
+                      if dist.get_backend() == "nccl" else None}
+                     if world > 1 and dist.is_initialized() else None),
             "clocks": clk.summary()}
 
     # e2e: same metric through the C ABI with host buffers (pinned), copies timed
